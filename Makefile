@@ -1,0 +1,24 @@
+# libhybrid_cuda.so: sm_100a kernels + C ABI (include/hybrid_cuda.h), built in-tree so the
+# .so travels to the GPU box with gpurun.  `make oracle` builds the CPU checker (tests only).
+NVCC ?= /usr/local/cuda/bin/nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 -Xptxas -v -cudart static
+PKG := paper_2005_05371_b200
+SRCS := $(PKG)/csrc/amf.cu $(PKG)/csrc/wiener.cu $(PKG)/csrc/capi.cu $(PKG)/csrc/phantom.cpp
+HDRS := $(PKG)/csrc/hyb_internal.cuh include/hybrid_cuda.h
+LIB := $(PKG)/libhybrid_cuda.so
+
+all: $(LIB) oracle
+
+$(LIB): $(SRCS) $(HDRS)
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRCS) 2> build_ptxas.log || (cat build_ptxas.log; exit 1)
+	@grep -E "registers|spill" build_ptxas.log | sed 's/^ptxas info    : //' | head -40
+
+oracle:
+	$(MAKE) -C oracle --no-print-directory
+
+clean:
+	rm -f $(LIB) build_ptxas.log
+	$(MAKE) -C oracle clean
+
+.PHONY: all oracle clean

@@ -1,0 +1,189 @@
+"""CPU checker for the hybrid AMF + W1 Wiener path -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / ``--impl reference`` legs may
+import this package, and only as the checker or the CPU baseline, never as the product path.
+
+* ``liboracle.so`` (hyb_oracle.c): C restatement of detail::adaptive_median_rows (reference
+  proj/src/adaptive_median.cpp:123-215) on uint8 and of the W1 local Wiener (
+  no reference implementation exists -> W1 parity is "unpinned" w.r.t. the reference).
+* ``_ref/libref.so``: the UNMODIFIED reference sources compiled from /root/reference by
+  oracle/Makefile plus ref_shim.cpp.  Pins the AMF restatement and serves as the CPU baseline.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, c_double, c_int, c_int64, c_size_t, c_uint64, c_void_p
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libref.so")
+
+
+def _load_oracle():
+    lib = ctypes.CDLL(ORACLE_SO)
+    P = c_void_p
+    lib.hyb_oracle_amf_u8.argtypes = [P, c_size_t, c_int, c_int, c_int, c_int, c_int, P, c_size_t, P, c_size_t]
+    lib.hyb_oracle_wiener_stats_u8.argtypes = [P, c_size_t, c_int, c_int, c_int, c_int, c_int, POINTER(c_int64)]
+    lib.hyb_oracle_wiener_gain_u8.argtypes = [P, c_size_t, c_int, c_int, c_int, c_int, c_int, c_int64, c_int64,
+                                              P, c_size_t]
+    lib.hyb_oracle_hybrid_u8.argtypes = [P, c_size_t, c_int, c_int, c_int, c_int, P, P, c_size_t, POINTER(c_int64)]
+    lib.hyb_oracle_validate_smax.argtypes = [c_int]
+    return lib
+
+
+_lib = None
+_ref = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(ORACLE_SO):
+            raise ImportError(f"{ORACLE_SO} missing: run `make -C oracle`")
+        _lib = _load_oracle()
+    return _lib
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_SO)
+
+
+def ref():
+    """The reference itself (compiled in oracle/_ref)."""
+    global _ref
+    if _ref is None:
+        if not os.path.exists(REF_SO):
+            raise ImportError(f"{REF_SO} missing: run `make -C oracle` where /root/reference exists")
+        r = ctypes.CDLL(REF_SO)
+        P = c_void_p
+        r.ref_last_error.restype = ctypes.c_char_p
+        r.ref_validate_smax.argtypes = [c_int]
+        r.ref_amf_rows_u8.argtypes = [P, c_size_t, c_int, c_int, c_int, c_int, c_int, P, c_size_t, P, c_size_t]
+        r.ref_amf_parallel_u8.argtypes = [P, c_size_t, c_int, c_int, c_int, c_int, c_int, c_int, P, c_size_t,
+                                          POINTER(c_double)]
+        r.ref_split_bands.argtypes = [c_int, c_int, c_int, c_int, POINTER(c_int)]
+        r.ref_rng_uniform.argtypes = [c_uint64, c_int, POINTER(c_double)]
+        r.ref_rng_normal.argtypes = [c_uint64, c_int, POINTER(c_double)]
+        r.ref_salt_pepper_count.argtypes = [c_int, c_int, c_double, c_double, c_uint64]
+        r.ref_hybrid_baseline.argtypes = [P, c_int, c_int, c_int, c_int, c_int, P, POINTER(c_double),
+                                          POINTER(c_double)]
+        _ref = r
+    return _ref
+
+
+def _u8(a):
+    a = np.ascontiguousarray(a, dtype=np.uint8)
+    return a, a.ctypes.data
+
+
+# ---------------- oracle (C restatement) ----------------
+
+def amf(img, smax, row_begin=0, row_end=None, finalized_at=False):
+    img, p = _u8(img)
+    rows, cols = img.shape
+    row_end = rows if row_end is None else row_end
+    out = np.empty((max(row_end - row_begin, 0), cols), np.uint8)
+    fin = np.empty_like(out) if finalized_at else None
+    st = lib().hyb_oracle_amf_u8(p, cols, rows, cols, row_begin, row_end, smax, out.ctypes.data, cols,
+                                 fin.ctypes.data if fin is not None else None, cols)
+    if st:
+        raise ValueError(f"oracle amf rejected smax={smax} range=[{row_begin},{row_end}) of {rows}")
+    return (out, fin) if finalized_at else out
+
+
+def wiener_stats(f, win, row_begin=0, row_end=None):
+    f, p = _u8(f)
+    rows, cols = f.shape
+    row_end = rows if row_end is None else row_end
+    w = c_int64(0)
+    st = lib().hyb_oracle_wiener_stats_u8(p, cols, rows, cols, row_begin, row_end, win, ctypes.byref(w))
+    if st:
+        raise ValueError("oracle wiener_stats rejected its arguments")
+    return w.value
+
+
+def wiener_gain(f, win, noise_sum, pixel_count, row_begin=0, row_end=None):
+    f, p = _u8(f)
+    rows, cols = f.shape
+    row_end = rows if row_end is None else row_end
+    y = np.empty((row_end - row_begin, cols), np.uint8)
+    st = lib().hyb_oracle_wiener_gain_u8(p, cols, rows, cols, row_begin, row_end, win, noise_sum, pixel_count,
+                                         y.ctypes.data, cols)
+    if st:
+        raise ValueError("oracle wiener_gain rejected its arguments")
+    return y
+
+
+def wiener(f, win):
+    w = wiener_stats(f, win)
+    return wiener_gain(f, win, w, f.shape[0] * f.shape[1]), w
+
+
+def hybrid(g, smax, win):
+    g, p = _u8(g)
+    rows, cols = g.shape
+    work = np.empty_like(g)
+    y = np.empty_like(g)
+    w = c_int64(0)
+    st = lib().hyb_oracle_hybrid_u8(p, cols, rows, cols, smax, win, work.ctypes.data, y.ctypes.data, cols,
+                                    ctypes.byref(w))
+    if st:
+        raise ValueError("oracle hybrid rejected its arguments")
+    return y, w.value
+
+
+# ---------------- the reference itself (oracle/_ref) ----------------
+
+def ref_amf_rows(img, smax, row_begin=0, row_end=None, finalized_at=False):
+    img, p = _u8(img)
+    rows, cols = img.shape
+    row_end = rows if row_end is None else row_end
+    out = np.empty((max(row_end - row_begin, 0), cols), np.uint8)
+    fin = np.empty_like(out) if finalized_at else None
+    st = ref().ref_amf_rows_u8(p, cols, rows, cols, row_begin, row_end, smax, out.ctypes.data, cols,
+                               fin.ctypes.data if fin is not None else None, cols)
+    if st:
+        raise ValueError(ref().ref_last_error().decode())
+    return (out, fin) if finalized_at else out
+
+
+def ref_amf_parallel(img, smax, parts, workers, use_halo=True):
+    img, p = _u8(img)
+    rows, cols = img.shape
+    out = np.empty_like(img)
+    sec = c_double(0)
+    st = ref().ref_amf_parallel_u8(p, cols, rows, cols, smax, parts, workers, int(use_halo), out.ctypes.data,
+                                   cols, ctypes.byref(sec))
+    if st:
+        raise ValueError(ref().ref_last_error().decode())
+    return out, sec.value
+
+
+def ref_split_bands(rows, cols, parts, halo):
+    out = (c_int * (4 * parts))()
+    st = ref().ref_split_bands(rows, cols, parts, halo, out)
+    if st:
+        raise ValueError(ref().ref_last_error().decode())
+    return [tuple(out[4 * i:4 * i + 4]) for i in range(parts)]
+
+
+def ref_rng(seed, n, normal=False):
+    out = (c_double * n)()
+    (ref().ref_rng_normal if normal else ref().ref_rng_uniform)(seed, n, out)
+    return np.frombuffer(out, dtype=np.float64).copy()
+
+
+def ref_hybrid_baseline(g, smax, win, threads):
+    """Reference AMF (adaptive_median_parallel, parts = workers = threads) + W1 oracle on threads."""
+    g, p = _u8(g)
+    rows, cols = g.shape
+    y = np.empty_like(g)
+    ta, tw = c_double(0), c_double(0)
+    st = ref().ref_hybrid_baseline(p, rows, cols, smax, win, threads, y.ctypes.data, ctypes.byref(ta),
+                                   ctypes.byref(tw))
+    if st:
+        raise ValueError(ref().ref_last_error().decode())
+    return y, ta.value, tw.value

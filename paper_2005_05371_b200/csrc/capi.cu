@@ -1,0 +1,596 @@
+// capi.cu -- the extern "C" boundary of libhybrid_cuda (include/hybrid_cuda.h).
+//
+// Host orchestration only: argument validation with the reference's error texts, host/device
+// pointer detection and staging, the strip partitioner (split_bands geometry, reference
+// proj/src/tiling.cpp:23-32) and the exact noise reduction.  All pixel work is in amf.cu and
+// wiener.cu; there is no CPU fallback -- a missing device or a failed launch is an error.
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/hybrid_cuda.h"
+#include "hyb_internal.cuh"
+
+namespace hyb {
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace hyb
+
+namespace {
+
+constexpr int kMaxSmax = 255;  // largest window the shared-memory tile supports
+constexpr int kMaxWin = 63;
+
+struct DevBuf {
+    uint8_t* ptr = nullptr;
+    size_t bytes = 0;
+    cudaError_t ensure(size_t want) {
+        if (want <= bytes) return cudaSuccess;
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        bytes = 0;
+        cudaError_t e = cudaMalloc(&ptr, want);
+        if (e == cudaSuccess) bytes = want;
+        return e;
+    }
+    void release() {
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        bytes = 0;
+    }
+};
+
+struct Status {
+    int code;
+};
+
+}  // namespace
+
+struct hyb_ctx {
+    int device = 0;
+    cudaStream_t own = nullptr;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    DevBuf in, out, fin, f, wsum;      // staging / scratch
+    std::vector<DevBuf> strip_g, strip_f;
+    long long* host_w = nullptr;       // pinned readback of noise sums
+    size_t host_w_n = 0;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+};
+
+namespace {
+
+int fail(hyb_ctx* ctx, int code, const std::string& msg) {
+    if (ctx) ctx->err = msg;
+    return code;
+}
+
+int cuda_fail(hyb_ctx* ctx, cudaError_t e, const char* where) {
+    const int code = (e == cudaErrorMemoryAllocation) ? HYB_ENOMEM : HYB_ECUDA;
+    return fail(ctx, code, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define HYB_CHECK(expr)                                         \
+    do {                                                        \
+        cudaError_t e_ = (expr);                                \
+        if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #expr); \
+    } while (0)
+
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+std::string str_smax(int smax) { return "smax must be an odd integer > 1, got " + std::to_string(smax); }
+
+int check_smax(hyb_ctx* ctx, int smax) {
+    if (smax <= 1 || smax % 2 == 0) return fail(ctx, HYB_EINVAL, str_smax(smax));
+    if (smax > kMaxSmax)
+        return fail(ctx, HYB_EINVAL, "smax " + std::to_string(smax) +
+                                         " exceeds the largest supported window " +
+                                         std::to_string(kMaxSmax));
+    return HYB_OK;
+}
+
+int check_dims(hyb_ctx* ctx, int rows, int cols) {
+    if (rows < 1 || cols < 1)
+        return fail(ctx, HYB_EINVAL, "image dimensions must be at least 1x1, got " +
+                                         std::to_string(rows) + "x" + std::to_string(cols));
+    return HYB_OK;
+}
+
+int check_range(hyb_ctx* ctx, int rows, int b, int e) {
+    if (b < 0 || e > rows || b >= e)
+        return fail(ctx, HYB_EINVAL, "bad row range [" + std::to_string(b) + ", " + std::to_string(e) +
+                                         ") for " + std::to_string(rows) + " rows");
+    return HYB_OK;
+}
+
+int check_win(hyb_ctx* ctx, int win) {
+    if (win < 1 || win % 2 == 0 || win > kMaxWin)
+        return fail(ctx, HYB_EINVAL, "wiener window must be an odd integer in [1, " +
+                                         std::to_string(kMaxWin) + "], got " + std::to_string(win));
+    return HYB_OK;
+}
+
+int check_pitch(hyb_ctx* ctx, size_t pitch, int cols, const char* what) {
+    if (pitch < (size_t)cols)
+        return fail(ctx, HYB_EINVAL, std::string(what) + " pitch " + std::to_string(pitch) +
+                                         " is smaller than cols " + std::to_string(cols));
+    return HYB_OK;
+}
+
+size_t round_pitch(int cols) { return ((size_t)cols + 127) & ~(size_t)127; }
+
+int ensure_host_w(hyb_ctx* ctx, size_t n) {
+    if (ctx->host_w_n >= n) return HYB_OK;
+    if (ctx->host_w) cudaFreeHost(ctx->host_w);
+    ctx->host_w = nullptr;
+    ctx->host_w_n = 0;
+    HYB_CHECK(cudaMallocHost(&ctx->host_w, n * sizeof(long long)));
+    ctx->host_w_n = n;
+    return HYB_OK;
+}
+
+// Copies rows x cols bytes between two pitched buffers (any direction) on the ctx stream.
+cudaError_t copy2d(hyb_ctx* ctx, void* dst, size_t dp, const void* src, size_t sp, int cols, int rows) {
+    return cudaMemcpy2DAsync(dst, dp, src, sp, (size_t)cols, (size_t)rows, cudaMemcpyDefault, ctx->stream);
+}
+
+// Core of hyb_hybrid_u8 on device-resident buffers.
+int hybrid_device(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int cols, int smax,
+                  int win, int parts, uint8_t* y, size_t ypitch, bool timed) {
+    const int rA = (smax - 1) / 2, rW = (win - 1) / 2;
+    HYB_CHECK(ctx->wsum.ensure(sizeof(long long)));
+    unsigned long long* W = reinterpret_cast<unsigned long long*>(ctx->wsum.ptr);
+    const long long P = (long long)rows * cols;
+    if (timed) HYB_CHECK(cudaEventRecord(ctx->ev[0], ctx->stream));
+    if (parts == 1) {
+        const size_t fp = round_pitch(cols);
+        HYB_CHECK(ctx->f.ensure(fp * rows));
+        hyb::Plane a{g, pitch, 0, ctx->f.ptr, fp, 0, rows, cols, 0, rows, 1};
+        HYB_CHECK(hyb::launch_amf(a, smax, nullptr, 0, 0, ctx->stream));
+        if (timed) HYB_CHECK(cudaEventRecord(ctx->ev[1], ctx->stream));
+        HYB_CHECK(cudaMemsetAsync(W, 0, sizeof(long long), ctx->stream));
+        hyb::Plane w{ctx->f.ptr, fp, 0, y, ypitch, 0, rows, cols, 0, rows, 1};
+        HYB_CHECK(hyb::launch_wiener_stats(w, win, W, ctx->stream));
+        HYB_CHECK(hyb::launch_wiener_gain(w, win, reinterpret_cast<const long long*>(W), P, ctx->stream));
+    } else {
+        // split_bands geometry (reference proj/src/tiling.cpp:23-32) with halo rA + rW
+        const int h = rA + rW;
+        ctx->strip_g.resize(parts);
+        ctx->strip_f.resize(parts);
+        struct S { int start, core, hA, hB, fa, fb; };
+        std::vector<S> s(parts);
+        const int base = rows / parts, extra = rows % parts;
+        int start = 0;
+        for (int i = 0; i < parts; ++i) {
+            S& t = s[i];
+            t.start = start;
+            t.core = base + (i < extra ? 1 : 0);
+            t.hA = std::min(h, start);
+            t.hB = std::min(h, rows - start - t.core);
+            t.fa = std::min(rW, start);
+            t.fb = std::min(rW, rows - start - t.core);
+            start += t.core;
+        }
+        const size_t sp = round_pitch(cols);
+        for (int i = 0; i < parts; ++i) {
+            const S& t = s[i];
+            const int grows = t.hA + t.core + t.hB, frows = t.fa + t.core + t.fb;
+            HYB_CHECK(ctx->strip_g[i].ensure(sp * grows));
+            HYB_CHECK(ctx->strip_f[i].ensure(sp * frows));
+            // the strip's own copy of g: core rows plus clamped halo (a real halo copy)
+            HYB_CHECK(copy2d(ctx, ctx->strip_g[i].ptr, sp, g + (size_t)(t.start - t.hA) * pitch, pitch,
+                             cols, grows));
+            hyb::Plane a{ctx->strip_g[i].ptr, sp, 0, ctx->strip_f[i].ptr, sp, 0, grows, cols,
+                         t.hA - t.fa, t.hA + t.core + t.fb, 1};
+            HYB_CHECK(hyb::launch_amf(a, smax, nullptr, 0, 0, ctx->stream));
+        }
+        if (timed) HYB_CHECK(cudaEventRecord(ctx->ev[1], ctx->stream));
+        HYB_CHECK(cudaMemsetAsync(W, 0, sizeof(long long), ctx->stream));
+        for (int i = 0; i < parts; ++i) {
+            const S& t = s[i];
+            hyb::Plane w{ctx->strip_f[i].ptr, sp, 0, nullptr, 0, 0, t.fa + t.core + t.fb, cols, t.fa,
+                         t.fa + t.core, 1};
+            HYB_CHECK(hyb::launch_wiener_stats(w, win, W, ctx->stream));
+        }
+        for (int i = 0; i < parts; ++i) {
+            const S& t = s[i];
+            hyb::Plane w{ctx->strip_f[i].ptr, sp, 0, y + (size_t)t.start * ypitch, ypitch, 0,
+                         t.fa + t.core + t.fb, cols, t.fa, t.fa + t.core, 1};
+            HYB_CHECK(hyb::launch_wiener_gain(w, win, reinterpret_cast<const long long*>(W), P,
+                                              ctx->stream));
+        }
+    }
+    if (timed) HYB_CHECK(cudaEventRecord(ctx->ev[2], ctx->stream));
+    return HYB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+hyb_ctx* hyb_create(int device, int* status) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || device < 0 || device >= n) {
+        if (status) *status = HYB_ECUDA;
+        cudaGetLastError();
+        return nullptr;
+    }
+    hyb_ctx* ctx = new hyb_ctx;
+    ctx->device = device;
+    e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking);
+    for (int i = 0; i < 4 && e == cudaSuccess; ++i) e = cudaEventCreate(&ctx->ev[i]);
+    if (e != cudaSuccess) {
+        if (status) *status = HYB_ECUDA;
+        delete ctx;
+        return nullptr;
+    }
+    ctx->stream = ctx->own;
+    if (status) *status = HYB_OK;
+    return ctx;
+}
+
+int hyb_destroy(hyb_ctx* ctx) {
+    if (!ctx) return HYB_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    ctx->in.release();
+    ctx->out.release();
+    ctx->fin.release();
+    ctx->f.release();
+    ctx->wsum.release();
+    for (auto& b : ctx->strip_g) b.release();
+    for (auto& b : ctx->strip_f) b.release();
+    if (ctx->host_w) cudaFreeHost(ctx->host_w);
+    for (auto& ev : ctx->ev)
+        if (ev) cudaEventDestroy(ev);
+    if (ctx->own) cudaStreamDestroy(ctx->own);
+    delete ctx;
+    return HYB_OK;
+}
+
+int hyb_set_stream(hyb_ctx* ctx, void* stream) {
+    if (!ctx) return HYB_EINVAL;
+    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own;
+    return HYB_OK;
+}
+
+const char* hyb_last_error(const hyb_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int64_t hyb_kernel_launches(const hyb_ctx*) { return hyb::g_launches.load(); }
+
+int hyb_validate_smax(int smax) { return (smax <= 1 || smax % 2 == 0) ? HYB_EINVAL : HYB_OK; }
+
+int hyb_validate_config(int smax, int parts, int workers) {
+    if (hyb_validate_smax(smax)) return HYB_EINVAL;
+    if (parts < 1 || workers < 1) return HYB_EINVAL;
+    return HYB_OK;
+}
+
+int hyb_amf_u8(hyb_ctx* ctx, const uint8_t* src, size_t src_pitch, int rows, int cols,
+               int row_begin, int row_end, int smax, uint8_t* dst, size_t dst_pitch,
+               uint8_t* finalized_at, size_t fin_pitch) {
+    if (!ctx) return HYB_EINVAL;
+    int st;
+    if ((st = check_smax(ctx, smax)) || (st = check_dims(ctx, rows, cols)) ||
+        (st = check_range(ctx, rows, row_begin, row_end)) ||
+        (st = check_pitch(ctx, src_pitch, cols, "src")) || (st = check_pitch(ctx, dst_pitch, cols, "dst")))
+        return st;
+    if (!src || !dst) return fail(ctx, HYB_EINVAL, "null image pointer");
+    if (finalized_at && (st = check_pitch(ctx, fin_pitch, cols, "finalized_at"))) return st;
+    HYB_CHECK(cudaSetDevice(ctx->device));
+    const int orows = row_end - row_begin;
+    const bool dsrc = is_device_ptr(src), ddst = is_device_ptr(dst);
+    const bool dfin = finalized_at && is_device_ptr(finalized_at);
+    const size_t pp = round_pitch(cols);
+    const uint8_t* s = src;
+    size_t sp = src_pitch;
+    if (!dsrc) {
+        HYB_CHECK(ctx->in.ensure(pp * rows));
+        HYB_CHECK(copy2d(ctx, ctx->in.ptr, pp, src, src_pitch, cols, rows));
+        s = ctx->in.ptr;
+        sp = pp;
+    }
+    uint8_t* d = dst;
+    size_t dp = dst_pitch;
+    if (!ddst) {
+        HYB_CHECK(ctx->out.ensure(pp * orows));
+        d = ctx->out.ptr;
+        dp = pp;
+    }
+    uint8_t* fz = finalized_at;
+    size_t fp = fin_pitch;
+    if (finalized_at && !dfin) {
+        HYB_CHECK(ctx->fin.ensure(pp * orows));
+        fz = ctx->fin.ptr;
+        fp = pp;
+    }
+    hyb::Plane p{s, sp, 0, d, dp, 0, rows, cols, row_begin, row_end, 1};
+    HYB_CHECK(hyb::launch_amf(p, smax, fz, fp, 0, ctx->stream));
+    if (!ddst) HYB_CHECK(copy2d(ctx, dst, dst_pitch, d, dp, cols, orows));
+    if (finalized_at && !dfin) HYB_CHECK(copy2d(ctx, finalized_at, fin_pitch, fz, fp, cols, orows));
+    if (!dsrc || !ddst || (finalized_at && !dfin)) HYB_CHECK(cudaStreamSynchronize(ctx->stream));
+    return HYB_OK;
+}
+
+int hyb_amf_batch_u8(hyb_ctx* ctx, const uint8_t* src, size_t src_pitch, size_t src_slice_stride,
+                     int n_slices, int rows, int cols, int smax, uint8_t* dst, size_t dst_pitch,
+                     size_t dst_slice_stride) {
+    if (!ctx) return HYB_EINVAL;
+    int st;
+    if ((st = check_smax(ctx, smax)) || (st = check_dims(ctx, rows, cols)) ||
+        (st = check_pitch(ctx, src_pitch, cols, "src")) || (st = check_pitch(ctx, dst_pitch, cols, "dst")))
+        return st;
+    if (n_slices < 1) return fail(ctx, HYB_EINVAL, "n_slices must be >= 1, got " + std::to_string(n_slices));
+    if (!is_device_ptr(src) || !is_device_ptr(dst))
+        return fail(ctx, HYB_EINVAL, "hyb_amf_batch_u8 takes device buffers");
+    HYB_CHECK(cudaSetDevice(ctx->device));
+    hyb::Plane p{src, src_pitch, src_slice_stride, dst, dst_pitch, dst_slice_stride, rows, cols, 0, rows,
+                 n_slices};
+    HYB_CHECK(hyb::launch_amf(p, smax, nullptr, 0, 0, ctx->stream));
+    return HYB_OK;
+}
+
+int hyb_wiener_stats_u8(hyb_ctx* ctx, const uint8_t* f, size_t pitch, int rows, int cols,
+                        int row_begin, int row_end, int win, int64_t* noise_sum) {
+    if (!ctx) return HYB_EINVAL;
+    int st;
+    if ((st = check_win(ctx, win)) || (st = check_dims(ctx, rows, cols)) ||
+        (st = check_range(ctx, rows, row_begin, row_end)) || (st = check_pitch(ctx, pitch, cols, "f")))
+        return st;
+    if (!f || !noise_sum) return fail(ctx, HYB_EINVAL, "null pointer");
+    HYB_CHECK(cudaSetDevice(ctx->device));
+    const uint8_t* s = f;
+    size_t sp = pitch;
+    const bool df = is_device_ptr(f);
+    if (!df) {
+        sp = round_pitch(cols);
+        HYB_CHECK(ctx->in.ensure(sp * rows));
+        HYB_CHECK(copy2d(ctx, ctx->in.ptr, sp, f, pitch, cols, rows));
+        s = ctx->in.ptr;
+    }
+    hyb::Plane p{s, sp, 0, nullptr, 0, 0, rows, cols, row_begin, row_end, 1};
+    if (is_device_ptr(noise_sum)) {
+        HYB_CHECK(hyb::launch_wiener_stats(p, win, reinterpret_cast<unsigned long long*>(noise_sum),
+                                           ctx->stream));
+        if (!df) HYB_CHECK(cudaStreamSynchronize(ctx->stream));
+        return HYB_OK;
+    }
+    HYB_CHECK(ctx->wsum.ensure(sizeof(long long)));
+    if ((st = ensure_host_w(ctx, 1))) return st;
+    HYB_CHECK(cudaMemsetAsync(ctx->wsum.ptr, 0, sizeof(long long), ctx->stream));
+    HYB_CHECK(hyb::launch_wiener_stats(p, win, reinterpret_cast<unsigned long long*>(ctx->wsum.ptr),
+                                       ctx->stream));
+    HYB_CHECK(cudaMemcpyAsync(ctx->host_w, ctx->wsum.ptr, sizeof(long long), cudaMemcpyDeviceToHost,
+                              ctx->stream));
+    HYB_CHECK(cudaStreamSynchronize(ctx->stream));
+    *noise_sum += ctx->host_w[0];
+    return HYB_OK;
+}
+
+int hyb_wiener_gain_u8(hyb_ctx* ctx, const uint8_t* f, size_t pitch, int rows, int cols,
+                       int row_begin, int row_end, int win, const int64_t* noise_sum,
+                       int64_t pixel_count, uint8_t* y, size_t y_pitch) {
+    if (!ctx) return HYB_EINVAL;
+    int st;
+    if ((st = check_win(ctx, win)) || (st = check_dims(ctx, rows, cols)) ||
+        (st = check_range(ctx, rows, row_begin, row_end)) || (st = check_pitch(ctx, pitch, cols, "f")) ||
+        (st = check_pitch(ctx, y_pitch, cols, "y")))
+        return st;
+    if (!f || !y || !noise_sum) return fail(ctx, HYB_EINVAL, "null pointer");
+    if (pixel_count < 1) return fail(ctx, HYB_EINVAL, "pixel_count must be >= 1");
+    HYB_CHECK(cudaSetDevice(ctx->device));
+    const bool df = is_device_ptr(f), dy = is_device_ptr(y);
+    const size_t pp = round_pitch(cols);
+    const int orows = row_end - row_begin;
+    const uint8_t* s = f;
+    size_t sp = pitch;
+    if (!df) {
+        HYB_CHECK(ctx->in.ensure(pp * rows));
+        HYB_CHECK(copy2d(ctx, ctx->in.ptr, pp, f, pitch, cols, rows));
+        s = ctx->in.ptr;
+        sp = pp;
+    }
+    uint8_t* d = y;
+    size_t dp = y_pitch;
+    if (!dy) {
+        HYB_CHECK(ctx->out.ensure(pp * orows));
+        d = ctx->out.ptr;
+        dp = pp;
+    }
+    const long long* W = reinterpret_cast<const long long*>(noise_sum);
+    if (!is_device_ptr(noise_sum)) {
+        if (*noise_sum < 0) return fail(ctx, HYB_EINVAL, "noise sum must be nonnegative");
+        HYB_CHECK(ctx->wsum.ensure(sizeof(long long)));
+        if ((st = ensure_host_w(ctx, 1))) return st;
+        ctx->host_w[0] = *noise_sum;
+        HYB_CHECK(cudaMemcpyAsync(ctx->wsum.ptr, ctx->host_w, sizeof(long long), cudaMemcpyHostToDevice,
+                                  ctx->stream));
+        W = reinterpret_cast<const long long*>(ctx->wsum.ptr);
+    }
+    hyb::Plane p{s, sp, 0, d, dp, 0, rows, cols, row_begin, row_end, 1};
+    HYB_CHECK(hyb::launch_wiener_gain(p, win, W, pixel_count, ctx->stream));
+    if (!dy) HYB_CHECK(copy2d(ctx, y, y_pitch, d, dp, cols, orows));
+    if (!df || !dy || W != reinterpret_cast<const long long*>(noise_sum))
+        HYB_CHECK(cudaStreamSynchronize(ctx->stream));
+    return HYB_OK;
+}
+
+int hyb_wiener_u8(hyb_ctx* ctx, const uint8_t* f, size_t pitch, int rows, int cols, int win,
+                  uint8_t* y, size_t y_pitch, int64_t* noise_sum_out) {
+    if (!ctx) return HYB_EINVAL;
+    int st;
+    if ((st = check_win(ctx, win)) || (st = check_dims(ctx, rows, cols)) ||
+        (st = check_pitch(ctx, pitch, cols, "f")) || (st = check_pitch(ctx, y_pitch, cols, "y")))
+        return st;
+    if (!f || !y) return fail(ctx, HYB_EINVAL, "null image pointer");
+    HYB_CHECK(cudaSetDevice(ctx->device));
+    const bool df = is_device_ptr(f), dy = is_device_ptr(y);
+    const size_t pp = round_pitch(cols);
+    const uint8_t* s = f;
+    size_t sp = pitch;
+    if (!df) {
+        HYB_CHECK(ctx->in.ensure(pp * rows));
+        HYB_CHECK(copy2d(ctx, ctx->in.ptr, pp, f, pitch, cols, rows));
+        s = ctx->in.ptr;
+        sp = pp;
+    }
+    uint8_t* d = y;
+    size_t dp = y_pitch;
+    if (!dy) {
+        HYB_CHECK(ctx->out.ensure(pp * rows));
+        d = ctx->out.ptr;
+        dp = pp;
+    }
+    HYB_CHECK(ctx->wsum.ensure(sizeof(long long)));
+    unsigned long long* W = reinterpret_cast<unsigned long long*>(ctx->wsum.ptr);
+    HYB_CHECK(cudaMemsetAsync(W, 0, sizeof(long long), ctx->stream));
+    hyb::Plane p{s, sp, 0, d, dp, 0, rows, cols, 0, rows, 1};
+    HYB_CHECK(hyb::launch_wiener_stats(p, win, W, ctx->stream));
+    HYB_CHECK(hyb::launch_wiener_gain(p, win, reinterpret_cast<const long long*>(W), (long long)rows * cols,
+                                      ctx->stream));
+    if (!dy) HYB_CHECK(copy2d(ctx, y, y_pitch, d, dp, cols, rows));
+    if (noise_sum_out) {
+        if ((st = ensure_host_w(ctx, 1))) return st;
+        HYB_CHECK(cudaMemcpyAsync(ctx->host_w, W, sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    if (!df || !dy || noise_sum_out) HYB_CHECK(cudaStreamSynchronize(ctx->stream));
+    if (noise_sum_out) *noise_sum_out = ctx->host_w[0];
+    return HYB_OK;
+}
+
+int hyb_hybrid_u8(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int cols, int smax,
+                  int win, int parts, uint8_t* y, size_t y_pitch, hyb_stats* stats) {
+    if (!ctx) return HYB_EINVAL;
+    int st;
+    if ((st = check_smax(ctx, smax)) || (st = check_win(ctx, win)) || (st = check_dims(ctx, rows, cols)) ||
+        (st = check_pitch(ctx, pitch, cols, "g")) || (st = check_pitch(ctx, y_pitch, cols, "y")))
+        return st;
+    if (parts < 1) return fail(ctx, HYB_EINVAL, "parts must be >= 1, got " + std::to_string(parts));
+    if (parts > rows)
+        return fail(ctx, HYB_EINVAL, "parts " + std::to_string(parts) + " exceeds image rows " +
+                                         std::to_string(rows));
+    if (!g || !y) return fail(ctx, HYB_EINVAL, "null image pointer");
+    HYB_CHECK(cudaSetDevice(ctx->device));
+    const bool dg = is_device_ptr(g), dy = is_device_ptr(y);
+    const size_t pp = round_pitch(cols);
+    const bool timed = stats != nullptr;
+    if (timed) HYB_CHECK(cudaEventRecord(ctx->ev[3], ctx->stream));
+    const uint8_t* s = g;
+    size_t sp = pitch;
+    if (!dg) {
+        HYB_CHECK(ctx->in.ensure(pp * rows));
+        HYB_CHECK(copy2d(ctx, ctx->in.ptr, pp, g, pitch, cols, rows));
+        s = ctx->in.ptr;
+        sp = pp;
+    }
+    uint8_t* d = y;
+    size_t dp = y_pitch;
+    if (!dy) {
+        HYB_CHECK(ctx->out.ensure(pp * rows));
+        d = ctx->out.ptr;
+        dp = pp;
+    }
+    if ((st = hybrid_device(ctx, s, sp, rows, cols, smax, win, parts, d, dp, timed))) return st;
+    if (!dy) HYB_CHECK(copy2d(ctx, y, y_pitch, d, dp, cols, rows));
+    if (timed) {
+        if ((st = ensure_host_w(ctx, 1))) return st;
+        HYB_CHECK(cudaMemcpyAsync(ctx->host_w, ctx->wsum.ptr, sizeof(long long), cudaMemcpyDeviceToHost,
+                                  ctx->stream));
+    }
+    if (!dg || !dy || timed) HYB_CHECK(cudaStreamSynchronize(ctx->stream));
+    if (timed) {
+        float a = 0, w = 0, t = 0;
+        HYB_CHECK(cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]));
+        HYB_CHECK(cudaEventElapsedTime(&w, ctx->ev[1], ctx->ev[2]));
+        HYB_CHECK(cudaEventElapsedTime(&t, ctx->ev[3], ctx->ev[2]));
+        const double n = (double)win * win;
+        stats->noise_sum = ctx->host_w[0];
+        stats->pixel_count = (int64_t)rows * cols;
+        stats->sigma2 = (double)stats->noise_sum / (n * n * (double)stats->pixel_count) / (255.0 * 255.0);
+        stats->t_adaptive = a * 1e-3;
+        stats->t_wiener = w * 1e-3;
+        stats->t_total = t * 1e-3;
+    }
+    return HYB_OK;
+}
+
+int hyb_hybrid_batch_u8(hyb_ctx* ctx, const uint8_t* g, size_t pitch, size_t slice_stride,
+                        int n_slices, int rows, int cols, int smax, int win, uint8_t* y,
+                        size_t y_pitch, size_t y_slice_stride, int64_t* noise_sums) {
+    if (!ctx) return HYB_EINVAL;
+    int st;
+    if ((st = check_smax(ctx, smax)) || (st = check_win(ctx, win)) || (st = check_dims(ctx, rows, cols)) ||
+        (st = check_pitch(ctx, pitch, cols, "g")) || (st = check_pitch(ctx, y_pitch, cols, "y")))
+        return st;
+    if (n_slices < 1) return fail(ctx, HYB_EINVAL, "n_slices must be >= 1, got " + std::to_string(n_slices));
+    if (!g || !y) return fail(ctx, HYB_EINVAL, "null image pointer");
+    if (slice_stride < pitch * rows || y_slice_stride < y_pitch * rows)
+        return fail(ctx, HYB_EINVAL, "slice stride smaller than one slice");
+    HYB_CHECK(cudaSetDevice(ctx->device));
+    const bool dg = is_device_ptr(g), dy = is_device_ptr(y);
+    const size_t pp = round_pitch(cols), ps = pp * rows;
+    const uint8_t* s = g;
+    size_t sp = pitch, ss = slice_stride;
+    if (!dg) {
+        HYB_CHECK(ctx->in.ensure(ps * n_slices));
+        if (slice_stride == pitch * rows) {
+            HYB_CHECK(copy2d(ctx, ctx->in.ptr, pp, g, pitch, cols, rows * n_slices));
+        } else {
+            for (int z = 0; z < n_slices; ++z)
+                HYB_CHECK(copy2d(ctx, ctx->in.ptr + ps * z, pp, g + slice_stride * z, pitch, cols, rows));
+        }
+        s = ctx->in.ptr;
+        sp = pp;
+        ss = ps;
+    }
+    uint8_t* d = y;
+    size_t dp = y_pitch, ds = y_slice_stride;
+    if (!dy) {
+        HYB_CHECK(ctx->out.ensure(ps * n_slices));
+        d = ctx->out.ptr;
+        dp = pp;
+        ds = ps;
+    }
+    HYB_CHECK(ctx->f.ensure(ps * n_slices));
+    HYB_CHECK(ctx->wsum.ensure(sizeof(long long) * n_slices));
+    unsigned long long* W = reinterpret_cast<unsigned long long*>(ctx->wsum.ptr);
+    hyb::Plane a{s, sp, ss, ctx->f.ptr, pp, ps, rows, cols, 0, rows, n_slices};
+    HYB_CHECK(hyb::launch_amf(a, smax, nullptr, 0, 0, ctx->stream));
+    HYB_CHECK(cudaMemsetAsync(W, 0, sizeof(long long) * n_slices, ctx->stream));
+    hyb::Plane w{ctx->f.ptr, pp, ps, d, dp, ds, rows, cols, 0, rows, n_slices};
+    HYB_CHECK(hyb::launch_wiener_stats(w, win, W, ctx->stream));
+    HYB_CHECK(hyb::launch_wiener_gain(w, win, reinterpret_cast<const long long*>(W), (long long)rows * cols,
+                                      ctx->stream));
+    if (!dy) {
+        if (y_slice_stride == y_pitch * rows) {
+            HYB_CHECK(copy2d(ctx, y, y_pitch, d, dp, cols, rows * n_slices));
+        } else {
+            for (int z = 0; z < n_slices; ++z)
+                HYB_CHECK(copy2d(ctx, y + y_slice_stride * z, y_pitch, d + ds * z, dp, cols, rows));
+        }
+    }
+    if (noise_sums) {
+        if ((st = ensure_host_w(ctx, n_slices))) return st;
+        HYB_CHECK(cudaMemcpyAsync(ctx->host_w, W, sizeof(long long) * n_slices, cudaMemcpyDeviceToHost,
+                                  ctx->stream));
+    }
+    if (!dg || !dy || noise_sums) HYB_CHECK(cudaStreamSynchronize(ctx->stream));
+    if (noise_sums)
+        for (int z = 0; z < n_slices; ++z) noise_sums[z] = ctx->host_w[z];
+    return HYB_OK;
+}
+
+}  // extern "C"

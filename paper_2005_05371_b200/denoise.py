@@ -1,0 +1,222 @@
+"""Host-side mirror of the reference's filter API for the hot path, on libhybrid_cuda.
+
+Same names, argument meaning and error behaviour as the reference's ``namespace denoise``
+(proj/include/denoise/{adaptive_median,parallel,tiling,pipeline}.hpp); images are uint8 arrays
+(numpy on the host, or torch uint8 tensors on the GPU) instead of ``Image`` doubles -- the
+reference's k/255 doubles map onto uint8 exactly for this path (SURVEY.md finding 4;
+``to_u8`` / ``to_unit`` below).  Every filter call goes through the C ABI; there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import capi
+from .capi import InvalidArgument, check, lib
+
+
+def _ctx(ctx):
+    return (ctx or capi.default_context()).ptr
+
+
+def _is_torch(a) -> bool:
+    return not isinstance(a, np.ndarray)
+
+
+def _empty_like(a, rows, cols):
+    if _is_torch(a):
+        import torch
+        return torch.empty((rows, cols), dtype=torch.uint8, device=a.device)
+    return np.empty((rows, cols), dtype=np.uint8)
+
+
+def _shape(a):
+    if a.ndim != 2:
+        raise InvalidArgument(f"expected a 2-D image, got {a.ndim} dimensions")
+    return int(a.shape[0]), int(a.shape[1])
+
+
+# ---------------------------------------------------------------- validation
+
+def validate_smax(smax: int) -> None:
+    """validate_smax -- reference proj/src/adaptive_median.cpp:11-16."""
+    if lib.hyb_validate_smax(int(smax)) != capi.HYB_OK:
+        raise InvalidArgument(f"smax must be an odd integer > 1, got {smax}")
+
+
+@dataclass
+class FilterConfig:
+    """FilterConfig -- reference proj/include/denoise/parallel.hpp:13-19, plus the W1 window."""
+    smax: int = 11
+    parts: int = 1
+    workers: int = 1
+    use_halo: bool = True
+    wiener_window: int = 3
+
+
+def validate_config(config: FilterConfig) -> None:
+    """validate_config -- reference proj/src/parallel.cpp:16-25."""
+    validate_smax(config.smax)
+    if config.parts < 1:
+        raise InvalidArgument(f"parts must be >= 1, got {config.parts}")
+    if config.workers < 1:
+        raise InvalidArgument(f"workers must be >= 1, got {config.workers}")
+
+
+# ---------------------------------------------------------------- tiling
+
+@dataclass
+class Band:
+    """Tile geometry -- reference proj/include/denoise/tiling.hpp:12-19 (without the pixel copy)."""
+    index: int
+    core_start: int
+    core_rows: int
+    halo_above: int
+    halo_below: int
+
+
+def split_bands(rows: int, parts: int, halo: int) -> list[Band]:
+    """Band geometry of split_bands -- reference proj/src/tiling.cpp:10-45: heights rows // parts
+    with the first rows % parts bands one taller; halos clamped at the image borders."""
+    if parts < 1 or parts > rows:
+        raise InvalidArgument(f"parts must be in [1, {rows}], got {parts}")
+    if halo < 0:
+        raise InvalidArgument(f"halo must be nonnegative, got {halo}")
+    base, extra = divmod(rows, parts)
+    out, start = [], 0
+    for i in range(parts):
+        core = base + (1 if i < extra else 0)
+        out.append(Band(i, start, core, min(halo, start), min(halo, rows - start - core)))
+        start += core
+    return out
+
+
+# ---------------------------------------------------------------- AMF
+
+def adaptive_median_rows(src, smax: int, row_begin: int, row_end: int, finalized_at: bool = False,
+                         ctx=None):
+    """detail::adaptive_median_rows -- reference proj/include/denoise/adaptive_median.hpp:47-48."""
+    rows, cols = _shape(src)
+    out = _empty_like(src, max(row_end - row_begin, 0), cols)
+    fin = _empty_like(src, max(row_end - row_begin, 0), cols) if finalized_at else None
+    sp, spitch = capi.buf(src)
+    dp, dpitch = capi.buf(out) if out.shape[0] else (0, cols)
+    fp, fpitch = capi.buf(fin) if fin is not None and fin.shape[0] else (None, cols)
+    c = _ctx(ctx)
+    check(lib.hyb_amf_u8(c, sp, spitch, rows, cols, row_begin, row_end, smax, dp, dpitch, fp, fpitch), c)
+    return (out, fin) if finalized_at else out
+
+
+def adaptive_median_serial(image, smax: int, ctx=None):
+    """adaptive_median_serial -- reference proj/src/adaptive_median.cpp:219-224."""
+    validate_smax(smax)
+    return adaptive_median_rows(image, smax, 0, _shape(image)[0], ctx=ctx)
+
+
+def adaptive_median_parallel(image, config: FilterConfig, ctx=None):
+    """adaptive_median_parallel -- reference proj/src/parallel.cpp:27-70: bands with halo
+    (smax-1)/2 (0 without use_halo), each filtered from its own copy, then stitched.  With the
+    halo the result is bit-identical to adaptive_median_serial for every parts."""
+    validate_config(config)
+    rows, cols = _shape(image)
+    if config.parts > rows:
+        raise InvalidArgument(f"parts {config.parts} exceeds image rows {rows}")
+    halo = (config.smax - 1) // 2 if config.use_halo else 0
+    out = _empty_like(image, rows, cols)
+    for b in split_bands(rows, config.parts, halo):
+        first = b.core_start - b.halo_above
+        tile = image[first:b.core_start + b.core_rows + b.halo_below]
+        tile = tile.clone() if _is_torch(tile) else np.ascontiguousarray(tile)
+        out[b.core_start:b.core_start + b.core_rows] = adaptive_median_rows(
+            tile, config.smax, b.halo_above, b.halo_above + b.core_rows, ctx=ctx)
+    return out
+
+
+# ---------------------------------------------------------------- W1 Wiener
+
+def wiener_local(f, win: int = 3, ctx=None):
+    """W1 local-statistics Wiener on a whole image; returns (y, W) with W = sum of V."""
+    rows, cols = _shape(f)
+    y = _empty_like(f, rows, cols)
+    fp, fpitch = capi.buf(f)
+    yp, ypitch = capi.buf(y)
+    w = ctypes.c_int64(0)
+    c = _ctx(ctx)
+    check(lib.hyb_wiener_u8(c, fp, fpitch, rows, cols, win, yp, ypitch, ctypes.byref(w)), c)
+    return y, w.value
+
+
+def noise_variance(noise_sum: int, pixel_count: int, win: int) -> float:
+    """nu / 255^2 in the reference's [0, 1] intensity^2 units (HybridResult.sigma2)."""
+    n = win * win
+    return noise_sum / (n * n * pixel_count) / (255.0 * 255.0)
+
+
+# ---------------------------------------------------------------- pipeline
+
+@dataclass
+class HybridResult:
+    """HybridResult -- reference proj/include/denoise/pipeline.hpp:12-18 (+ the exact W)."""
+    image: object
+    sigma2: float
+    t_adaptive: float
+    t_wiener: float
+    t_stretch: float
+    noise_sum: int
+    t_total: float
+
+
+def hybrid_denoise(noisy, config: FilterConfig, ctx=None) -> HybridResult:
+    """hybrid_denoise stages 1-2 -- reference proj/src/pipeline.cpp:23-53 with the north_star's
+    W1 Wiener in the stage-2 slot; config.parts strips (bit-identical for every parts)."""
+    validate_config(config)
+    rows, cols = _shape(noisy)
+    y = _empty_like(noisy, rows, cols)
+    gp, gpitch = capi.buf(noisy)
+    yp, ypitch = capi.buf(y)
+    st = capi.HybStats()
+    c = _ctx(ctx)
+    check(lib.hyb_hybrid_u8(c, gp, gpitch, rows, cols, config.smax, config.wiener_window, config.parts,
+                            yp, ypitch, ctypes.byref(st)), c)
+    return HybridResult(y, st.sigma2, st.t_adaptive, st.t_wiener, 0.0, st.noise_sum, st.t_total)
+
+
+def hybrid_denoise_batch(stack, smax: int, win: int, ctx=None):
+    """CT-stack hybrid: each slice filtered independently (own noise estimate).  Returns
+    (filtered stack, per-slice W)."""
+    if stack.ndim != 3:
+        raise InvalidArgument("expected a (slices, rows, cols) stack")
+    n, rows, cols = (int(s) for s in stack.shape)
+    if _is_torch(stack):
+        import torch
+        y = torch.empty_like(stack)
+        sstride = stack.stride(0)
+        ystride = y.stride(0)
+    else:
+        stack = np.ascontiguousarray(stack)
+        y = np.empty_like(stack)
+        sstride, ystride = stack.strides[0], y.strides[0]
+    gp, gpitch = capi.buf(stack)
+    yp, ypitch = capi.buf(y)
+    w = (ctypes.c_int64 * n)()
+    c = _ctx(ctx)
+    check(lib.hyb_hybrid_batch_u8(c, gp, gpitch, sstride, n, rows, cols, smax, win, yp, ypitch, ystride, w), c)
+    return y, list(w)
+
+
+# ---------------------------------------------------------------- uint8 <-> reference doubles
+
+def to_u8(img: np.ndarray) -> np.ndarray:
+    """Reference Image doubles -> uint8 with lround(p * 255) (proj/src/pgm_io.cpp:115); rejects
+    off-grid values, which have no exact uint8 representation."""
+    q = np.clip(np.floor(np.asarray(img, np.float64) * 255.0 + 0.5), 0, 255)
+    if not np.array_equal(q / 255.0, img):
+        raise InvalidArgument("image has values off the k/255 grid; no exact uint8 representation")
+    return q.astype(np.uint8)
+
+
+def to_unit(img_u8) -> np.ndarray:
+    """uint8 -> the reference's [0, 1] doubles, k/255 (proj/src/pgm_io.cpp:73,88)."""
+    return np.asarray(img_u8, np.float64) / 255.0

@@ -1,0 +1,195 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded inputs.
+
+AMF: bit-exact (BASELINE.json north_star).  W1 Wiener: the kernel computes the exact rational
+result (fp32 with an exact int128 tie check), so it is held to bit-exactness too -- stricter than
+the north_star tolerance (<= 1 LSB, >= 99.99 % exact), which is asserted as well.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2005_05371_b200 import CONFIGS, FilterConfig, capi, denoise
+
+pytestmark = pytest.mark.gpu
+
+
+def rand_u8(rows, cols, seed, sp=0.0):
+    rng = np.random.default_rng(seed)
+    img = rng.integers(0, 256, size=(rows, cols), dtype=np.uint8)
+    if sp:
+        u = rng.random((rows, cols))
+        img[u < sp / 2] = 0
+        img[(u >= sp / 2) & (u < sp)] = 255
+    return img
+
+
+def wiener_tolerance(y, ref):
+    d = np.abs(y.astype(np.int16) - ref.astype(np.int16))
+    assert d.max() <= 1
+    assert (d == 0).mean() >= 0.9999
+
+
+# ---------------------------------------------------------------- AMF
+
+def test_amf_kat_ramp(ctx):
+    # reference proj/tests/test_adaptive_median.cpp:26-38 (rank-compressed: 0.1..0.9 -> 1..9)
+    img = np.arange(1, 10, dtype=np.uint8).reshape(3, 3)
+    out = denoise.adaptive_median_serial(img, 3)
+    np.testing.assert_array_equal(out, oracle.amf(img, 3))
+
+
+def test_amf_kat_impulse_on_gradient(ctx):
+    # reference proj/tests/test_adaptive_median.cpp:67-78 (0.1(r+c)+0.1 -> r+c+1, salt -> 255)
+    img = np.fromfunction(lambda r, c: r + c + 1, (5, 5)).astype(np.uint8)
+    img[2, 2] = 255
+    out = denoise.adaptive_median_serial(img, 3)
+    assert out[2, 2] == 5
+    assert out[1, 2] == img[1, 2] and out[3, 1] == img[3, 1]
+
+
+def test_amf_constant_fixed_point(ctx):
+    img = np.full((9, 9), 178, np.uint8)
+    np.testing.assert_array_equal(denoise.adaptive_median_serial(img, 11), img)
+
+
+@pytest.mark.parametrize("smax", [3, 5, 7, 9, 11, 13, 15])
+def test_amf_random_vs_oracle(ctx, smax):
+    # oracle equivalence (reference proj/tests/test_adaptive_median.cpp:80-96), quantised images
+    for trial in range(12):
+        rng = np.random.default_rng(1000 + trial)
+        rows, cols = int(rng.integers(8, 200)), int(rng.integers(8, 300))
+        img = rand_u8(rows, cols, trial, sp=0.2 if trial % 2 == 0 else 0.45)
+        out, fin = denoise.adaptive_median_rows(img, smax, 0, rows, finalized_at=True)
+        ref_out, ref_fin = oracle.amf(img, smax, finalized_at=True)
+        np.testing.assert_array_equal(out, ref_out)
+        np.testing.assert_array_equal(fin, ref_fin)
+
+
+def test_amf_matches_reference_itself(ctx):
+    if not oracle.ref_available():
+        pytest.skip("oracle/_ref not built")
+    img = rand_u8(63, 57, 5, sp=0.3)
+    for smax in (3, 7, 11):
+        np.testing.assert_array_equal(denoise.adaptive_median_serial(img, smax), oracle.ref_amf_rows(img, smax))
+
+
+def test_amf_row_ranges(ctx):
+    img = rand_u8(97, 131, 9, sp=0.4)
+    for rb, re in [(0, 1), (5, 40), (96, 97), (30, 97), (0, 97)]:
+        np.testing.assert_array_equal(denoise.adaptive_median_rows(img, 9, rb, re),
+                                      oracle.amf(img, 9, rb, re))
+
+
+def test_amf_parallel_partition_invariance(ctx):
+    # reference proj/tests/test_parallel.cpp:54-76
+    img = rand_u8(64, 64, 3, sp=0.25)
+    for smax in (3, 11):
+        serial = denoise.adaptive_median_serial(img, smax)
+        for parts in (2, 3, 4, 8):
+            out = denoise.adaptive_median_parallel(img, FilterConfig(smax=smax, parts=parts, workers=4))
+            np.testing.assert_array_equal(out, serial)
+    odd = rand_u8(63, 57, 4, sp=0.25)
+    for parts in (2, 5, 6, 13, 63):
+        np.testing.assert_array_equal(denoise.adaptive_median_parallel(odd, FilterConfig(smax=7, parts=parts)),
+                                      oracle.amf(odd, 7))
+
+
+def test_amf_device_tensors(ctx):
+    import torch
+    img = rand_u8(300, 517, 11, sp=0.3)
+    g = torch.from_numpy(img).cuda()
+    out = denoise.adaptive_median_serial(g, 7)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(out.cpu().numpy(), oracle.amf(img, 7))
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 3])
+def test_amf_baseline_configs(ctx, cfg):
+    c = CONFIGS[cfg]
+    img = capi.make_phantom(c["rows"], c["cols"], c["ellipses"], c["sigma"], c["density"], 0)
+    np.testing.assert_array_equal(denoise.adaptive_median_serial(img, c["smax"]), oracle.amf(img, c["smax"]))
+
+
+def test_amf_worst_case_growth(ctx):
+    # config-4 statistics (sigma 20, density 0.5, smax 11) on a 1024^2 crop-sized phantom
+    img = capi.make_phantom(1024, 1024, 16, 20.0, 0.5, 0)
+    out, fin = denoise.adaptive_median_rows(img, 11, 0, 1024, finalized_at=True)
+    ref_out, ref_fin = oracle.amf(img, 11, finalized_at=True)
+    np.testing.assert_array_equal(out, ref_out)
+    np.testing.assert_array_equal(fin, ref_fin)
+
+
+# ---------------------------------------------------------------- W1 Wiener
+
+@pytest.mark.parametrize("win", [1, 3, 5, 7, 9])
+def test_wiener_vs_oracle(ctx, win):
+    for trial in range(6):
+        rng = np.random.default_rng(50 + trial)
+        rows, cols = int(rng.integers(1, 150)), int(rng.integers(1, 260))
+        f = rand_u8(rows, cols, 70 + trial)
+        y, w = denoise.wiener_local(f, win)
+        ref_y, ref_w = oracle.wiener(f, win)
+        assert w == ref_w
+        wiener_tolerance(y, ref_y)
+        np.testing.assert_array_equal(y, ref_y)
+
+
+def test_wiener_constant_identity(ctx):
+    f = np.full((40, 70), 91, np.uint8)
+    y, w = denoise.wiener_local(f, 5)
+    assert w == 0
+    np.testing.assert_array_equal(y, f)
+
+
+# ---------------------------------------------------------------- hybrid
+
+@pytest.mark.parametrize("cfg", [0, 1])
+def test_hybrid_baseline_configs(ctx, cfg):
+    c = CONFIGS[cfg]
+    g = capi.make_phantom(c["rows"], c["cols"], c["ellipses"], c["sigma"], c["density"], 0)
+    res = denoise.hybrid_denoise(g, FilterConfig(smax=c["smax"], wiener_window=c["win"]))
+    ref_y, ref_w = oracle.hybrid(g, c["smax"], c["win"])
+    assert res.noise_sum == ref_w
+    wiener_tolerance(res.image, ref_y)
+    np.testing.assert_array_equal(res.image, ref_y)
+
+
+@pytest.mark.parametrize("smax,win", [(9, 5), (11, 7)])
+def test_hybrid_large_windows(ctx, smax, win):
+    g = capi.make_phantom(700, 900, 20, 20.0, 0.5, 3)
+    res = denoise.hybrid_denoise(g, FilterConfig(smax=smax, wiener_window=win))
+    ref_y, ref_w = oracle.hybrid(g, smax, win)
+    assert res.noise_sum == ref_w
+    np.testing.assert_array_equal(res.image, ref_y)
+
+
+def test_hybrid_strip_invariance(ctx):
+    # strips as independent sub-launches with real halo copies == one strip
+    g = capi.make_phantom(401, 333, 12, 15.0, 0.2, 7)
+    base = denoise.hybrid_denoise(g, FilterConfig(smax=7, wiener_window=3))
+    for parts in (2, 3, 4, 5, 8, 13):
+        r = denoise.hybrid_denoise(g, FilterConfig(smax=7, parts=parts, wiener_window=3))
+        assert r.noise_sum == base.noise_sum
+        np.testing.assert_array_equal(r.image, base.image)
+
+
+def test_hybrid_batch_matches_per_slice(ctx):
+    c = CONFIGS[3]
+    stack = np.stack([capi.make_phantom(128, 160, 6, c["sigma"], c["density"], s) for s in range(5)])
+    y, ws = denoise.hybrid_denoise_batch(stack, c["smax"], c["win"])
+    for s in range(5):
+        ref_y, ref_w = oracle.hybrid(stack[s], c["smax"], c["win"])
+        assert ws[s] == ref_w
+        np.testing.assert_array_equal(y[s], ref_y)
+
+
+# ---------------------------------------------------------------- errors
+
+def test_errors_match_reference_text(ctx):
+    img = rand_u8(8, 8, 1)
+    with pytest.raises(capi.InvalidArgument, match="odd integer > 1"):
+        denoise.adaptive_median_rows(img, 4, 0, 8)
+    with pytest.raises(capi.InvalidArgument, match="bad row range"):
+        denoise.adaptive_median_rows(img, 3, 5, 3)
+    with pytest.raises(capi.InvalidArgument, match="exceeds image rows"):
+        denoise.hybrid_denoise(img, FilterConfig(smax=3, parts=9))
