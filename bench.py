@@ -182,7 +182,10 @@ def run_gpu(args, cfg, c):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
-    stream = torch.cuda.current_stream(dev)
+    # a dedicated stream: the legacy default stream's handle is 0, which the C ABI reads as
+    # "use the context's own stream"
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     ctx = capi.Context(local)
     ctx.set_stream(stream.cuda_stream)
     lib = capi.lib

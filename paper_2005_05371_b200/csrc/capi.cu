@@ -13,6 +13,7 @@
 
 #include "../../include/hybrid_cuda.h"
 #include "hyb_internal.cuh"
+#include "tma.cuh"
 
 namespace hyb {
 static std::atomic<long long> g_launches{0};
@@ -292,8 +293,10 @@ int hyb_amf_u8(hyb_ctx* ctx, const uint8_t* src, size_t src_pitch, int rows, int
     if (finalized_at && (st = check_pitch(ctx, fin_pitch, cols, "finalized_at"))) return st;
     HYB_CHECK(cudaSetDevice(ctx->device));
     const int orows = row_end - row_begin;
-    const bool dsrc = is_device_ptr(src), ddst = is_device_ptr(dst);
-    const bool dfin = finalized_at && is_device_ptr(finalized_at);
+    // device buffers are used in place when TMA can address them (16-byte aligned base and pitch)
+    const bool dsrc = is_device_ptr(src) && hyb::tma_compatible(src, src_pitch, 0);
+    const bool ddst = is_device_ptr(dst) && hyb::tma_compatible(dst, dst_pitch, 0);
+    const bool dfin = finalized_at && is_device_ptr(finalized_at) && hyb::tma_compatible(finalized_at, fin_pitch, 0);
     const size_t pp = round_pitch(cols);
     const uint8_t* s = src;
     size_t sp = src_pitch;
@@ -336,6 +339,8 @@ int hyb_amf_batch_u8(hyb_ctx* ctx, const uint8_t* src, size_t src_pitch, size_t 
     if (n_slices < 1) return fail(ctx, HYB_EINVAL, "n_slices must be >= 1, got " + std::to_string(n_slices));
     if (!is_device_ptr(src) || !is_device_ptr(dst))
         return fail(ctx, HYB_EINVAL, "hyb_amf_batch_u8 takes device buffers");
+    if (!hyb::tma_compatible(src, src_pitch, src_slice_stride) || !hyb::tma_compatible(dst, dst_pitch, dst_slice_stride))
+        return fail(ctx, HYB_EINVAL, "batch buffers need 16-byte aligned bases, pitches and slice strides");
     HYB_CHECK(cudaSetDevice(ctx->device));
     hyb::Plane p{src, src_pitch, src_slice_stride, dst, dst_pitch, dst_slice_stride, rows, cols, 0, rows,
                  n_slices};
@@ -484,7 +489,7 @@ int hyb_hybrid_u8(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int co
                                          std::to_string(rows));
     if (!g || !y) return fail(ctx, HYB_EINVAL, "null image pointer");
     HYB_CHECK(cudaSetDevice(ctx->device));
-    const bool dg = is_device_ptr(g), dy = is_device_ptr(y);
+    const bool dg = is_device_ptr(g) && hyb::tma_compatible(g, pitch, 0), dy = is_device_ptr(y);
     const size_t pp = round_pitch(cols);
     const bool timed = stats != nullptr;
     if (timed) HYB_CHECK(cudaEventRecord(ctx->ev[3], ctx->stream));
@@ -540,7 +545,7 @@ int hyb_hybrid_batch_u8(hyb_ctx* ctx, const uint8_t* g, size_t pitch, size_t sli
     if (slice_stride < pitch * rows || y_slice_stride < y_pitch * rows)
         return fail(ctx, HYB_EINVAL, "slice stride smaller than one slice");
     HYB_CHECK(cudaSetDevice(ctx->device));
-    const bool dg = is_device_ptr(g), dy = is_device_ptr(y);
+    const bool dg = is_device_ptr(g) && hyb::tma_compatible(g, pitch, slice_stride), dy = is_device_ptr(y);
     const size_t pp = round_pitch(cols), ps = pp * rows;
     const uint8_t* s = g;
     size_t sp = pitch, ss = slice_stride;
