@@ -56,6 +56,7 @@ struct hyb_ctx {
     cudaStream_t stream = nullptr;
     std::string err;
     DevBuf in, out, fin, f, wsum;      // staging / scratch
+    DevBuf amf_q[2], amf_cnt;          // AMF growth work queues
     std::vector<DevBuf> strip_g, strip_f;
     long long* host_w = nullptr;       // pinned readback of noise sums
     size_t host_w_n = 0;
@@ -146,6 +147,20 @@ cudaError_t copy2d(hyb_ctx* ctx, void* dst, size_t dp, const void* src, size_t s
     return cudaMemcpy2DAsync(dst, dp, src, sp, (size_t)cols, (size_t)rows, cudaMemcpyDefault, ctx->stream);
 }
 
+// AMF launch with the context's growth workspace.
+cudaError_t run_amf(hyb_ctx* ctx, const hyb::Plane& p, int smax, uint8_t* fin, size_t fpitch, size_t fslice) {
+    const size_t words = hyb::amf_queue_words(p);
+    cudaError_t e;
+    if ((e = ctx->amf_q[0].ensure(words * 4)) != cudaSuccess) return e;
+    if ((e = ctx->amf_q[1].ensure(words * 4)) != cudaSuccess) return e;
+    if ((e = ctx->amf_cnt.ensure(128 * sizeof(int))) != cudaSuccess) return e;
+    hyb::AmfWork w;
+    w.queue[0] = reinterpret_cast<uint32_t*>(ctx->amf_q[0].ptr);
+    w.queue[1] = reinterpret_cast<uint32_t*>(ctx->amf_q[1].ptr);
+    w.counts = reinterpret_cast<int*>(ctx->amf_cnt.ptr);
+    return hyb::launch_amf(p, smax, fin, fpitch, fslice, w, ctx->stream);
+}
+
 // Core of hyb_hybrid_u8 on device-resident buffers.
 int hybrid_device(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int cols, int smax,
                   int win, int parts, uint8_t* y, size_t ypitch, bool timed) {
@@ -158,7 +173,7 @@ int hybrid_device(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int co
         const size_t fp = round_pitch(cols);
         HYB_CHECK(ctx->f.ensure(fp * rows));
         hyb::Plane a{g, pitch, 0, ctx->f.ptr, fp, 0, rows, cols, 0, rows, 1};
-        HYB_CHECK(hyb::launch_amf(a, smax, nullptr, 0, 0, ctx->stream));
+        HYB_CHECK(run_amf(ctx, a, smax, nullptr, 0, 0));
         if (timed) HYB_CHECK(cudaEventRecord(ctx->ev[1], ctx->stream));
         HYB_CHECK(cudaMemsetAsync(W, 0, sizeof(long long), ctx->stream));
         hyb::Plane w{ctx->f.ptr, fp, 0, y, ypitch, 0, rows, cols, 0, rows, 1};
@@ -194,7 +209,7 @@ int hybrid_device(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int co
                              cols, grows));
             hyb::Plane a{ctx->strip_g[i].ptr, sp, 0, ctx->strip_f[i].ptr, sp, 0, grows, cols,
                          t.hA - t.fa, t.hA + t.core + t.fb, 1};
-            HYB_CHECK(hyb::launch_amf(a, smax, nullptr, 0, 0, ctx->stream));
+            HYB_CHECK(run_amf(ctx, a, smax, nullptr, 0, 0));
         }
         if (timed) HYB_CHECK(cudaEventRecord(ctx->ev[1], ctx->stream));
         HYB_CHECK(cudaMemsetAsync(W, 0, sizeof(long long), ctx->stream));
@@ -252,6 +267,8 @@ int hyb_destroy(hyb_ctx* ctx) {
     ctx->fin.release();
     ctx->f.release();
     ctx->wsum.release();
+    for (auto& b : ctx->amf_q) b.release();
+    ctx->amf_cnt.release();
     for (auto& b : ctx->strip_g) b.release();
     for (auto& b : ctx->strip_f) b.release();
     if (ctx->host_w) cudaFreeHost(ctx->host_w);
@@ -321,7 +338,7 @@ int hyb_amf_u8(hyb_ctx* ctx, const uint8_t* src, size_t src_pitch, int rows, int
         fp = pp;
     }
     hyb::Plane p{s, sp, 0, d, dp, 0, rows, cols, row_begin, row_end, 1};
-    HYB_CHECK(hyb::launch_amf(p, smax, fz, fp, 0, ctx->stream));
+    HYB_CHECK(run_amf(ctx, p, smax, fz, fp, 0));
     if (!ddst) HYB_CHECK(copy2d(ctx, dst, dst_pitch, d, dp, cols, orows));
     if (finalized_at && !dfin) HYB_CHECK(copy2d(ctx, finalized_at, fin_pitch, fz, fp, cols, orows));
     if (!dsrc || !ddst || (finalized_at && !dfin)) HYB_CHECK(cudaStreamSynchronize(ctx->stream));
@@ -344,7 +361,7 @@ int hyb_amf_batch_u8(hyb_ctx* ctx, const uint8_t* src, size_t src_pitch, size_t 
     HYB_CHECK(cudaSetDevice(ctx->device));
     hyb::Plane p{src, src_pitch, src_slice_stride, dst, dst_pitch, dst_slice_stride, rows, cols, 0, rows,
                  n_slices};
-    HYB_CHECK(hyb::launch_amf(p, smax, nullptr, 0, 0, ctx->stream));
+    HYB_CHECK(run_amf(ctx, p, smax, nullptr, 0, 0));
     return HYB_OK;
 }
 
@@ -573,7 +590,7 @@ int hyb_hybrid_batch_u8(hyb_ctx* ctx, const uint8_t* g, size_t pitch, size_t sli
     HYB_CHECK(ctx->wsum.ensure(sizeof(long long) * n_slices));
     unsigned long long* W = reinterpret_cast<unsigned long long*>(ctx->wsum.ptr);
     hyb::Plane a{s, sp, ss, ctx->f.ptr, pp, ps, rows, cols, 0, rows, n_slices};
-    HYB_CHECK(hyb::launch_amf(a, smax, nullptr, 0, 0, ctx->stream));
+    HYB_CHECK(run_amf(ctx, a, smax, nullptr, 0, 0));
     HYB_CHECK(cudaMemsetAsync(W, 0, sizeof(long long) * n_slices, ctx->stream));
     hyb::Plane w{ctx->f.ptr, pp, ps, d, dp, ds, rows, cols, 0, rows, n_slices};
     HYB_CHECK(hyb::launch_wiener_stats(w, win, W, ctx->stream));

@@ -20,9 +20,17 @@ struct Plane {
     int n_slices;
 };
 
-// AMF launch (amf.cu).  fin may be null.
+// Device workspace of the AMF growth stage: two ping-pong work queues (u32 pixel ids, capacity
+// amf_queue_words(p) each) and one int counter per growth level (smax <= 255 -> 127 levels).
+struct AmfWork {
+    uint32_t* queue[2];
+    int* counts;
+};
+size_t amf_queue_words(const Plane& p);
+
+// AMF launch (amf.cu): k = 3 tile kernel + one growth kernel per k = 5..smax.  fin may be null.
 cudaError_t launch_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, size_t fslice,
-                       cudaStream_t stream);
+                       const AmfWork& work, cudaStream_t stream);
 
 // W1 statistics launch (wiener.cu): adds sum of V over the rows into noise_sum[slice].
 cudaError_t launch_wiener_stats(const Plane& p, int win, unsigned long long* noise_sum,
