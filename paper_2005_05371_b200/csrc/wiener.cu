@@ -12,9 +12,13 @@
 // The gain runs in fp32 and falls back to an exact __int128 comparison only when the fp32
 // result lies within 2^-11 of a rounding boundary, so the output equals the exact rational
 // result bit for bit.
+#include <cuda.h>
+
+#include <algorithm>
 #include <cstdint>
 
 #include "hyb_internal.cuh"
+#include "tma.cuh"
 
 namespace hyb {
 namespace {
@@ -210,16 +214,325 @@ cudaError_t launch(const Plane& p, int win, unsigned long long* wsum, const long
     return cudaGetLastError();
 }
 
+
+// ------------------------------------------------------------------------------------------
+// Fast path for win in {1, 3, 5, 7} (every BASELINE config): warp-autonomous 128 x 32 tiles.
+// Each warp owns one tile at a time (TMA box of the tile plus an RW halo into a warp-private
+// double-buffered slot), each lane 4 columns.  Per input row a lane forms, for each of its 4
+// pixels, the horizontal window sums of f and f^2 with IDP.4A (dp4a) on byte-aligned words,
+// and slides them down the tile through an N-deep register ring, so every pixel costs a few
+// integer ops; statistics stay exact int32 per pixel.
+// ------------------------------------------------------------------------------------------
+constexpr int FW = 128;          // tile columns
+constexpr int FH = 16;           // tile rows
+constexpr int FCP = 16;          // column pad (TMA box x offsets must be 16-byte aligned)
+constexpr int FBS = FW + 2 * FCP;  // staged row bytes (160)
+constexpr int FNW = 8;           // warps per CTA
+__host__ __device__ constexpr int kFastSmemSlot(int rw) { return ((FBS * (FH + 2 * rw)) + 127) / 128 * 128; }
+
+struct FastArgs {
+    uint8_t* dst;
+    size_t dpitch, dslice;
+    int rows, cols, row_begin, row_end, n_slices;
+    int tiles_x, tiles_y;
+    unsigned long long* wsum;  // stats
+    const long long* wread;    // gain
+    long long pixel_count;
+};
+
+// 4 bytes starting at byte S of the 12-byte window [w0 w1 w2] (S compile-time, 0..11).
+template <int S>
+__device__ __forceinline__ uint32_t bytes4(uint32_t w0, uint32_t w1, uint32_t w2) {
+    if (S == 0) return w0;
+    if (S == 4) return w1;
+    if (S == 8) return w2;
+    if (S < 4) return __funnelshift_r(w0, w1, 8 * S);
+    if (S < 8) return __funnelshift_r(w1, w2, 8 * (S - 4));
+    return w2 >> (8 * (S - 8));  // only the low 12 - S bytes are meaningful
+}
+
+// Horizontal window sums (f, f^2) of pixel I (0..3) of the lane's 4 columns.
+template <int RW, int I>
+__device__ __forceinline__ void hsums(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t& h1, uint32_t& h2) {
+    constexpr int N = 2 * RW + 1;
+    constexpr int S = 4 + I - RW;  // first window byte in [w0 w1 w2] (w1 = the lane's own word)
+    if (N == 1) {
+        const uint32_t x = (bytes4<S>(w0, w1, w2)) & 0xFFu;
+        h1 = x;
+        h2 = x * x;
+    } else if (N == 3) {
+        const uint32_t x = bytes4<S>(w0, w1, w2) & 0x00FFFFFFu;
+        h1 = __dp4a(x, 0x01010101u, 0u);
+        h2 = __dp4a(x, x, 0u);
+    } else {
+        const uint32_t lo = bytes4<S>(w0, w1, w2);
+        constexpr uint32_t hm = N == 5 ? 0x000000FFu : 0x00FFFFFFu;
+        const uint32_t hi = bytes4<S + 4>(w0, w1, w2) & hm;
+        h1 = __dp4a(hi, 0x01010101u, __dp4a(lo, 0x01010101u, 0u));
+        h2 = __dp4a(hi, hi, __dp4a(lo, lo, 0u));
+    }
+}
+
+template <int RW, bool GAIN>
+__global__ void __launch_bounds__(FNW * 32) wiener_fast_kernel(const __grid_constant__ CUtensorMap tm,
+                                                               const __grid_constant__ FastArgs a) {
+    constexpr int N = 2 * RW + 1;
+    constexpr int NN = N * N;
+    constexpr int SROWS = FH + 2 * RW;
+    constexpr int SLOT = kFastSmemSlot(RW);
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem) + 2 * warp;  // 2 per warp
+    uint8_t* slots = smem + 128 + (size_t)warp * 2 * SLOT;
+    const int per_slice = a.tiles_x * a.tiles_y;
+    const int ntiles = per_slice * a.n_slices;
+    const int gw = blockIdx.x * FNW + warp, nw = gridDim.x * FNW;  // global warp id / count
+    if (gw >= ntiles) return;
+    auto coords = [&](int t, int& x0, int& y0, int& z) {
+        z = t / per_slice;
+        const int rem = t - z * per_slice;
+        const int by = rem / a.tiles_x;
+        x0 = (rem - by * a.tiles_x) * FW;
+        y0 = a.row_begin + by * FH;
+    };
+    auto issue = [&](int t, int slot) {
+        int x0, y0, z;
+        coords(t, x0, y0, z);
+        mbar_expect_tx(&bar[slot], FBS * SROWS);
+        tma_load_3d(slots + slot * SLOT, &tm, &bar[slot], x0 - FCP, y0 - RW, z);
+    };
+    if (lane == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+        issue(gw, 0);
+        if (gw + nw < ntiles) issue(gw + nw, 1);
+    }
+    __syncwarp();
+
+    constexpr int n = N * N;
+    long long W = 0;
+    int wq32 = 0;  // floor(W / P), clamped: V <= wq32 <=> V P <= W
+    float kn = 0.f;
+    if (GAIN) {
+        W = a.wread[0];  // per-slice values are re-read below when n_slices > 1
+    }
+    unsigned long long vsum = 0;
+    int zprev = -1;
+    int it = 0;
+    for (int t = gw; t < ntiles; t += nw, ++it) {
+        const int slot = it & 1;
+        mbar_wait(&bar[slot], (uint32_t)(it >> 1) & 1u);
+        int x0, y0, z;
+        coords(t, x0, y0, z);
+        uint8_t* T = slots + slot * SLOT;
+        if (GAIN && z != zprev) {
+            W = a.wread[z];
+            const long long wq = W / a.pixel_count;
+            wq32 = wq > 0x7FFFFFFFll ? 0x7FFFFFFF : (int)wq;
+            kn = (float)((double)W / ((double)a.pixel_count * (double)n));
+            zprev = z;
+        }
+        if (!GAIN && z != zprev) {
+            if (zprev >= 0) {
+#pragma unroll
+                for (int d = 16; d > 0; d >>= 1) vsum += __shfl_down_sync(0xFFFFFFFFu, vsum, d);
+                if (lane == 0 && vsum) atomicAdd(a.wsum + zprev, vsum);
+                vsum = 0;
+            }
+            zprev = z;
+        }
+
+        // ---- border tiles: replicate edges into the zero-filled halo (warp-private slot) ----
+        const int sx0 = x0 - FCP, sy0 = y0 - RW;
+        if (sx0 < 0 || sx0 + FBS > a.cols || sy0 < 0 || sy0 + SROWS > a.rows) {
+            const int c_lo = max(0, -sx0), c_hi = min(FBS, a.cols - sx0);
+            const int r_lo = max(0, -sy0), r_hi = min(SROWS, a.rows - sy0);
+            if (c_lo > 0 || c_hi < FBS) {
+                for (int rr = r_lo; rr < r_hi; ++rr) {
+                    uint8_t* row = T + rr * FBS;
+                    const uint8_t lv = row[c_lo], rv = row[c_hi - 1];
+                    for (int cc = lane; cc < FBS; cc += 32) {
+                        if (cc < c_lo) row[cc] = lv;
+                        else if (cc >= c_hi) row[cc] = rv;
+                    }
+                }
+                __syncwarp();
+            }
+            for (int rr = 0; rr < SROWS; ++rr) {
+                const int src_r = rr < r_lo ? r_lo : (rr >= r_hi ? r_hi - 1 : rr);
+                if (src_r == rr) continue;
+                for (int q = lane; q < FBS / 4; q += 32)
+                    reinterpret_cast<uint32_t*>(T + rr * FBS)[q] = reinterpret_cast<const uint32_t*>(T + src_r * FBS)[q];
+            }
+            __syncwarp();
+        }
+
+        // ---- sliding window sums: lane = columns 4 lane .. 4 lane + 3 ----
+        // s += hsums(row rr) - hsums(row rr - N): the leaving row is re-read from the tile rather
+        // than kept in a register ring (smaller code and register footprint, no unroll by N).
+        const int c = 4 * lane;
+        const int col_lim = a.cols - x0, row_lim = a.row_end - y0;
+        uint32_t s1[4] = {0, 0, 0, 0}, s2[4] = {0, 0, 0, 0};
+        const uint32_t* base = reinterpret_cast<const uint32_t*>(T + FCP + c - 4);
+        auto add_row = [&](int rr, bool sub) {
+            const uint32_t* rp = base + rr * (FBS / 4);
+            const uint32_t w0 = rp[0], w1 = rp[1], w2 = rp[2];
+            uint32_t h1[4], h2[4];
+            hsums<RW, 0>(w0, w1, w2, h1[0], h2[0]);
+            hsums<RW, 1>(w0, w1, w2, h1[1], h2[1]);
+            hsums<RW, 2>(w0, w1, w2, h1[2], h2[2]);
+            hsums<RW, 3>(w0, w1, w2, h1[3], h2[3]);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                s1[i] = sub ? s1[i] - h1[i] : s1[i] + h1[i];
+                s2[i] = sub ? s2[i] - h2[i] : s2[i] + h2[i];
+            }
+        };
+#pragma unroll
+        for (int rr = 0; rr < N - 1; ++rr) add_row(rr, false);
+        uint8_t* drow = GAIN ? a.dst + (size_t)z * a.dslice + (size_t)(y0 - a.row_begin) * a.dpitch + x0 + c : nullptr;
+        const bool vec_store = GAIN && c + 4 <= col_lim && ((reinterpret_cast<uintptr_t>(drow) & 3) == 0) &&
+                               (a.dpitch & 3) == 0;
+#pragma unroll 1
+        for (int y = 0; y < FH; ++y) {
+            add_row(y + N - 1, false);  // window of output row y = input rows y .. y + N - 1
+            if (!GAIN) {
+                if (y < row_lim) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        if (c + i < col_lim) vsum += NN * s2[i] - s1[i] * s1[i];
+                }
+            } else {
+                const uint32_t own = *(base + (y + RW) * (FBS / 4) + 1);  // f of the 4 output pixels
+                uint32_t out = 0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const uint32_t f = (own >> (8 * i)) & 0xFFu;
+                    const uint32_t S1 = s1[i];
+                    const int V = (int)(NN * s2[i] - S1 * S1);
+                    const uint32_t mu = (2u * S1 + NN) / (2u * NN);  // round(S1 / n), half up
+                    const int d = (int)(NN * f) - (int)S1;            // |d| <= 49 * 255 < 2^14
+                    // fp32 gain, conversions by exponent tricks (FMA/ALU pipes) except I2F(V), RCP
+                    const float df = __int_as_float(0x4B000000 + d + 16384) - 8404992.0f;  // (float)d
+                    const float fh = __int_as_float(0x4B000000 | f) - 8388607.5f;          // f + 0.5
+                    float rv;
+                    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rv) : "f"((float)V));
+                    const float h = fh - df * kn * rv;  // y + 1/2, y = f - D W / (n V P)
+                    const int hb = __float_as_int(__fadd_rd(h, 12582912.0f));  // floor(h) in the mantissa
+                    const float fr = h - (__int_as_float(hb) - 12582912.0f);
+                    int q = hb - 0x4B400000;
+                    const bool use_mu = V <= wq32;
+                    if (!use_mu && fabsf(fr - 0.5f) > 0.5f - kTieEps) {
+                        // exact: y >= m - 1/2  <=>  (2 (f - m) + 1) n V P >= 2 D W
+                        const int m = fr < 0.5f ? q : q + 1;
+                        const __int128 Q = (__int128)((long long)NN * V) * a.pixel_count;
+                        const __int128 lhs = (__int128)(2 * ((int)f - m) + 1) * Q;
+                        const __int128 rhs = (__int128)(2 * (long long)d) * W;
+                        q = lhs >= rhs ? m : m - 1;
+                    }
+                    out |= (uint32_t)(use_mu ? (int)mu : q) << (8 * i);  // y in [min(mu, f), max(mu, f)]
+                }
+                if (y < row_lim) {
+                    if (vec_store) {
+                        *reinterpret_cast<uint32_t*>(drow) = out;
+                    } else {
+                        for (int i = 0; i < 4 && c + i < col_lim; ++i) drow[i] = (uint8_t)(out >> (8 * i));
+                    }
+                }
+                drow += a.dpitch;
+            }
+            add_row(y, true);  // drop input row y
+        }
+        __syncwarp();
+        // refill this slot with the warp's tile after next
+        if (lane == 0 && t + 2 * nw < ntiles) {
+            fence_proxy_async_smem();
+            issue(t + 2 * nw, slot);
+        }
+    }
+    if (!GAIN && zprev >= 0) {
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) vsum += __shfl_down_sync(0xFFFFFFFFu, vsum, d);
+        if (lane == 0 && vsum) atomicAdd(a.wsum + zprev, vsum);
+    }
+}
+
+int g_wsms = 0;
+
+template <int RW, bool GAIN>
+cudaError_t launch_fast(const Plane& p, unsigned long long* wsum, const long long* wread, long long pixel_count,
+                        cudaStream_t stream) {
+    constexpr int SLOT = kFastSmemSlot(RW);
+    constexpr size_t smem = 128 + (size_t)FNW * 2 * SLOT + 128;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(wiener_fast_kernel<RW, GAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    if (!g_wsms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_wsms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    CUtensorMap tm;
+    cudaError_t e = make_tmap_u8(&tm, p.src, p.cols, p.rows, p.n_slices, p.spitch, p.sslice, FBS, FH + 2 * RW);
+    if (e != cudaSuccess) return e;
+    FastArgs a;
+    a.dst = p.dst;
+    a.dpitch = p.dpitch;
+    a.dslice = p.dslice;
+    a.rows = p.rows;
+    a.cols = p.cols;
+    a.row_begin = p.row_begin;
+    a.row_end = p.row_end;
+    a.n_slices = p.n_slices;
+    a.tiles_x = (p.cols + FW - 1) / FW;
+    a.tiles_y = (p.row_end - p.row_begin + FH - 1) / FH;
+    a.wsum = wsum;
+    a.wread = wread;
+    a.pixel_count = pixel_count;
+    static int per_sm = 0;
+    if (!per_sm) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, wiener_fast_kernel<RW, GAIN>, FNW * 32, smem);
+        if (per_sm < 1) per_sm = 1;
+    }
+    const long long ntiles = (long long)a.tiles_x * a.tiles_y * a.n_slices;
+    const long long warps = std::min<long long>(ntiles, (long long)g_wsms * per_sm * FNW);
+    const int grid = (int)((warps + FNW - 1) / FNW);
+    wiener_fast_kernel<RW, GAIN><<<grid, FNW * 32, smem, stream>>>(tm, a);
+    count_launch();
+    return cudaGetLastError();
+}
+
+template <bool GAIN>
+cudaError_t dispatch(const Plane& p, int win, unsigned long long* wsum, const long long* wread,
+                     long long pixel_count, cudaStream_t stream) {
+    if (tma_compatible(p.src, p.spitch, p.sslice)) {
+        switch (win) {
+            case 1: return launch_fast<0, GAIN>(p, wsum, wread, pixel_count, stream);
+            case 3: return launch_fast<1, GAIN>(p, wsum, wread, pixel_count, stream);
+            case 5: return launch_fast<2, GAIN>(p, wsum, wread, pixel_count, stream);
+            case 7: return launch_fast<3, GAIN>(p, wsum, wread, pixel_count, stream);
+            default: break;
+        }
+    }
+    return launch<GAIN>(p, win, wsum, wread, pixel_count, stream);
+}
+
 }  // namespace
 
 cudaError_t launch_wiener_stats(const Plane& p, int win, unsigned long long* noise_sum,
                                 cudaStream_t stream) {
-    return launch<false>(p, win, noise_sum, nullptr, 0, stream);
+    return dispatch<false>(p, win, noise_sum, nullptr, 0, stream);
 }
 
 cudaError_t launch_wiener_gain(const Plane& p, int win, const long long* noise_sum,
                                long long pixel_count, cudaStream_t stream) {
-    return launch<true>(p, win, nullptr, noise_sum, pixel_count, stream);
+    return dispatch<true>(p, win, nullptr, noise_sum, pixel_count, stream);
 }
 
 }  // namespace hyb
