@@ -68,6 +68,9 @@ def ref():
         r.ref_rng_uniform.argtypes = [c_uint64, c_int, POINTER(c_double)]
         r.ref_rng_normal.argtypes = [c_uint64, c_int, POINTER(c_double)]
         r.ref_salt_pepper_count.argtypes = [c_int, c_int, c_double, c_double, c_uint64]
+        r.ref_rng_u64.argtypes = [c_uint64, c_int, POINTER(c_uint64)]
+        r.ref_random_image_u8.argtypes = [c_int, c_int, c_uint64, c_double, c_uint64, P]
+        r.ref_noisy_phantom_u8.argtypes = [c_int, c_int, c_uint64, P]
         r.ref_hybrid_baseline.argtypes = [P, c_int, c_int, c_int, c_int, c_int, P, POINTER(c_double),
                                           POINTER(c_double)]
         _ref = r
@@ -174,6 +177,26 @@ def ref_rng(seed, n, normal=False):
     out = (c_double * n)()
     (ref().ref_rng_normal if normal else ref().ref_rng_uniform)(seed, n, out)
     return np.frombuffer(out, dtype=np.float64).copy()
+
+
+def ref_rng_u64(seed, n):
+    out = (c_uint64 * n)()
+    ref().ref_rng_u64(seed, n, out)
+    return [int(v) for v in out]
+
+
+def ref_random_image(rows, cols, seed, density=0.0, sp_seed=0):
+    out = np.empty((rows, cols), np.uint8)
+    if ref().ref_random_image_u8(rows, cols, seed, density, sp_seed, out.ctypes.data):
+        raise ValueError(ref().ref_last_error().decode())
+    return out
+
+
+def ref_noisy_phantom(rows, cols, seed):
+    out = np.empty((rows, cols), np.uint8)
+    if ref().ref_noisy_phantom_u8(rows, cols, seed, out.ctypes.data):
+        raise ValueError(ref().ref_last_error().decode())
+    return out
 
 
 def ref_hybrid_baseline(g, smax, win, threads):

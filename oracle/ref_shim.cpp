@@ -24,6 +24,7 @@
 #include "denoise/image.hpp"
 #include "denoise/noise.hpp"
 #include "denoise/parallel.hpp"
+#include "denoise/phantom.hpp"
 #include "denoise/tiling.hpp"
 
 extern "C" {
@@ -134,6 +135,34 @@ void ref_rng_uniform(uint64_t seed, int n, double* out) {
 void ref_rng_normal(uint64_t seed, int n, double* out) {
     denoise::Rng64 rng(seed);
     for (int i = 0; i < n; ++i) out[i] = rng.normal();
+}
+
+void ref_rng_u64(uint64_t seed, int n, uint64_t* out) {
+    denoise::Rng64 rng(seed);
+    for (int i = 0; i < n; ++i) out[i] = rng.next_u64();
+}
+
+// oracles::random_image (reference proj/tests/support/oracles.hpp:18-23): Rng64(seed) uniforms,
+// quantised to the k/255 grid with lround(p * 255); then, if density > 0, add_salt_pepper
+// (proj/src/noise.cpp:40-57) at sp_seed (impulses are exactly 0 / 255).
+int ref_random_image_u8(int rows, int cols, uint64_t seed, double density, uint64_t sp_seed, uint8_t* out) {
+    return guarded([&] {
+        denoise::Rng64 rng(seed);
+        denoise::Image img(rows, cols);
+        for (double& p : img.pixels()) p = std::lround(rng.uniform01() * 255.0) / 255.0;
+        if (density > 0) img = denoise::add_salt_pepper(img, density, sp_seed);
+        from_image(img, out, (size_t)cols);
+    });
+}
+
+// degrade(make_phantom(rows, cols, seed), NoiseSpec{seed}) quantised to uint8 -- the
+// noisy_phantom fixture of proj/tests/test_parallel.cpp:21-24.
+int ref_noisy_phantom_u8(int rows, int cols, uint64_t seed, uint8_t* out) {
+    return guarded([&] {
+        denoise::NoiseSpec spec;
+        spec.seed = seed;
+        from_image(denoise::degrade(denoise::make_phantom(rows, cols, seed), spec), out, (size_t)cols);
+    });
 }
 
 // add_salt_pepper (reference proj/src/noise.cpp:40-57) on a constant image;
