@@ -7,8 +7,20 @@ PKG := paper_2005_05371_b200
 SRCS := $(PKG)/csrc/tma_host.cu $(PKG)/csrc/amf.cu $(PKG)/csrc/wiener.cu $(PKG)/csrc/capi.cu $(PKG)/csrc/phantom.cpp
 HDRS := $(PKG)/csrc/hyb_internal.cuh $(PKG)/csrc/tma.cuh $(PKG)/csrc/networks.cuh include/hybrid_cuda.h
 LIB := $(PKG)/libhybrid_cuda.so
+HOSTLIB := $(PKG)/libdenoise_cuda.so
+CXX ?= g++
+CPPTEST := tests/cpp/test_host
 
-all: $(LIB) oracle
+all: $(LIB) $(HOSTLIB) oracle $(CPPTEST)
+
+# C++ host driver with the reference's filter API (paper_2005_05371_b200/host/denoise_cuda.hpp)
+$(HOSTLIB): $(PKG)/host/denoise_cuda.cpp $(PKG)/host/denoise_cuda.hpp include/hybrid_cuda.h $(LIB)
+	$(CXX) -std=c++20 -O2 -fPIC -Wall -Wextra -shared -o $@ $(PKG)/host/denoise_cuda.cpp -L$(PKG) -lhybrid_cuda -Wl,-rpath,'$$ORIGIN'
+
+# the reference's unit tests re-expressed against the host driver (run by tests/test_cpp_host.py)
+$(CPPTEST): tests/cpp/test_host.cpp oracle/hyb_oracle.c $(HOSTLIB)
+	$(CXX) -std=c++20 -O2 -Wall -Wextra -o $@ tests/cpp/test_host.cpp -x c oracle/hyb_oracle.c -x none \
+		-L$(PKG) -ldenoise_cuda -lhybrid_cuda -Wl,-rpath,'$$ORIGIN/../../$(PKG)'
 
 $(LIB): $(SRCS) $(HDRS)
 	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRCS) 2> build_ptxas.log || (cat build_ptxas.log; exit 1)
@@ -18,7 +30,7 @@ oracle:
 	$(MAKE) -C oracle --no-print-directory
 
 clean:
-	rm -f $(LIB) build_ptxas.log
+	rm -f $(LIB) $(HOSTLIB) $(CPPTEST) build_ptxas.log
 	$(MAKE) -C oracle clean
 
 .PHONY: all oracle clean

@@ -1,0 +1,207 @@
+// denoise_cuda.cpp -- C++ host driver (reference filter API) on the libhybrid_cuda C ABI.
+#include "denoise_cuda.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <map>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/hybrid_cuda.h"
+
+namespace denoise_cuda {
+namespace {
+
+// One hyb_ctx per (host thread, device), like the reference's per-call pool (proj/src/parallel.cpp:62-65).
+struct Contexts {
+    std::map<int, hyb_ctx*> by_device;
+    ~Contexts() {
+        for (auto& kv : by_device) hyb_destroy(kv.second);
+    }
+};
+
+hyb_ctx* context(int device) {
+    thread_local Contexts ctxs;
+    auto it = ctxs.by_device.find(device);
+    if (it != ctxs.by_device.end()) return it->second;
+    int st = 0;
+    hyb_ctx* c = hyb_create(device, &st);
+    if (!c) throw std::runtime_error("libhybrid_cuda: no CUDA device " + std::to_string(device));
+    ctxs.by_device[device] = c;
+    return c;
+}
+
+void check(int status, hyb_ctx* ctx) {
+    if (status == HYB_OK) return;
+    const std::string msg = hyb_last_error(ctx);
+    if (status == HYB_EINVAL) throw std::invalid_argument(msg);
+    throw std::runtime_error("libhybrid_cuda: " + msg);
+}
+
+// uint8 view of an Image for the AMF: the k/255 grid, or a rank code when the image has at most 256
+// distinct values (order-isomorphic, exact for an order-statistics filter).
+struct Coded {
+    std::vector<uint8_t> px;
+    std::vector<double> table;  // empty: grid coding (value k/255)
+    double decode(uint8_t k) const { return table.empty() ? k / 255.0 : table[k]; }
+};
+
+bool on_grid(const Image& img, std::vector<uint8_t>* out) {
+    if (out) out->resize(img.size());
+    const auto& px = img.pixels();
+    for (std::size_t i = 0; i < px.size(); ++i) {
+        const long q = std::lround(px[i] * 255.0);
+        if (q < 0 || q > 255 || q / 255.0 != px[i]) return false;
+        if (out) (*out)[i] = static_cast<uint8_t>(q);
+    }
+    return true;
+}
+
+Coded encode_for_amf(const Image& img) {
+    Coded c;
+    if (on_grid(img, &c.px)) return c;
+    std::vector<double> vals = img.pixels();
+    std::sort(vals.begin(), vals.end());
+    vals.erase(std::unique(vals.begin(), vals.end()), vals.end());
+    if (vals.size() > 256)
+        throw std::invalid_argument("image has " + std::to_string(vals.size()) +
+                                    " distinct values off the 8-bit grid; the uint8 filter path cannot represent it");
+    c.table = vals;
+    c.px.resize(img.size());
+    const auto& px = img.pixels();
+    for (std::size_t i = 0; i < px.size(); ++i)
+        c.px[i] = static_cast<uint8_t>(std::lower_bound(vals.begin(), vals.end(), px[i]) - vals.begin());
+    return c;
+}
+
+}  // namespace
+
+Image::Image(int rows, int cols, double fill) : rows_(rows), cols_(cols) {
+    if (rows < 1 || cols < 1)
+        throw std::invalid_argument("image dimensions must be at least 1x1, got " + std::to_string(rows) + "x" +
+                                    std::to_string(cols));
+    px_.assign(static_cast<std::size_t>(rows) * static_cast<std::size_t>(cols), fill);
+}
+
+Image Image::from_pixels(int rows, int cols, std::vector<double> px) {
+    Image img(rows, cols);
+    if (px.size() != img.size())
+        throw std::invalid_argument("pixel buffer length " + std::to_string(px.size()) + " does not match " +
+                                    std::to_string(rows) + "x" + std::to_string(cols));
+    img.px_ = std::move(px);
+    return img;
+}
+
+void validate_smax(int smax) {
+    if (hyb_validate_smax(smax) != HYB_OK)
+        throw std::invalid_argument("smax must be an odd integer > 1, got " + std::to_string(smax));
+}
+
+void validate_config(const FilterConfig& config) {
+    validate_smax(config.smax);
+    if (config.parts < 1) throw std::invalid_argument("parts must be >= 1, got " + std::to_string(config.parts));
+    if (config.workers < 1)
+        throw std::invalid_argument("workers must be >= 1, got " + std::to_string(config.workers));
+}
+
+std::vector<uint8_t> to_u8(const Image& image) {
+    std::vector<uint8_t> px;
+    if (!on_grid(image, &px)) throw std::invalid_argument("image values are not on the k/255 grid");
+    return px;
+}
+
+Image from_u8(const uint8_t* px, int rows, int cols) {
+    Image img(rows, cols);
+    for (std::size_t i = 0; i < img.size(); ++i) img.pixels()[i] = px[i] / 255.0;
+    return img;
+}
+
+namespace detail {
+
+void adaptive_median_rows(const Image& src, int smax, int row_begin, int row_end, Image& dst,
+                          std::vector<int>* finalized_at) {
+    validate_smax(smax);
+    const int rows = src.rows(), cols = src.cols();
+    if (row_begin < 0 || row_end > rows || row_begin >= row_end)
+        throw std::invalid_argument("bad row range [" + std::to_string(row_begin) + ", " + std::to_string(row_end) +
+                                    ") for " + std::to_string(rows) + " rows");
+    const Coded in = encode_for_amf(src);
+    const int out_rows = row_end - row_begin;
+    std::vector<uint8_t> out((std::size_t)out_rows * cols), fin;
+    if (finalized_at) fin.resize(out.size());
+    hyb_ctx* ctx = context(0);
+    check(hyb_amf_u8(ctx, in.px.data(), cols, rows, cols, row_begin, row_end, smax, out.data(), cols,
+                     finalized_at ? fin.data() : nullptr, cols),
+          ctx);
+    if (dst.rows() != out_rows || dst.cols() != cols) dst = Image(out_rows, cols);
+    for (std::size_t i = 0; i < out.size(); ++i) dst.pixels()[i] = in.decode(out[i]);
+    if (finalized_at) finalized_at->assign(fin.begin(), fin.end());
+}
+
+}  // namespace detail
+
+Image adaptive_median_serial(const Image& image, int smax) {
+    validate_smax(smax);
+    Image out;
+    detail::adaptive_median_rows(image, smax, 0, image.rows(), out);
+    return out;
+}
+
+Image adaptive_median_parallel(const Image& image, const FilterConfig& config) {
+    validate_config(config);
+    const int rows = image.rows(), cols = image.cols();
+    if (config.parts > rows)
+        throw std::invalid_argument("parts " + std::to_string(config.parts) + " exceeds image rows " +
+                                    std::to_string(rows));
+    // band geometry of split_bands (proj/src/tiling.cpp:23-32); each band filtered from its own copy
+    const int halo = config.use_halo ? (config.smax - 1) / 2 : 0;
+    Image out(rows, cols);
+    const int base = rows / config.parts, extra = rows % config.parts;
+    int start = 0;
+    for (int i = 0; i < config.parts; ++i) {
+        const int core = base + (i < extra ? 1 : 0);
+        const int ha = std::min(halo, start), hb = std::min(halo, rows - start - core);
+        Image band(ha + core + hb, cols);
+        std::copy(image.row(start - ha), image.row(start - ha) + band.size(), band.pixels().begin());
+        Image res;
+        detail::adaptive_median_rows(band, config.smax, ha, ha + core, res);
+        std::copy(res.pixels().begin(), res.pixels().end(), out.row(start));
+        start += core;
+    }
+    return out;
+}
+
+Image wiener_local(const Image& filtered, int window, double* sigma2) {
+    const std::vector<uint8_t> f = to_u8(filtered);
+    std::vector<uint8_t> y(f.size());
+    int64_t w = 0;
+    hyb_ctx* ctx = context(0);
+    check(hyb_wiener_u8(ctx, f.data(), filtered.cols(), filtered.rows(), filtered.cols(), window, y.data(),
+                        filtered.cols(), &w),
+          ctx);
+    if (sigma2) {
+        const double n = (double)window * window;
+        *sigma2 = (double)w / (n * n * (double)f.size()) / (255.0 * 255.0);
+    }
+    return from_u8(y.data(), filtered.rows(), filtered.cols());
+}
+
+HybridResult hybrid_denoise(const Image& noisy, const FilterConfig& config) {
+    validate_config(config);
+    const std::vector<uint8_t> g = to_u8(noisy);
+    std::vector<uint8_t> y(g.size());
+    hyb_ctx* ctx = context(config.device);
+    hyb_stats st{};
+    check(hyb_hybrid_u8(ctx, g.data(), noisy.cols(), noisy.rows(), noisy.cols(), config.smax, config.wiener_window,
+                        config.parts, y.data(), noisy.cols(), &st),
+          ctx);
+    HybridResult r;
+    r.image = from_u8(y.data(), noisy.rows(), noisy.cols());
+    r.sigma2 = st.sigma2;
+    r.t_adaptive = st.t_adaptive;
+    r.t_wiener = st.t_wiener;
+    r.noise_sum = st.noise_sum;
+    return r;
+}
+
+}  // namespace denoise_cuda

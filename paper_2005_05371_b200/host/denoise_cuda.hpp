@@ -1,0 +1,95 @@
+// denoise_cuda.hpp -- C++ host driver with the reference's filter API, on libhybrid_cuda.
+//
+// Mirrors the reference's `namespace denoise` signatures for the hot path
+// (proj/include/denoise/{image,adaptive_median,parallel,tiling,pipeline}.hpp) so a caller of the
+// reference can switch by changing the namespace: same names, argument meaning and exception
+// types (std::invalid_argument with the reference's message texts, std::runtime_error for device
+// failures).  Pixels travel to the GPU as uint8: the reference's Image doubles are k/255 values
+// (proj/src/pgm_io.cpp:73,88); images with <= 256 distinct values that are not on that grid are
+// rank-compressed, which is exact for the AMF (it only compares and selects).  The Wiener stage is
+// the north_star's local-statistics W1 (the reference's stage-2 slot, proj/src/pipeline.cpp:45-53).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <vector>
+
+namespace denoise_cuda {
+
+/// Row-major double raster, reference proj/include/denoise/image.hpp:13-50.
+class Image {
+public:
+    Image() = default;
+    Image(int rows, int cols, double fill = 0.0);
+    static Image from_pixels(int rows, int cols, std::vector<double> px);
+
+    int rows() const noexcept { return rows_; }
+    int cols() const noexcept { return cols_; }
+    std::size_t size() const noexcept { return px_.size(); }
+    double& at(int r, int c) noexcept { return px_[idx(r, c)]; }
+    double at(int r, int c) const noexcept { return px_[idx(r, c)]; }
+    double* row(int r) noexcept { return px_.data() + idx(r, 0); }
+    const double* row(int r) const noexcept { return px_.data() + idx(r, 0); }
+    std::vector<double>& pixels() noexcept { return px_; }
+    const std::vector<double>& pixels() const noexcept { return px_; }
+    bool same_size(const Image& o) const noexcept { return rows_ == o.rows_ && cols_ == o.cols_; }
+    friend bool operator==(const Image&, const Image&) = default;
+
+private:
+    std::size_t idx(int r, int c) const noexcept {
+        return static_cast<std::size_t>(r) * static_cast<std::size_t>(cols_) + static_cast<std::size_t>(c);
+    }
+    int rows_ = 0;
+    int cols_ = 0;
+    std::vector<double> px_;
+};
+
+/// validate_smax -- proj/src/adaptive_median.cpp:11-16.
+void validate_smax(int smax);
+
+/// FilterConfig -- proj/include/denoise/parallel.hpp:13-19 (+ the W1 window, + the device).
+struct FilterConfig {
+    int smax = 11;
+    int parts = 1;
+    int workers = 1;
+    bool use_halo = true;
+    int wiener_window = 3;
+    int device = 0;
+};
+
+/// validate_config -- proj/src/parallel.cpp:16-25.
+void validate_config(const FilterConfig& config);
+
+/// adaptive_median_serial -- proj/include/denoise/adaptive_median.hpp:35.
+Image adaptive_median_serial(const Image& image, int smax);
+
+namespace detail {
+/// adaptive_median_rows -- proj/include/denoise/adaptive_median.hpp:47-48.
+void adaptive_median_rows(const Image& src, int smax, int row_begin, int row_end, Image& dst,
+                          std::vector<int>* finalized_at = nullptr);
+}  // namespace detail
+
+/// adaptive_median_parallel -- proj/include/denoise/parallel.hpp:31 (bands = strips on the GPU).
+Image adaptive_median_parallel(const Image& image, const FilterConfig& config);
+
+/// W1 local-statistics Wiener; *sigma2 (nullable) receives nu / 255^2.
+Image wiener_local(const Image& filtered, int window, double* sigma2 = nullptr);
+
+/// HybridResult -- proj/include/denoise/pipeline.hpp:12-18 (+ the exact noise sum W).
+struct HybridResult {
+    Image image;
+    double sigma2 = 0.0;
+    double t_adaptive = 0.0;
+    double t_wiener = 0.0;
+    double t_stretch = 0.0;
+    long long noise_sum = 0;
+};
+
+/// hybrid_denoise stages 1-2 -- proj/src/pipeline.cpp:23-53 (AMF, then W1 in the Wiener slot).
+HybridResult hybrid_denoise(const Image& noisy, const FilterConfig& config);
+
+/// uint8 <-> reference doubles (k/255).  to_u8 throws std::invalid_argument off the grid.
+std::vector<uint8_t> to_u8(const Image& image);
+Image from_u8(const uint8_t* px, int rows, int cols);
+
+}  // namespace denoise_cuda

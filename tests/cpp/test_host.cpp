@@ -1,0 +1,163 @@
+// test_host.cpp -- the reference's hot-path unit tests re-expressed against the C++ host driver
+// (denoise_cuda, on the GPU) with the C oracle (oracle/hyb_oracle.c) as the checker.  Mirrors
+// proj/tests/test_adaptive_median.cpp and proj/tests/test_parallel.cpp case by case.
+// Exit code = number of failed checks (like the reference acceptance gate).
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../paper_2005_05371_b200/host/denoise_cuda.hpp"
+
+extern "C" {
+int hyb_oracle_amf_u8(const uint8_t*, size_t, int, int, int, int, int, uint8_t*, size_t, uint8_t*, size_t);
+int hyb_oracle_hybrid_u8(const uint8_t*, size_t, int, int, int, int, uint8_t*, uint8_t*, size_t, int64_t*);
+int hyb_make_phantom_u8(int, int, int, double, double, uint64_t, uint8_t*, size_t);
+}
+
+using namespace denoise_cuda;
+
+static int g_fail = 0, g_checks = 0;
+#define CHECK(cond)                                                            \
+    do {                                                                       \
+        ++g_checks;                                                            \
+        if (!(cond)) {                                                         \
+            ++g_fail;                                                          \
+            std::printf("FAIL %s:%d  %s\n", __FILE__, __LINE__, #cond);        \
+        }                                                                      \
+    } while (0)
+#define CHECK_THROWS_AS(expr, T)                                               \
+    do {                                                                       \
+        bool thrown_ = false;                                                  \
+        try {                                                                  \
+            (void)(expr);                                                      \
+        } catch (const T&) {                                                   \
+            thrown_ = true;                                                    \
+        } catch (...) {                                                        \
+        }                                                                      \
+        CHECK(thrown_ && #expr);                                               \
+    } while (0)
+
+static Image random_grid_image(int rows, int cols, uint64_t seed, double sp) {
+    std::mt19937_64 gen(seed);
+    Image img(rows, cols);
+    for (double& p : img.pixels()) {
+        const double u = (gen() >> 11) * 0x1.0p-53;
+        const double v = (gen() >> 11) * 0x1.0p-53;
+        p = std::lround(u * 255.0) / 255.0;
+        if (v < sp / 2) p = 0.0;
+        else if (v < sp) p = 1.0;
+    }
+    return img;
+}
+
+static Image oracle_amf(const Image& img, int smax) {
+    std::vector<uint8_t> in = to_u8(img), out(in.size());
+    hyb_oracle_amf_u8(in.data(), img.cols(), img.rows(), img.cols(), 0, img.rows(), smax, out.data(), img.cols(),
+                      nullptr, 0);
+    return from_u8(out.data(), img.rows(), img.cols());
+}
+
+int main() {
+    // validate_smax (proj/tests/test_adaptive_median.cpp:17-24)
+    validate_smax(3);
+    validate_smax(11);
+    CHECK_THROWS_AS(validate_smax(4), std::invalid_argument);
+    CHECK_THROWS_AS(validate_smax(1), std::invalid_argument);
+    CHECK_THROWS_AS(validate_smax(0), std::invalid_argument);
+    CHECK_THROWS_AS(validate_smax(-3), std::invalid_argument);
+    try {
+        validate_smax(4);
+    } catch (const std::invalid_argument& e) {
+        CHECK(std::string(e.what()).find("odd integer > 1") != std::string::npos);
+    }
+
+    // constants are a fixed point (:61-65)
+    {
+        Image flat(9, 9, 0.7);
+        CHECK(adaptive_median_serial(flat, 11) == flat);
+        CHECK_THROWS_AS(adaptive_median_serial(flat, 4), std::invalid_argument);
+    }
+    // a lone impulse on a gradient is replaced by the window median (:67-78): off-grid values,
+    // rank-coded by the host driver
+    {
+        Image img(5, 5);
+        for (int r = 0; r < 5; ++r)
+            for (int c = 0; c < 5; ++c) img.at(r, c) = 0.1 * (r + c) + 0.1;
+        img.at(2, 2) = 1.0;
+        Image out = adaptive_median_serial(img, 3);
+        CHECK(std::fabs(out.at(2, 2) - 0.5) < 1e-12);
+        CHECK(out.at(1, 2) == img.at(1, 2));
+        CHECK(out.at(3, 1) == img.at(3, 1));
+    }
+    // oracle equivalence on random grid images (:80-96)
+    for (int trial = 0; trial < 20; ++trial) {
+        const int rows = 8 + trial % 25, cols = 8 + (trial * 7) % 25;
+        Image img = random_grid_image(rows, cols, 1000 + trial, trial % 2 == 0 ? 0.2 : 0.0);
+        for (int smax : {3, 5, 7, 11}) CHECK(adaptive_median_serial(img, smax) == oracle_amf(img, smax));
+    }
+    // finalized_at agrees across smax (:108-130)
+    {
+        Image img = random_grid_image(20, 20, 70, 0.25);
+        Image small, big;
+        std::vector<int> fs, fb;
+        detail::adaptive_median_rows(img, 5, 0, 20, small, &fs);
+        detail::adaptive_median_rows(img, 11, 0, 20, big, &fb);
+        for (std::size_t i = 0; i < img.size(); ++i) {
+            if (fs[i] != 0) {
+                CHECK(fs[i] == 3 || fs[i] == 5);
+                CHECK(fb[i] == fs[i]);
+                CHECK(big.pixels()[i] == small.pixels()[i]);
+            }
+            if (fb[i] == 0) CHECK(big.pixels()[i] == img.pixels()[i]);
+        }
+    }
+    // parallel: validate_config, parts > rows, every parts x workers == serial (test_parallel.cpp)
+    {
+        FilterConfig c;
+        c.smax = 4;
+        CHECK_THROWS_AS(validate_config(c), std::invalid_argument);
+        c.smax = 3;
+        c.parts = 0;
+        CHECK_THROWS_AS(validate_config(c), std::invalid_argument);
+        Image img = random_grid_image(8, 16, 1, 0.1);
+        c.parts = 9;
+        CHECK_THROWS_AS(adaptive_median_parallel(img, c), std::invalid_argument);
+        Image big = random_grid_image(64, 64, 3, 0.1);
+        for (int smax : {3, 11}) {
+            const Image serial = adaptive_median_serial(big, smax);
+            for (int parts : {2, 3, 4, 8})
+                for (int workers : {1, 4}) {
+                    FilterConfig cfg;
+                    cfg.smax = smax;
+                    cfg.parts = parts;
+                    cfg.workers = workers;
+                    CHECK(adaptive_median_parallel(big, cfg) == serial);
+                }
+        }
+    }
+    // hybrid: AMF + W1 equals the oracle, and parts do not change the output
+    {
+        const int rows = 300, cols = 260;
+        std::vector<uint8_t> g((size_t)rows * cols), y(g.size()), work(g.size());
+        hyb_make_phantom_u8(rows, cols, 8, 15.0, 0.2, 5, g.data(), cols);
+        int64_t w = 0;
+        hyb_oracle_hybrid_u8(g.data(), cols, rows, cols, 7, 3, work.data(), y.data(), cols, &w);
+        const Image noisy = from_u8(g.data(), rows, cols);
+        for (int parts : {1, 2, 5}) {
+            FilterConfig cfg;
+            cfg.smax = 7;
+            cfg.parts = parts;
+            cfg.wiener_window = 3;
+            HybridResult r = hybrid_denoise(noisy, cfg);
+            CHECK(r.noise_sum == w);
+            CHECK(r.image == from_u8(y.data(), rows, cols));
+            CHECK(r.sigma2 > 0);
+        }
+    }
+    std::printf("%d checks, %d failed\n", g_checks, g_fail);
+    return g_fail;
+}
