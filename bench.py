@@ -246,7 +246,9 @@ def run_gpu(args, cfg, c):
             ms = float(t.item())
         return ms
 
-    for i in range(args.warmup):
+    # untimed warm-up: at least W steps and two passes over the rotating buffers (the library
+    # captures a CUDA graph per buffer pair on its second use and replays it afterwards)
+    for i in range(max(args.warmup, 2 * nbuf)):
         step(i)
     torch.cuda.synchronize()
     l0 = ctx.launches()

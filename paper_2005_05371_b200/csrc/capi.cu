@@ -6,6 +6,8 @@
 // wiener.cu; there is no CPU fallback -- a missing device or a failed launch is an error.
 #include <algorithm>
 #include <atomic>
+#include <map>
+#include <tuple>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -61,6 +63,18 @@ struct hyb_ctx {
     long long* host_w = nullptr;       // pinned readback of noise sums
     size_t host_w_n = 0;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaStream_t copy = nullptr;       // host<->device staging stream of the pipelined path
+    // CUDA-graph cache of hyb_hybrid_u8 calls: a key seen once is captured on its second call and
+    // replayed afterwards (one launch per step instead of ~10-30 API calls).
+    using GraphKey = std::tuple<const void*, void*, size_t, size_t, int, int, int, int, int, cudaStream_t>;
+    struct Graph {
+        cudaGraphExec_t exec = nullptr;
+        long long kernels = 0;
+    };
+    std::map<GraphKey, Graph> graphs;
+    std::map<GraphKey, int> graph_seen;
+    static constexpr int kMaxChunks = 8;
+    cudaEvent_t ev_h2d[kMaxChunks] = {}, ev_gain[kMaxChunks] = {};
 };
 
 namespace {
@@ -130,7 +144,9 @@ int check_pitch(hyb_ctx* ctx, size_t pitch, int cols, const char* what) {
     return HYB_OK;
 }
 
-size_t round_pitch(int cols) { return ((size_t)cols + 127) & ~(size_t)127; }
+// Pitch of context buffers: 16-byte multiple (TMA), so images with cols % 16 == 0 stay contiguous
+// and host<->device staging is a single linear copy.
+size_t round_pitch(int cols) { return ((size_t)cols + 15) & ~(size_t)15; }
 
 int ensure_host_w(hyb_ctx* ctx, size_t n) {
     if (ctx->host_w_n >= n) return HYB_OK;
@@ -144,6 +160,8 @@ int ensure_host_w(hyb_ctx* ctx, size_t n) {
 
 // Copies rows x cols bytes between two pitched buffers (any direction) on the ctx stream.
 cudaError_t copy2d(hyb_ctx* ctx, void* dst, size_t dp, const void* src, size_t sp, int cols, int rows) {
+    if (dp == (size_t)cols && sp == (size_t)cols)  // both contiguous: one linear DMA
+        return cudaMemcpyAsync(dst, src, (size_t)cols * rows, cudaMemcpyDefault, ctx->stream);
     return cudaMemcpy2DAsync(dst, dp, src, sp, (size_t)cols, (size_t)rows, cudaMemcpyDefault, ctx->stream);
 }
 
@@ -231,6 +249,71 @@ int hybrid_device(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int co
     return HYB_OK;
 }
 
+// Host buffers, one GPU, parts == 1: the image moves in row chunks so the PCIe transfers overlap
+// the kernels.  Copy stream: H2D chunk k -> ev_h2d[k].  Compute stream: AMF of chunk k once the
+// chunks holding its rows + rA halo have landed, statistics of chunk k-1 (its f halo rows are now
+// final); after the single noise reduction, gain of chunk k -> ev_gain[k] while the copy stream
+// brings chunk k-1 back.  The W dependence keeps every gain after every statistic, so the
+// critical path is H2D + last AMF/stats + first gain + D2H instead of H2D + all kernels + D2H.
+int hybrid_host_pipelined(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int cols, int smax, int win,
+                          uint8_t* y, size_t y_pitch, bool timed) {
+    const int rA = (smax - 1) / 2, rW = (win - 1) / 2;
+    // Chunking pays only when the copies dominate: each chunk adds the fixed latency of its kernels,
+    // so images below ~8 MB move in one piece.
+    const long long bytes = (long long)rows * cols;
+    const int want = bytes < (8ll << 20) ? 1 : 4;
+    const int K = std::max(1, std::min(want, rows / std::max(64, 2 * (rA + rW) + 1)));
+    const size_t pp = round_pitch(cols);
+    HYB_CHECK(ctx->in.ensure(pp * rows));
+    HYB_CHECK(ctx->f.ensure(pp * rows));
+    HYB_CHECK(ctx->out.ensure(pp * rows));
+    HYB_CHECK(ctx->wsum.ensure(sizeof(long long)));
+    unsigned long long* W = reinterpret_cast<unsigned long long*>(ctx->wsum.ptr);
+    std::vector<int> a(K + 1);
+    for (int k = 0; k <= K; ++k) a[k] = (int)((long long)rows * k / K);
+    cudaStream_t cs = ctx->stream, xs = ctx->copy;
+    auto cp = [&](void* dst, size_t dp, const void* src, size_t sp, int nrows) {
+        if (dp == (size_t)cols && sp == (size_t)cols)
+            return cudaMemcpyAsync(dst, src, (size_t)cols * nrows, cudaMemcpyDefault, xs);
+        return cudaMemcpy2DAsync(dst, dp, src, sp, (size_t)cols, (size_t)nrows, cudaMemcpyDefault, xs);
+    };
+    if (timed) HYB_CHECK(cudaEventRecord(ctx->ev[3], cs));
+    HYB_CHECK(cudaEventRecord(ctx->ev_gain[0], cs));  // copy stream starts after earlier compute-stream work
+    HYB_CHECK(cudaStreamWaitEvent(xs, ctx->ev_gain[0], 0));
+    for (int k = 0; k < K; ++k) {
+        HYB_CHECK(cp(ctx->in.ptr + (size_t)a[k] * pp, pp, g + (size_t)a[k] * pitch, pitch, a[k + 1] - a[k]));
+        HYB_CHECK(cudaEventRecord(ctx->ev_h2d[k], xs));
+    }
+    HYB_CHECK(cudaMemsetAsync(W, 0, sizeof(long long), cs));
+    if (timed) HYB_CHECK(cudaEventRecord(ctx->ev[0], cs));
+    auto stats = [&](int k) -> cudaError_t {
+        hyb::Plane w{ctx->f.ptr, pp, 0, nullptr, 0, 0, rows, cols, a[k], a[k + 1], 1};
+        return hyb::launch_wiener_stats(w, win, W, cs);
+    };
+    for (int k = 0; k < K; ++k) {
+        int need = k;  // last chunk holding input rows < a[k+1] + rA
+        while (need + 1 < K && a[need + 1] < std::min(rows, a[k + 1] + rA)) ++need;
+        HYB_CHECK(cudaStreamWaitEvent(cs, ctx->ev_h2d[need], 0));
+        hyb::Plane am{ctx->in.ptr, pp, 0, ctx->f.ptr + (size_t)a[k] * pp, pp, 0, rows, cols, a[k], a[k + 1], 1};
+        HYB_CHECK(run_amf(ctx, am, smax, nullptr, 0, 0));
+        if (k >= 1 && a[k + 1] - a[k] >= rW) HYB_CHECK(stats(k - 1));
+        else if (k >= 1) return fail(ctx, HYB_EINVAL, "chunk thinner than the Wiener halo");
+    }
+    HYB_CHECK(stats(K - 1));
+    if (timed) HYB_CHECK(cudaEventRecord(ctx->ev[1], cs));
+    for (int k = 0; k < K; ++k) {
+        hyb::Plane w{ctx->f.ptr, pp, 0, ctx->out.ptr + (size_t)a[k] * pp, pp, 0, rows, cols, a[k], a[k + 1], 1};
+        HYB_CHECK(hyb::launch_wiener_gain(w, win, reinterpret_cast<const long long*>(W), (long long)rows * cols, cs));
+        HYB_CHECK(cudaEventRecord(ctx->ev_gain[k], cs));
+        HYB_CHECK(cudaStreamWaitEvent(xs, ctx->ev_gain[k], 0));
+        HYB_CHECK(cp(y + (size_t)a[k] * y_pitch, y_pitch, ctx->out.ptr + (size_t)a[k] * pp, pp, a[k + 1] - a[k]));
+    }
+    if (timed) HYB_CHECK(cudaEventRecord(ctx->ev[2], cs));
+    HYB_CHECK(cudaEventRecord(ctx->ev_h2d[0], xs));  // compute stream resumes after the last D2H
+    HYB_CHECK(cudaStreamWaitEvent(cs, ctx->ev_h2d[0], 0));
+    return HYB_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -248,6 +331,16 @@ hyb_ctx* hyb_create(int device, int* status) {
     e = cudaSetDevice(device);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking);
     for (int i = 0; i < 4 && e == cudaSuccess; ++i) e = cudaEventCreate(&ctx->ev[i]);
+    if (e != cudaSuccess) {
+        if (status) *status = HYB_ECUDA;
+        delete ctx;
+        return nullptr;
+    }
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking);
+    for (int i = 0; i < hyb_ctx::kMaxChunks && e == cudaSuccess; ++i) {
+        e = cudaEventCreateWithFlags(&ctx->ev_h2d[i], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_gain[i], cudaEventDisableTiming);
+    }
     if (e != cudaSuccess) {
         if (status) *status = HYB_ECUDA;
         delete ctx;
@@ -274,6 +367,13 @@ int hyb_destroy(hyb_ctx* ctx) {
     if (ctx->host_w) cudaFreeHost(ctx->host_w);
     for (auto& ev : ctx->ev)
         if (ev) cudaEventDestroy(ev);
+    for (auto& kv : ctx->graphs)
+        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    for (auto& ev : ctx->ev_h2d)
+        if (ev) cudaEventDestroy(ev);
+    for (auto& ev : ctx->ev_gain)
+        if (ev) cudaEventDestroy(ev);
+    if (ctx->copy) cudaStreamDestroy(ctx->copy);
     if (ctx->own) cudaStreamDestroy(ctx->own);
     delete ctx;
     return HYB_OK;
@@ -493,8 +593,59 @@ int hyb_wiener_u8(hyb_ctx* ctx, const uint8_t* f, size_t pitch, int rows, int co
     return HYB_OK;
 }
 
+static int hybrid_u8_impl(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int cols, int smax,
+                          int win, int parts, uint8_t* y, size_t y_pitch, hyb_stats* stats, bool capturing);
+
 int hyb_hybrid_u8(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int cols, int smax,
                   int win, int parts, uint8_t* y, size_t y_pitch, hyb_stats* stats) {
+    if (!ctx) return HYB_EINVAL;
+    // Untimed calls on device buffers or pinned host buffers replay a cached CUDA graph.
+    cudaPointerAttributes ga{}, ya{};
+    const bool gok = g && cudaPointerGetAttributes(&ga, g) == cudaSuccess;
+    const bool yok = y && cudaPointerGetAttributes(&ya, y) == cudaSuccess;
+    cudaGetLastError();
+    const bool graphable = !stats && gok && yok && ga.type != cudaMemoryTypeUnregistered &&
+                           ya.type != cudaMemoryTypeUnregistered && ctx->stream != nullptr;
+    if (!graphable) return hybrid_u8_impl(ctx, g, pitch, rows, cols, smax, win, parts, y, y_pitch, stats, false);
+    const hyb_ctx::GraphKey key{g, y, pitch, y_pitch, rows, cols, smax, win, parts, ctx->stream};
+    auto it = ctx->graphs.find(key);
+    if (it == ctx->graphs.end()) {
+        int& seen = ctx->graph_seen[key];
+        if (seen++ == 0)  // first use: plain run (allocates every buffer the sequence needs)
+            return hybrid_u8_impl(ctx, g, pitch, rows, cols, smax, win, parts, y, y_pitch, nullptr, false);
+        HYB_CHECK(cudaSetDevice(ctx->device));
+        HYB_CHECK(cudaStreamSynchronize(ctx->stream));
+        const long long k0 = hyb::g_launches.load();
+        HYB_CHECK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+        int st = hybrid_u8_impl(ctx, g, pitch, rows, cols, smax, win, parts, y, y_pitch, nullptr, true);
+        cudaGraph_t graph = nullptr;
+        cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
+        if (st) {
+            if (graph) cudaGraphDestroy(graph);
+            return st;
+        }
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaStreamEndCapture");
+        hyb_ctx::Graph gr;
+        e = cudaGraphInstantiate(&gr.exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaGraphInstantiate");
+        gr.kernels = hyb::g_launches.load() - k0;
+        hyb::g_launches.fetch_sub(gr.kernels);  // counted again at each replay
+        if (ctx->graphs.size() >= 4096) {
+            for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second.exec);
+            ctx->graphs.clear();
+        }
+        it = ctx->graphs.emplace(key, gr).first;
+    }
+    HYB_CHECK(cudaGraphLaunch(it->second.exec, ctx->stream));
+    hyb::g_launches.fetch_add(it->second.kernels);
+    if (ga.type != cudaMemoryTypeDevice || ya.type != cudaMemoryTypeDevice)
+        HYB_CHECK(cudaStreamSynchronize(ctx->stream));
+    return HYB_OK;
+}
+
+static int hybrid_u8_impl(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int cols, int smax,
+                          int win, int parts, uint8_t* y, size_t y_pitch, hyb_stats* stats, bool capturing) {
     if (!ctx) return HYB_EINVAL;
     int st;
     if ((st = check_smax(ctx, smax)) || (st = check_win(ctx, win)) || (st = check_dims(ctx, rows, cols)) ||
@@ -509,6 +660,29 @@ int hyb_hybrid_u8(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int co
     const bool dg = is_device_ptr(g) && hyb::tma_compatible(g, pitch, 0), dy = is_device_ptr(y);
     const size_t pp = round_pitch(cols);
     const bool timed = stats != nullptr;
+    if (!dg && !dy && !is_device_ptr(g) && parts == 1) {
+        if ((st = hybrid_host_pipelined(ctx, g, pitch, rows, cols, smax, win, y, y_pitch, timed))) return st;
+        if (timed) {
+            if ((st = ensure_host_w(ctx, 1))) return st;
+            HYB_CHECK(cudaMemcpyAsync(ctx->host_w, ctx->wsum.ptr, sizeof(long long), cudaMemcpyDeviceToHost,
+                                      ctx->stream));
+        }
+        if (!capturing) HYB_CHECK(cudaStreamSynchronize(ctx->stream));
+        if (timed) {
+            float am = 0, w = 0, t = 0;
+            HYB_CHECK(cudaEventElapsedTime(&am, ctx->ev[0], ctx->ev[1]));
+            HYB_CHECK(cudaEventElapsedTime(&w, ctx->ev[1], ctx->ev[2]));
+            HYB_CHECK(cudaEventElapsedTime(&t, ctx->ev[3], ctx->ev[2]));
+            const double n = (double)win * win;
+            stats->noise_sum = ctx->host_w[0];
+            stats->pixel_count = (int64_t)rows * cols;
+            stats->sigma2 = (double)stats->noise_sum / (n * n * (double)stats->pixel_count) / (255.0 * 255.0);
+            stats->t_adaptive = am * 1e-3;  // AMF + statistics (interleaved with the upload)
+            stats->t_wiener = w * 1e-3;     // gains (interleaved with the download)
+            stats->t_total = t * 1e-3;
+        }
+        return HYB_OK;
+    }
     if (timed) HYB_CHECK(cudaEventRecord(ctx->ev[3], ctx->stream));
     const uint8_t* s = g;
     size_t sp = pitch;
@@ -532,7 +706,7 @@ int hyb_hybrid_u8(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int co
         HYB_CHECK(cudaMemcpyAsync(ctx->host_w, ctx->wsum.ptr, sizeof(long long), cudaMemcpyDeviceToHost,
                                   ctx->stream));
     }
-    if (!dg || !dy || timed) HYB_CHECK(cudaStreamSynchronize(ctx->stream));
+    if ((!dg || !dy || timed) && !capturing) HYB_CHECK(cudaStreamSynchronize(ctx->stream));
     if (timed) {
         float a = 0, w = 0, t = 0;
         HYB_CHECK(cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]));
