@@ -738,7 +738,7 @@ cudaError_t launch_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, si
         // grid sized for the worst case of this level, capped at a few waves (grid-stride loops)
         const long long items = (k <= 7) ? (npix + 1) / 2 : npix;
         const int blocks =
-            (int)std::max<long long>(1, std::min<long long>((items + 255) / 256, (long long)g_num_sms * 8));
+            (int)std::max<long long>(1, std::min<long long>((items + 255) / 256, (long long)g_num_sms * 4));
         switch (k) {
             case 5: amf_grow_pair_kernel<5><<<blocks, 256, 0, stream>>>(g); break;
             case 7: amf_grow_pair_kernel<7><<<blocks, 256, 0, stream>>>(g); break;

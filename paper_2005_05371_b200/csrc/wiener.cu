@@ -273,6 +273,42 @@ __device__ __forceinline__ void hsums(uint32_t w0, uint32_t w1, uint32_t w2, uin
     }
 }
 
+// Horizontal window sum of f only (statistics pass); window bytes beyond N get weight 0.
+template <int RW, int I>
+__device__ __forceinline__ uint32_t hsum1(uint32_t w0, uint32_t w1, uint32_t w2) {
+    constexpr int N = 2 * RW + 1;
+    constexpr int S = 4 + I - RW;
+    if (N == 1) return bytes4<S>(w0, w1, w2) & 0xFFu;
+    if (N == 3) return __dp4a(bytes4<S>(w0, w1, w2), 0x00010101u, 0u);
+    constexpr uint32_t hw = N == 5 ? 0x00000001u : 0x00010101u;
+    return __dp4a(bytes4<S + 4>(w0, w1, w2), hw, __dp4a(bytes4<S>(w0, w1, w2), 0x01010101u, 0u));
+}
+
+// Number of (output position p in [lo, hi), offset d in [-RW, RW]) pairs whose clamped coordinate
+// clamp(p + d, 0, n - 1) equals r: how many output windows cover row (or column) r.
+__device__ __forceinline__ int win_count(int r, int lo, int hi, int n, int RW) {
+    int cnt = 0;
+    for (int d = -RW; d <= RW; ++d) {
+        int plo, phi;
+        if (n == 1) {
+            plo = lo;
+            phi = hi - 1;
+        } else if (r == 0) {
+            plo = lo;
+            phi = -d;
+        } else if (r == n - 1) {
+            plo = n - 1 - d;
+            phi = hi - 1;
+        } else {
+            plo = phi = r - d;
+        }
+        plo = max(plo, lo);
+        phi = min(phi, hi - 1);
+        cnt += max(0, phi - plo + 1);
+    }
+    return cnt;
+}
+
 template <int RW, bool GAIN>
 __global__ void __launch_bounds__(FNW * 32) wiener_fast_kernel(const __grid_constant__ CUtensorMap tm,
                                                                const __grid_constant__ FastArgs a) {
@@ -314,7 +350,8 @@ __global__ void __launch_bounds__(FNW * 32) wiener_fast_kernel(const __grid_cons
     constexpr int n = N * N;
     long long W = 0;
     int wq32 = 0;  // floor(W / P), clamped: V <= wq32 <=> V P <= W
-    float kn = 0.f;
+    float kn = 0.f, kq = 0.f;
+    const float inv_n = 1.0f / (float)NN;
     if (GAIN) {
         W = a.wread[0];  // per-slice values are re-read below when n_slices > 1
     }
@@ -332,6 +369,7 @@ __global__ void __launch_bounds__(FNW * 32) wiener_fast_kernel(const __grid_cons
             const long long wq = W / a.pixel_count;
             wq32 = wq > 0x7FFFFFFFll ? 0x7FFFFFFF : (int)wq;
             kn = (float)((double)W / ((double)a.pixel_count * (double)n));
+            kq = (float)((double)W / (double)a.pixel_count);
             zprev = z;
         }
         if (!GAIN && z != zprev) {
@@ -369,42 +407,109 @@ __global__ void __launch_bounds__(FNW * 32) wiener_fast_kernel(const __grid_cons
             __syncwarp();
         }
 
-        // ---- sliding window sums: lane = columns 4 lane .. 4 lane + 3 ----
-        // s += hsums(row rr) - hsums(row rr - N): the leaving row is re-read from the tile rather
-        // than kept in a register ring (smaller code and register footprint, no unroll by N).
         const int c = 4 * lane;
         const int col_lim = a.cols - x0, row_lim = a.row_end - y0;
-        uint32_t s1[4] = {0, 0, 0, 0}, s2[4] = {0, 0, 0, 0};
         const uint32_t* base = reinterpret_cast<const uint32_t*>(T + FCP + c - 4);
-        auto add_row = [&](int rr, bool sub) {
-            const uint32_t* rp = base + rr * (FBS / 4);
-            const uint32_t w0 = rp[0], w1 = rp[1], w2 = rp[2];
-            uint32_t h1[4], h2[4];
-            hsums<RW, 0>(w0, w1, w2, h1[0], h2[0]);
-            hsums<RW, 1>(w0, w1, w2, h1[1], h2[1]);
-            hsums<RW, 2>(w0, w1, w2, h1[2], h2[2]);
-            hsums<RW, 3>(w0, w1, w2, h1[3], h2[3]);
+        if (!GAIN) {
+            // ---- statistics: W = n * sum_p S2(p) - sum_p S1(p)^2 with sum_p S2(p) = sum_q f(q)^2 WR(q_r) WC(q_c)
+            // (WR / WC = how many output windows cover a row / column, clamping included), so only S1
+            // needs a per-pixel box sum.  Each image pixel's f^2 is owned by exactly one tile: its output
+            // rows, plus the RW halo rows outside the output range for the first / last tile.
+            uint32_t wc[4];
+            bool wc_full = true;
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                s1[i] = sub ? s1[i] - h1[i] : s1[i] + h1[i];
-                s2[i] = sub ? s2[i] - h2[i] : s2[i] + h2[i];
+                const int cc = x0 + c + i;
+                wc[i] = cc < a.cols ? (uint32_t)win_count(cc, 0, a.cols, a.cols, RW) : 0u;
+                wc_full &= wc[i] == (uint32_t)N;
             }
-        };
+            const int own_lo = (y0 == a.row_begin) ? max(0, a.row_begin - RW) : y0;
+            const int own_hi = (y0 + FH >= a.row_end) ? min(a.rows, a.row_end + RW) : y0 + FH;
+            uint32_t r1[N][4], s1[4] = {0, 0, 0, 0};
+            long long tile_sq = 0, tile_s1sq = 0;
+            auto take_row = [&](int rr, uint32_t (&h)[4]) {
+                const uint32_t* rp = base + rr * (FBS / 4);
+                const uint32_t w0 = rp[0], w1 = rp[1], w2 = rp[2];
+                h[0] = hsum1<RW, 0>(w0, w1, w2);
+                h[1] = hsum1<RW, 1>(w0, w1, w2);
+                h[2] = hsum1<RW, 2>(w0, w1, w2);
+                h[3] = hsum1<RW, 3>(w0, w1, w2);
+                const int r = y0 - RW + rr;  // image row of this tile row
+                if (r >= own_lo && r < own_hi) {
+                    const bool interior = r - RW >= max(a.row_begin, 0) && r + RW < min(a.row_end, a.rows);
+                    const uint32_t wr = interior ? (uint32_t)N : (uint32_t)win_count(r, a.row_begin, a.row_end, a.rows, RW);
+                    uint32_t q;
+                    if (wc_full) {
+                        q = (uint32_t)N * __dp4a(w1, w1, 0u);
+                    } else {
+                        q = 0;
 #pragma unroll
-        for (int rr = 0; rr < N - 1; ++rr) add_row(rr, false);
-        uint8_t* drow = GAIN ? a.dst + (size_t)z * a.dslice + (size_t)(y0 - a.row_begin) * a.dpitch + x0 + c : nullptr;
-        const bool vec_store = GAIN && c + 4 <= col_lim && ((reinterpret_cast<uintptr_t>(drow) & 3) == 0) &&
-                               (a.dpitch & 3) == 0;
-#pragma unroll 1
-        for (int y = 0; y < FH; ++y) {
-            add_row(y + N - 1, false);  // window of output row y = input rows y .. y + N - 1
-            if (!GAIN) {
-                if (y < row_lim) {
-#pragma unroll
-                    for (int i = 0; i < 4; ++i)
-                        if (c + i < col_lim) vsum += NN * s2[i] - s1[i] * s1[i];
+                        for (int i = 0; i < 4; ++i) {
+                            const uint32_t f = (w1 >> (8 * i)) & 0xFFu;
+                            q += wc[i] * f * f;
+                        }
+                    }
+                    tile_sq += (long long)wr * q;
                 }
-            } else {
+            };
+#pragma unroll
+            for (int rr = 0; rr < N - 1; ++rr) {
+                take_row(rr, r1[rr]);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) s1[i] += r1[rr][i];
+            }
+#pragma unroll 1
+            for (int yg = 0; yg < FH; yg += N) {
+#pragma unroll
+                for (int u = 0; u < N; ++u) {
+                    const int y = yg + u;
+                    if (y >= FH) break;
+                    uint32_t h[4];
+                    take_row(y + N - 1, h);
+                    uint32_t sq4 = 0;
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        s1[i] += h[i];
+                        r1[(u + N - 1) % N][i] = h[i];
+                        if (c + i < col_lim) sq4 += s1[i] * s1[i];  // <= 4 * 12495^2 < 2^32
+                    }
+                    if (y < row_lim) tile_s1sq += sq4;
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) s1[i] -= r1[u][i];
+                }
+            }
+            // the last rows of the tile box (below the window of the last output row) hold halo f^2
+#pragma unroll
+            for (int rr = FH + N - 1; rr < SROWS; ++rr) {
+                uint32_t h[4];
+                take_row(rr, h);
+            }
+            vsum += (unsigned long long)((long long)NN * tile_sq - tile_s1sq);  // two's complement sum
+        } else {
+            // ---- gain: per-pixel S1, S2 by horizontal dp4a sums slid down the tile; the leaving row is
+            // re-read from the tile (small code, high occupancy) rather than kept in a register ring ----
+            uint32_t s1[4] = {0, 0, 0, 0}, s2[4] = {0, 0, 0, 0};
+            auto add_row = [&](int rr, bool sub) {
+                const uint32_t* rp = base + rr * (FBS / 4);
+                const uint32_t w0 = rp[0], w1 = rp[1], w2 = rp[2];
+                uint32_t h1[4], h2[4];
+                hsums<RW, 0>(w0, w1, w2, h1[0], h2[0]);
+                hsums<RW, 1>(w0, w1, w2, h1[1], h2[1]);
+                hsums<RW, 2>(w0, w1, w2, h1[2], h2[2]);
+                hsums<RW, 3>(w0, w1, w2, h1[3], h2[3]);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    s1[i] = sub ? s1[i] - h1[i] : s1[i] + h1[i];
+                    s2[i] = sub ? s2[i] - h2[i] : s2[i] + h2[i];
+                }
+            };
+#pragma unroll
+            for (int rr = 0; rr < N - 1; ++rr) add_row(rr, false);
+            uint8_t* drow = a.dst + (size_t)z * a.dslice + (size_t)(y0 - a.row_begin) * a.dpitch + x0 + c;
+            const bool vec_store = c + 4 <= col_lim && ((reinterpret_cast<uintptr_t>(drow) & 3) == 0) && (a.dpitch & 3) == 0;
+#pragma unroll 1
+            for (int y = 0; y < FH; ++y) {
+                add_row(y + N - 1, false);  // window of output row y = tile rows y .. y + N - 1
                 const uint32_t own = *(base + (y + RW) * (FBS / 4) + 1);  // f of the 4 output pixels
                 uint32_t out = 0;
 #pragma unroll
@@ -412,27 +517,31 @@ __global__ void __launch_bounds__(FNW * 32) wiener_fast_kernel(const __grid_cons
                     const uint32_t f = (own >> (8 * i)) & 0xFFu;
                     const uint32_t S1 = s1[i];
                     const int V = (int)(NN * s2[i] - S1 * S1);
-                    const uint32_t mu = (2u * S1 + NN) / (2u * NN);  // round(S1 / n), half up
-                    const int d = (int)(NN * f) - (int)S1;            // |d| <= 49 * 255 < 2^14
-                    // fp32 gain, conversions by exponent tricks (FMA/ALU pipes) except I2F(V), RCP
-                    const float df = __int_as_float(0x4B000000 + d + 16384) - 8404992.0f;  // (float)d
-                    const float fh = __int_as_float(0x4B000000 | f) - 8388607.5f;          // f + 0.5
+                    const int d = (int)(NN * f) - (int)S1;  // n (f - mu), |d| <= 49 * 255 < 2^14
+                    // y + 1/2 = (S1 + g d) / n + 1/2, g = max(0, 1 - (W/P) / V): one FFMA chain, exponent-trick
+                    // conversions; within 2^-11 of a rounding boundary the exact integer test decides.
+                    const float s1f = __int_as_float(0x4B000000 | S1) - 8388608.0f;
+                    const float df = __int_as_float(0x4B000000 + d + 16384) - 8404992.0f;
                     float rv;
                     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rv) : "f"((float)V));
-                    const float h = fh - df * kn * rv;  // y + 1/2, y = f - D W / (n V P)
-                    const int hb = __float_as_int(__fadd_rd(h, 12582912.0f));  // floor(h) in the mantissa
-                    const float fr = h - (__int_as_float(hb) - 12582912.0f);
+                    const float gg = fmaxf(0.0f, 1.0f - kq * rv);
+                    const float hh = fmaf(fmaf(gg, df, s1f), inv_n, 0.5f);
+                    const int hb = __float_as_int(__fadd_rd(hh, 12582912.0f));  // floor in the mantissa
+                    const float fr = hh - (__int_as_float(hb) - 12582912.0f);
                     int q = hb - 0x4B400000;
-                    const bool use_mu = V <= wq32;
-                    if (!use_mu && fabsf(fr - 0.5f) > 0.5f - kTieEps) {
-                        // exact: y >= m - 1/2  <=>  (2 (f - m) + 1) n V P >= 2 D W
-                        const int m = fr < 0.5f ? q : q + 1;
-                        const __int128 Q = (__int128)((long long)NN * V) * a.pixel_count;
-                        const __int128 lhs = (__int128)(2 * ((int)f - m) + 1) * Q;
-                        const __int128 rhs = (__int128)(2 * (long long)d) * W;
-                        q = lhs >= rhs ? m : m - 1;
+                    if (fabsf(fr - 0.5f) > 0.5f - kTieEps) {
+                        if (V <= wq32) {
+                            q = (int)((2u * S1 + NN) / (2u * NN));  // v <= nu: y = mu, half up
+                        } else {
+                            // y >= m - 1/2  <=>  (2 (f - m) + 1) n V P >= 2 D W
+                            const int m = fr < 0.5f ? q : q + 1;
+                            const __int128 Q = (__int128)((long long)NN * V) * a.pixel_count;
+                            const __int128 lhs = (__int128)(2 * ((int)f - m) + 1) * Q;
+                            const __int128 rhs = (__int128)(2 * (long long)d) * W;
+                            q = lhs >= rhs ? m : m - 1;
+                        }
                     }
-                    out |= (uint32_t)(use_mu ? (int)mu : q) << (8 * i);  // y in [min(mu, f), max(mu, f)]
+                    out |= (uint32_t)q << (8 * i);  // y in [min(mu, f), max(mu, f)] -> 0..255
                 }
                 if (y < row_lim) {
                     if (vec_store) {
@@ -442,8 +551,8 @@ __global__ void __launch_bounds__(FNW * 32) wiener_fast_kernel(const __grid_cons
                     }
                 }
                 drow += a.dpitch;
+                add_row(y, true);  // drop tile row y
             }
-            add_row(y, true);  // drop input row y
         }
         __syncwarp();
         // refill this slot with the warp's tile after next
