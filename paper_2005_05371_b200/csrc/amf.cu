@@ -45,7 +45,7 @@ constexpr int BH = TH + 2;       // byte-tile rows (1-pixel halo)
 constexpr int BBYTES = (BS * BH + 127) / 128 * 128;  // ring slot (TMA destinations are 128-byte aligned)
 constexpr int NBUF = 4;          // TMA ring depth
 constexpr int HDR = 128;         // mbarriers, release counters, tile coordinates
-constexpr int WAREA = 2 * WPIX;  // per warp: output strip + finalized_at strip
+constexpr int WAREA = 2 * WPIX;  // per warp: output strip, finalized_at strip
 constexpr size_t SMEM = HDR + NBUF * BBYTES + NW * WAREA + 128;
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) { return __byte_perm(a, b, s); }
@@ -99,10 +99,8 @@ struct K3Args {
     int row_begin, row_end;  // output rows (source coordinates)
     int n_slices;
     int tiles_x, tiles_y;
-    int grow;                // queue level-A failures (smax >= 5)
-    uint32_t* queue;         // work queue for k = 5
-    int* queue_n;
-    int col_bits, row_bits;  // queue id = ((z << row_bits | out_row) << col_bits) | col
+    int grow;                // record level-A failures (smax >= 5)
+    uint8_t* bitmap;         // per tile 32 rows x 16 bytes: bit c%8 of byte c/8 = pixel (row, c) failed level A
 };
 
 __device__ __forceinline__ void issue_tile_load(const CUtensorMap* tm, uint8_t* Bbuf, uint64_t* bar, int x0, int y0,
@@ -161,6 +159,7 @@ __global__ void __launch_bounds__(NT, 3)
         claim = __shfl_sync(0xFFFFFFFFu, claim, 0);
         const int ti = claim >> 3, sub = claim & 7;
         if (ti >= my_tiles) break;
+        const int t = blockIdx.x + ti * gridDim.x;
         const int s = ti & (NBUF - 1);
         mbar_wait(&full[s], (uint32_t)(ti / NBUF) & 1u);
         const int x0 = tinfo[4 * s], y0 = tinfo[4 * s + 1], z = tinfo[4 * s + 2];
@@ -276,7 +275,8 @@ __global__ void __launch_bounds__(NT, 3)
         const int row_lim = args.row_end - y0 - sub * WR;  // strip rows < row_lim are in range
         const int col_lim = cols - x0;
 
-        // ---- append level-A failures (inside the output range) to the k = 5 work queue ----
+        // ---- level-A failures (inside the output range) -> the tile's failure bitmap (no atomics:
+        //      every bitmap byte of the tile is written by exactly one lane) ----
         if (args.grow) {
             const uint32_t rv = __brev(failbits);                     // bit 16+j: row lr; bit j: row lr+1
             uint32_t m = ((rv >> 16) & 0xFFu) | ((rv & 0xFFu) << 8);  // bit j: row lr; bit 8+j: row lr+1
@@ -286,24 +286,9 @@ __global__ void __launch_bounds__(NT, 3)
                 const uint32_t cm = col_lim <= c0 ? 0u : ((1u << (col_lim - c0)) - 1u);
                 m &= cm | (cm << 8);
             }
-            const int nf = __popc(m);
-            int incl = nf;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const int v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
-                if (lane >= d) incl += v;
-            }
-            const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
-            int base = 0;
-            if (lane == 31 && total) base = atomicAdd(args.queue_n, total);
-            base = __shfl_sync(0xFFFFFFFFu, base, 31);
-            int pos = base + incl - nf;
-            const uint32_t zrow = ((uint32_t)z << args.row_bits) | (uint32_t)(orow0 + lr);
-            while (m) {
-                const int bit = __ffs(m) - 1;
-                m &= m - 1;
-                args.queue[pos++] = ((zrow + (uint32_t)(bit >> 3)) << args.col_bits) | (uint32_t)(x0 + c0 + (bit & 7));
-            }
+            uint8_t* bm = args.bitmap + (size_t)t * 512 + (sub * WR + lr) * 16 + (c0 >> 3);
+            bm[0] = (uint8_t)m;
+            bm[16] = (uint8_t)(m >> 8);
         }
         __syncwarp();
 
@@ -343,22 +328,46 @@ __global__ void __launch_bounds__(NT, 3)
 }
 
 // ------------------------------------------------------------------------------------------
-// growth kernels (k >= 5) over the device-wide work queue
+// growth kernel (k = 5..smax): tile-wise, all levels from shared memory
 // ------------------------------------------------------------------------------------------
 
-struct GrowArgs {
-    const uint8_t* src;
-    size_t spitch, sslice;
+// Tile geometry of the growth kernel: the 128 x 32 tile plus a halo of R = (smax-1)/2.
+struct GGeo {
+    int R, CP, BS, BH;          // halo, column pad (multiple of 16), row stride, rows
+    int box_w, nbx, box_h, nby;  // TMA boxes (<= 256 per dimension)
+    int b_bytes;                 // bytes per tile buffer (128-aligned)
+};
+
+inline GGeo make_ggeo(int smax) {
+    GGeo g;
+    g.R = (smax - 1) / 2;
+    g.CP = 16 * ((g.R + 15) / 16 > 0 ? (g.R + 15) / 16 : 1);
+    const int need = TW + 2 * g.CP;
+    g.box_w = need <= 256 ? need : 128;
+    g.nbx = (need + g.box_w - 1) / g.box_w;
+    g.BS = g.box_w * g.nbx;
+    g.BH = TH + 2 * g.R;
+    g.box_h = g.BH <= 256 ? g.BH : 128;
+    g.nby = (g.BH + g.box_h - 1) / g.box_h;
+    g.b_bytes = (g.BS * g.box_h * g.nby + 127) / 128 * 128;
+    return g;
+}
+
+constexpr int GNT = 256;         // threads per growth CTA
+constexpr int GHDR = 1024;       // mbarriers, tile coordinates, level counters, scan scratch
+constexpr int MAX_LEVELS = 128;
+
+inline size_t grow_smem(const GGeo& g) { return GHDR + 2 * (size_t)g.b_bytes + 2 * TH * TW * 2 + 128; }
+
+struct GArgs {
+    GGeo geo;
     uint8_t* dst;
     size_t dpitch, dslice;
     uint8_t* fin;
     size_t fpitch, fslice;
-    int rows, cols, row_begin;
-    int col_bits, row_bits;
-    const uint32_t* qin;
-    const int* nin;
-    uint32_t* qout;  // null at the last level
-    int* nout;
+    const uint8_t* bitmap;
+    int rows, cols, row_begin, row_end, n_slices, smax;
+    int tiles_x, tiles_y;
 };
 
 template <int K>
@@ -374,51 +383,22 @@ struct Win {
     }
 };
 
-struct Pix {
-    int z, orow, r, c;  // slice, output row, source row, column
-};
-
-__device__ __forceinline__ Pix decode(const GrowArgs& a, uint32_t id) {
-    Pix p;
-    p.c = (int)(id & ((1u << a.col_bits) - 1u));
-    const uint32_t zr = id >> a.col_bits;
-    p.orow = (int)(zr & ((1u << a.row_bits) - 1u));
-    p.z = (int)(zr >> a.row_bits);
-    p.r = a.row_begin + p.orow;
-    return p;
-}
-
-// The K x K window around a pixel as K rows of AW byte-aligned words (edge replication).
+// The K x K window around tile pixel (ty, tx) as K rows of AW byte-aligned words from the tile.
 template <int K>
-__device__ __forceinline__ void load_window(const GrowArgs& a, const Pix& p, uint32_t (&w)[K][Win<K>::AW]) {
+__device__ __forceinline__ void load_window(const uint8_t* __restrict__ B, const GGeo& geo, int ty, int tx,
+                                            uint32_t (&a)[K][Win<K>::AW]) {
     using W = Win<K>;
-    const uint8_t* __restrict__ plane = a.src + (size_t)p.z * a.sslice;
-    const int start = p.c - W::RK;
-    if (p.r - W::RK >= 0 && p.r + W::RK < a.rows && start >= 0 && (start & ~3) + 4 * W::NRAW <= a.cols) {
-        const int sh = 8 * (start & 3);
+    const int start = tx + geo.CP - W::RK;
+    const int sh = 8 * (start & 3);
+    const uint32_t* rowp =
+        reinterpret_cast<const uint32_t*>(B + (size_t)(ty + geo.R - W::RK) * geo.BS) + (start >> 2);
 #pragma unroll
-        for (int r = 0; r < K; ++r) {
-            const uint32_t* rp =
-                reinterpret_cast<const uint32_t*>(plane + (size_t)(p.r - W::RK + r) * a.spitch + (start & ~3));
-            uint32_t raw[W::NRAW];
+    for (int r = 0; r < K; ++r) {
+        uint32_t raw[W::NRAW];
 #pragma unroll
-            for (int j = 0; j < W::NRAW; ++j) raw[j] = __ldg(rp + j);
+        for (int j = 0; j < W::NRAW; ++j) raw[j] = rowp[r * (geo.BS >> 2) + j];
 #pragma unroll
-            for (int j = 0; j < W::AW; ++j) w[r][j] = __funnelshift_r(raw[j], (j + 1 < W::NRAW) ? raw[j + 1] : 0u, sh);
-        }
-    } else {
-#pragma unroll
-        for (int r = 0; r < K; ++r) {
-            const uint8_t* rowp = plane + (size_t)min(max(p.r - W::RK + r, 0), a.rows - 1) * a.spitch;
-#pragma unroll
-            for (int j = 0; j < W::AW; ++j) {
-                uint32_t v = 0;
-#pragma unroll
-                for (int b = 0; b < 4; ++b)
-                    if (4 * j + b < K) v |= (uint32_t)__ldg(rowp + min(max(start + 4 * j + b, 0), a.cols - 1)) << (8 * b);
-                w[r][j] = v;
-            }
-        }
+        for (int j = 0; j < W::AW; ++j) a[r][j] = __funnelshift_r(raw[j], (j + 1 < W::NRAW) ? raw[j + 1] : 0u, sh);
     }
 }
 
@@ -433,66 +413,32 @@ __device__ __forceinline__ void select_net<7>(uint32_t (&v)[49], uint32_t& a, ui
     select_net7(v, a, b, c);
 }
 
-__device__ __forceinline__ void write_result(const GrowArgs& a, const Pix& p, uint32_t v, int k) {
-    a.dst[(size_t)p.z * a.dslice + (size_t)p.orow * a.dpitch + p.c] = (uint8_t)v;
-    if (a.fin) a.fin[(size_t)p.z * a.fslice + (size_t)p.orow * a.fpitch + p.c] = (uint8_t)k;
-}
-
-// Warp-aggregated append of the lanes with keep set to the next level's queue.
-__device__ __forceinline__ void requeue(const GrowArgs& a, bool keep, uint32_t id) {
-    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, keep);
-    if (!bal || !a.qout) return;
-    const int lane = threadIdx.x & 31;
-    const int leader = __ffs(bal) - 1;
-    int base = 0;
-    if (lane == leader) base = atomicAdd(a.nout, __popc(bal));
-    base = __shfl_sync(0xFFFFFFFFu, base, leader);
-    if (keep) a.qout[base + __popc(bal & ((1u << lane) - 1u))] = id;
-}
-
-// k = 5, 7: two queued pixels per thread in the u16x2 lanes, selection network.
+// k = 5, 7: two queued pixels in the u16x2 lanes of one thread, generated selection network.
 template <int K>
-__global__ void __launch_bounds__(256) amf_grow_pair_kernel(const GrowArgs a) {
+__device__ __forceinline__ void level_pair(const uint8_t* __restrict__ B, const GGeo& geo, int pa, int pb,
+                                           uint32_t& done, uint32_t& outw) {
     using W = Win<K>;
-    const int n = *a.nin;
-    const int npairs = (n + 1) >> 1;
-    const int stride = gridDim.x * blockDim.x;
-    for (int base = blockIdx.x * blockDim.x; base < npairs; base += stride) {
-        const int i = base + threadIdx.x;
-        bool keepA = false, keepB = false;
-        uint32_t ida = 0, idb = 0;
-        if (i < npairs) {
-            ida = a.qin[2 * i];
-            const bool hasb = 2 * i + 1 < n;
-            idb = hasb ? a.qin[2 * i + 1] : ida;
-            const Pix pa = decode(a, ida), pb = decode(a, idb);
-            uint32_t wa[K][W::AW], wb[K][W::AW];
-            load_window<K>(a, pa, wa);
-            load_window<K>(a, pb, wb);
-            uint32_t v[K * K];
+    uint32_t A[K][W::AW], Bw[K][W::AW];
+    load_window<K>(B, geo, pa >> 7, pa & 127, A);
+    load_window<K>(B, geo, pb >> 7, pb & 127, Bw);
+    uint32_t v[K * K];
 #pragma unroll
-            for (int r = 0; r < K; ++r)
+    for (int r = 0; r < K; ++r)
 #pragma unroll
-                for (int e = 0; e < K; ++e) v[r * K + e] = pairw_rt(wa[r][e >> 2], wb[r][e >> 2], e & 3);
-            const uint32_t g = v[W::RK * K + W::RK];
-            uint32_t zmin, zmed, zmax;
-            select_net<K>(v, zmin, zmed, zmax);
+        for (int e = 0; e < K; ++e) v[r * K + e] = pairw_rt(A[r][e >> 2], Bw[r][e >> 2], e & 3);
+    const uint32_t g = v[W::RK * K + W::RK];
+    uint32_t zmin, zmed, zmax;
+    select_net<K>(v, zmin, zmed, zmax);
+    done = 0;
+    outw = 0;
 #pragma unroll
-            for (int l = 0; l < 2; ++l) {
-                const uint32_t zn = (zmin >> (16 * l)) & 0xFFu, zd = (zmed >> (16 * l)) & 0xFFu;
-                const uint32_t zx = (zmax >> (16 * l)) & 0xFFu, gl = (g >> (16 * l)) & 0xFFu;
-                const bool done = zn < zd && zd < zx;
-                if (l == 0) {
-                    if (done) write_result(a, pa, (zn < gl && gl < zx) ? gl : zd, K);
-                    keepA = !done;
-                } else if (hasb) {
-                    if (done) write_result(a, pb, (zn < gl && gl < zx) ? gl : zd, K);
-                    keepB = !done;
-                }
-            }
+    for (int l = 0; l < 2; ++l) {
+        const uint32_t zn = (zmin >> (16 * l)) & 0xFFu, zd = (zmed >> (16 * l)) & 0xFFu;
+        const uint32_t zx = (zmax >> (16 * l)) & 0xFFu, gl = (g >> (16 * l)) & 0xFFu;
+        if (zn < zd && zd < zx) {
+            done |= 1u << l;
+            outw |= ((zn < gl && gl < zx) ? gl : zd) << (8 * l);
         }
-        requeue(a, keepA, ida);
-        requeue(a, keepB, idb);
     }
 }
 
@@ -534,124 +480,297 @@ __device__ __forceinline__ uint32_t select_rank(const uint32_t (&w)[K][Win<K>::A
 
 // k = 9, 11: one pixel per thread; level A from SWAR counts, median by radix select if needed.
 template <int K>
-__global__ void __launch_bounds__(256) amf_grow_radix_kernel(const GrowArgs a) {
+__device__ __forceinline__ bool level_radix(const uint8_t* __restrict__ B, const GGeo& geo, int ty, int tx,
+                                            uint8_t* out) {
     using W = Win<K>;
-    const int n = *a.nin;
-    const int stride = gridDim.x * blockDim.x;
-    for (int base = blockIdx.x * blockDim.x; base < n; base += stride) {
-        const int i = base + threadIdx.x;
-        bool keep = false;
-        uint32_t id = 0;
-        if (i < n) {
-            id = a.qin[i];
-            const Pix p = decode(a, id);
-            uint32_t w[K][W::AW];
-            load_window<K>(a, p, w);
-            uint32_t mn = 0x00FF00FFu, mx = 0u;
+    uint32_t w[K][W::AW];
+    load_window<K>(B, geo, ty, tx, w);
+    uint32_t mn = 0x00FF00FFu, mx = 0u;
 #pragma unroll
-            for (int r = 0; r < K; ++r)
+    for (int r = 0; r < K; ++r)
 #pragma unroll
-                for (int j = 0; j < W::AW; ++j) {
-                    const uint32_t x = w[r][j];
-                    uint32_t lo, hi;
-                    if (j < W::AW - 1 || W::TAIL == 0) {
-                        lo = prmt(x, 0, 0x4140);
-                        hi = prmt(x, 0, 0x4342);
-                    } else if (W::TAIL == 1) {
-                        lo = hi = prmt(x, 0, 0x4040);
-                    } else if (W::TAIL == 2) {
-                        lo = hi = prmt(x, 0, 0x4140);
-                    } else {
-                        lo = prmt(x, 0, 0x4140);
-                        hi = prmt(x, 0, 0x4242);
-                    }
-                    mn = __vimin3_u16x2(mn, lo, hi);
-                    mx = __vimax3_u16x2(mx, lo, hi);
-                }
-            const uint32_t zmin = min(mn & 0xFFFFu, mn >> 16), zmax = max(mx & 0xFFFFu, mx >> 16);
-            // level A <=> zmin < zmax, #(v == zmin) <= m and #(v == zmax) <= m
-            const bool done = zmin < zmax && count_eq<K>(w, zmin) <= W::M && count_eq<K>(w, zmax) <= W::M;
-            if (done) {
-                const uint32_t g = (w[W::RK][W::RK >> 2] >> (8 * (W::RK & 3))) & 0xFFu;
-                write_result(a, p, (g != zmin && g != zmax) ? g : select_rank<K>(w, W::M, zmin, zmax), K);
+        for (int j = 0; j < W::AW; ++j) {
+            const uint32_t x = w[r][j];
+            uint32_t lo, hi;
+            if (j < W::AW - 1 || W::TAIL == 0) {
+                lo = prmt(x, 0, 0x4140);
+                hi = prmt(x, 0, 0x4342);
+            } else if (W::TAIL == 1) {
+                lo = hi = prmt(x, 0, 0x4040);
+            } else if (W::TAIL == 2) {
+                lo = hi = prmt(x, 0, 0x4140);
+            } else {
+                lo = prmt(x, 0, 0x4140);
+                hi = prmt(x, 0, 0x4242);
             }
-            keep = !done;
+            mn = __vimin3_u16x2(mn, lo, hi);
+            mx = __vimax3_u16x2(mx, lo, hi);
         }
-        requeue(a, keep, id);
-    }
+    const uint32_t zmin = min(mn & 0xFFFFu, mn >> 16), zmax = max(mx & 0xFFFFu, mx >> 16);
+    // level A <=> zmin < zmax, #(v == zmin) <= m and #(v == zmax) <= m
+    if (zmin == zmax || count_eq<K>(w, zmin) > W::M || count_eq<K>(w, zmax) > W::M) return false;
+    const uint32_t g = B[(size_t)(ty + geo.R) * geo.BS + tx + geo.CP];
+    *out = (uint8_t)((g != zmin && g != zmax) ? g : select_rank<K>(w, W::M, zmin, zmax));
+    return true;
 }
 
-// k > 11 (windows beyond the compile-time set): same algorithm on clamped byte reads.
-__global__ void __launch_bounds__(256) amf_grow_generic_kernel(const GrowArgs a, int k) {
-    const int n = *a.nin;
-    const int stride = gridDim.x * blockDim.x;
-    const int rk = k / 2, m = (k * k - 1) / 2;
-    for (int base = blockIdx.x * blockDim.x; base < n; base += stride) {
-        const int i = base + threadIdx.x;
-        bool keep = false;
-        uint32_t id = 0;
-        if (i < n) {
-            id = a.qin[i];
-            const Pix p = decode(a, id);
-            const uint8_t* __restrict__ plane = a.src + (size_t)p.z * a.sslice;
-            auto at = [&](int dr, int dc) -> uint32_t {
-                return __ldg(plane + (size_t)min(max(p.r + dr, 0), a.rows - 1) * a.spitch +
-                             min(max(p.c + dc, 0), a.cols - 1));
-            };
-            uint32_t zmin = 255, zmax = 0;
-            for (int dr = -rk; dr <= rk; ++dr)
-                for (int dc = -rk; dc <= rk; ++dc) {
-                    const uint32_t v = at(dr, dc);
-                    zmin = min(zmin, v);
-                    zmax = max(zmax, v);
-                }
-            int cmin = 0, cmax = 0;
-            if (zmin < zmax)
-                for (int dr = -rk; dr <= rk; ++dr)
-                    for (int dc = -rk; dc <= rk; ++dc) {
-                        const uint32_t v = at(dr, dc);
-                        cmin += v == zmin;
-                        cmax += v == zmax;
-                    }
-            const bool done = zmin < zmax && cmin <= m && cmax <= m;
-            if (done) {
-                const uint32_t g = at(0, 0);
-                uint32_t out = g;
-                if (g == zmin || g == zmax) {
-                    const int hb = 31 - __clz(zmin ^ zmax);
-                    uint32_t prefix = zmin & ~((2u << hb) - 1u);
-                    int below = 0;
-                    for (int b = hb; b >= 0; --b) {
-                        const uint32_t mask = (0xFFu << b) & 0xFFu;
-                        int c = 0;
-                        for (int dr = -rk; dr <= rk; ++dr)
-                            for (int dc = -rk; dc <= rk; ++dc) c += ((at(dr, dc) ^ prefix) & mask) == 0;
-                        if (below + c <= m) {
-                            below += c;
-                            prefix |= 1u << b;
+// k > 11: same algorithm on byte reads from the tile.
+__device__ bool level_generic(const uint8_t* __restrict__ B, const GGeo& geo, int ty, int tx, int k, uint8_t* out) {
+    const int rk = k / 2;
+    const uint8_t* base = B + (size_t)(ty + geo.R - rk) * geo.BS + (tx + geo.CP - rk);
+    uint32_t zmin = 255, zmax = 0;
+    for (int r = 0; r < k; ++r)
+        for (int c = 0; c < k; ++c) {
+            const uint32_t v = base[(size_t)r * geo.BS + c];
+            zmin = min(zmin, v);
+            zmax = max(zmax, v);
+        }
+    if (zmin == zmax) return false;
+    const int m = (k * k - 1) / 2;
+    int cmin = 0, cmax = 0;
+    for (int r = 0; r < k; ++r)
+        for (int c = 0; c < k; ++c) {
+            const uint32_t v = base[(size_t)r * geo.BS + c];
+            cmin += v == zmin;
+            cmax += v == zmax;
+        }
+    if (cmin > m || cmax > m) return false;
+    const uint32_t g = B[(size_t)(ty + geo.R) * geo.BS + tx + geo.CP];
+    if (g != zmin && g != zmax) {
+        *out = (uint8_t)g;
+        return true;
+    }
+    const int hb = 31 - __clz(zmin ^ zmax);
+    uint32_t prefix = zmin & ~((2u << hb) - 1u);
+    int below = 0;
+    for (int b = hb; b >= 0; --b) {
+        const uint32_t mask = (0xFFu << b) & 0xFFu;
+        int c = 0;
+        for (int r = 0; r < k; ++r)
+            for (int cc = 0; cc < k; ++cc) c += ((base[(size_t)r * geo.BS + cc] ^ prefix) & mask) == 0;
+        if (below + c <= m) {
+            below += c;
+            prefix |= 1u << b;
+        }
+    }
+    *out = (uint8_t)prefix;
+    return true;
+}
+
+__device__ __forceinline__ void grow_tile_load(const CUtensorMap* tm, const GGeo& geo, uint8_t* Bbuf, uint64_t* bar,
+                                               int x0, int y0, int z) {
+    mbar_expect_tx(bar, (uint32_t)(geo.box_w * geo.nbx * geo.box_h * geo.nby));
+    for (int by = 0; by < geo.nby; ++by)
+        for (int bx = 0; bx < geo.nbx; ++bx)
+            tma_load_3d(Bbuf + (size_t)by * geo.box_h * geo.BS + (size_t)bx * geo.box_w, tm, bar,
+                        x0 - geo.CP + bx * geo.box_w, y0 - geo.R + by * geo.box_h, z);
+}
+
+// Persistent over tiles: the tile's failure bitmap (written by amf_k3_kernel) is compacted into a
+// shared-memory queue; if non-empty, the tile plus an R halo (TMA, double-buffered: the next tile
+// streams in meanwhile) serves every window size k = 5..smax, survivors re-compacted per level.
+template <bool FIN>
+__global__ void __launch_bounds__(GNT) amf_grow_kernel(const __grid_constant__ CUtensorMap tm,
+                                                      const __grid_constant__ GArgs args) {
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+    const GGeo& geo = args.geo;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);  // [2]
+    int* tinfo = reinterpret_cast<int*>(smem + 16);       // [2][4]
+    int* qcount = reinterpret_cast<int*>(smem + 64);      // [MAX_LEVELS]
+    int* wsum = reinterpret_cast<int*>(smem + 64 + 4 * MAX_LEVELS);  // [8] warp totals
+    uint8_t* bufs = smem + GHDR;
+    uint16_t* Q0 = reinterpret_cast<uint16_t*>(bufs + 2 * (size_t)geo.b_bytes);
+    uint16_t* Q1 = Q0 + TH * TW;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int per_slice = args.tiles_x * args.tiles_y;
+    const int ntiles = per_slice * args.n_slices;
+    if ((int)blockIdx.x >= ntiles) return;
+    auto coords = [&](int t, int* info) {
+        const int z = t / per_slice, rem = t - z * per_slice;
+        const int by = rem / args.tiles_x;
+        info[0] = (rem - by * args.tiles_x) * TW;
+        info[1] = args.row_begin + by * TH;
+        info[2] = z;
+    };
+    if (tid == 0) {
+        prefetch_tmap(&tm);
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+        coords(blockIdx.x, tinfo);
+        grow_tile_load(&tm, geo, bufs, &bar[0], tinfo[0], tinfo[1], tinfo[2]);
+    }
+    __syncthreads();
+    int it = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        const int s = it & 1;
+        if (tid == 0 && t + (int)gridDim.x < ntiles) {  // prefetch the next tile (its slot was freed last iteration)
+            coords(t + gridDim.x, tinfo + 4 * (s ^ 1));
+            fence_proxy_async_smem();
+            grow_tile_load(&tm, geo, bufs + (size_t)(s ^ 1) * geo.b_bytes, &bar[s ^ 1], tinfo[4 * (s ^ 1)],
+                           tinfo[4 * (s ^ 1) + 1], tinfo[4 * (s ^ 1) + 2]);
+        }
+        if (tid < MAX_LEVELS) qcount[tid] = 0;
+        // ---- bitmap -> queue 0 (block scan; 16 bits per thread) ----
+        const uint32_t word = reinterpret_cast<const uint32_t*>(args.bitmap + (size_t)t * 512)[tid >> 1];
+        uint32_t bits = (word >> (16 * (tid & 1))) & 0xFFFFu;
+        const int nf = __popc(bits);
+        int incl = nf;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+            if (lane >= d) incl += v;
+        }
+        if (lane == 31) wsum[warp] = incl;
+        __syncthreads();
+        int wbase = 0, n = 0;
+#pragma unroll
+        for (int w = 0; w < GNT / 32; ++w) {
+            const int v = wsum[w];
+            wbase += w < warp ? v : 0;
+            n += v;
+        }
+        {
+            int pos = wbase + incl - nf;
+            const int row = tid >> 3, colb = 16 * (tid & 7);  // 16 bits = row, columns colb..colb+15
+            while (bits) {
+                const int b = __ffs(bits) - 1;
+                bits &= bits - 1;
+                Q0[pos++] = (uint16_t)(row * TW + colb + b);
+            }
+        }
+        mbar_wait(&bar[s], (uint32_t)(it >> 1) & 1u);  // every thread observes the phase (keeps parity in step)
+        const int x0 = tinfo[4 * s], y0 = tinfo[4 * s + 1], z = tinfo[4 * s + 2];
+        uint8_t* B = bufs + (size_t)s * geo.b_bytes;
+        if (n > 0) {
+            // ---- border tiles: edge replication in place of TMA's zero fill ----
+            const int sx0 = x0 - geo.CP, sy0 = y0 - geo.R;
+            if (sx0 < 0 || sx0 + geo.BS > args.cols || sy0 < 0 || sy0 + geo.BH > args.rows) {
+                const int c_lo = max(0, -sx0), c_hi = min(geo.BS, args.cols - sx0);
+                const int r_lo = max(0, -sy0), r_hi = min(geo.BH, args.rows - sy0);
+                if (c_lo > 0 || c_hi < geo.BS) {
+                    for (int rr = r_lo + warp; rr < r_hi; rr += GNT / 32) {
+                        uint8_t* row = B + (size_t)rr * geo.BS;
+                        const uint8_t lv = row[c_lo], rv = row[c_hi - 1];
+                        for (int cc = lane; cc < geo.BS; cc += 32) {
+                            if (cc < c_lo) row[cc] = lv;
+                            else if (cc >= c_hi) row[cc] = rv;
                         }
                     }
-                    out = prefix;
                 }
-                write_result(a, p, out, k);
+                __syncthreads();
+                const int words = geo.BS >> 2;
+                for (int idx = tid; idx < geo.BH * words; idx += GNT) {
+                    const int rr = idx / words, q = idx - rr * words;
+                    const int src_r = rr < r_lo ? r_lo : (rr >= r_hi ? r_hi - 1 : rr);
+                    if (src_r != rr)
+                        reinterpret_cast<uint32_t*>(B + (size_t)rr * geo.BS)[q] =
+                            reinterpret_cast<const uint32_t*>(B + (size_t)src_r * geo.BS)[q];
+                }
             }
-            keep = !done;
+            __syncthreads();
+            uint8_t* dtile = args.dst + (size_t)z * args.dslice + (size_t)(y0 - args.row_begin) * args.dpitch + x0;
+            uint8_t* ftile = FIN ? args.fin + (size_t)z * args.fslice + (size_t)(y0 - args.row_begin) * args.fpitch + x0
+                                 : nullptr;
+            int lvl = 0;
+            for (int k = 5; k <= args.smax; k += 2, ++lvl) {
+                const uint16_t* qin = (lvl & 1) ? Q1 : Q0;
+                uint16_t* qout = (lvl & 1) ? Q0 : Q1;
+                const bool last = k + 2 > args.smax;
+                if (k <= 7) {
+                    const int npairs = (n + 1) >> 1;
+                    for (int base = warp * 32; base < npairs; base += GNT) {
+                        const int i = base + lane;
+                        uint32_t keep = 0;
+                        int pa = 0, pb = 0;
+                        if (i < npairs) {
+                            pa = qin[2 * i];
+                            const bool hasb = 2 * i + 1 < n;
+                            pb = hasb ? qin[2 * i + 1] : pa;
+                            uint32_t done, outw;
+                            if (k == 5) level_pair<5>(B, geo, pa, pb, done, outw);
+                            else level_pair<7>(B, geo, pa, pb, done, outw);
+                            if (done & 1u) {
+                                dtile[(size_t)(pa >> 7) * args.dpitch + (pa & 127)] = (uint8_t)outw;
+                                if (FIN) ftile[(size_t)(pa >> 7) * args.fpitch + (pa & 127)] = (uint8_t)k;
+                            } else {
+                                keep |= 1u;
+                            }
+                            if (hasb) {
+                                if (done & 2u) {
+                                    dtile[(size_t)(pb >> 7) * args.dpitch + (pb & 127)] = (uint8_t)(outw >> 8);
+                                    if (FIN) ftile[(size_t)(pb >> 7) * args.fpitch + (pb & 127)] = (uint8_t)k;
+                                } else {
+                                    keep |= 2u;
+                                }
+                            }
+                        }
+                        if (!last) {
+                            const uint32_t balA = __ballot_sync(0xFFFFFFFFu, keep & 1u);
+                            const uint32_t balB = __ballot_sync(0xFFFFFFFFu, keep & 2u);
+                            const int cnt = __popc(balA) + __popc(balB);
+                            if (cnt) {
+                                int qb = 0;
+                                if (lane == 0) qb = atomicAdd(&qcount[lvl + 1], cnt);
+                                qb = __shfl_sync(0xFFFFFFFFu, qb, 0);
+                                const uint32_t below = (1u << lane) - 1u;
+                                if (keep & 1u) qout[qb + __popc(balA & below)] = (uint16_t)pa;
+                                if (keep & 2u) qout[qb + __popc(balA) + __popc(balB & below)] = (uint16_t)pb;
+                            }
+                        }
+                    }
+                } else {
+                    for (int base = warp * 32; base < n; base += GNT) {
+                        const int i = base + lane;
+                        bool keep = false;
+                        int pix = 0;
+                        if (i < n) {
+                            pix = qin[i];
+                            const int ty = pix >> 7, tx = pix & 127;
+                            uint8_t o = 0;
+                            bool done;
+                            switch (k) {
+                                case 9: done = level_radix<9>(B, geo, ty, tx, &o); break;
+                                case 11: done = level_radix<11>(B, geo, ty, tx, &o); break;
+                                default: done = level_generic(B, geo, ty, tx, k, &o); break;
+                            }
+                            if (done) {
+                                dtile[(size_t)ty * args.dpitch + tx] = o;
+                                if (FIN) ftile[(size_t)ty * args.fpitch + tx] = (uint8_t)k;
+                            } else {
+                                keep = true;
+                            }
+                        }
+                        if (!last) {
+                            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, keep);
+                            if (bal) {
+                                int qb = 0;
+                                if (lane == 0) qb = atomicAdd(&qcount[lvl + 1], __popc(bal));
+                                qb = __shfl_sync(0xFFFFFFFFu, qb, 0);
+                                if (keep) qout[qb + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)pix;
+                            }
+                        }
+                    }
+                }
+                __syncthreads();
+                if (last) break;
+                n = qcount[lvl + 1];
+                if (n == 0) break;
+            }
         }
-        requeue(a, keep, id);
+        __syncthreads();  // this slot, the queues and the level counters are reused next iteration
     }
 }
 
 int g_num_sms = 0;
 
-int bits_for(long long n) {
-    int b = 0;
-    while ((1ll << b) < n) ++b;
-    return b;
-}
-
 }  // namespace
 
-size_t amf_queue_words(const Plane& p) { return (size_t)(p.row_end - p.row_begin) * p.cols * p.n_slices + 64; }
+size_t amf_bitmap_bytes(const Plane& p) {
+    const size_t tiles = (size_t)((p.cols + TW - 1) / TW) * ((p.row_end - p.row_begin + TH - 1) / TH) * p.n_slices;
+    return tiles * 512;
+}
 
 cudaError_t launch_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, size_t fslice, const AmfWork& work,
                        cudaStream_t stream) {
@@ -670,17 +789,10 @@ cudaError_t launch_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, si
         cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     }
     const int out_rows = p.row_end - p.row_begin;
-    const int col_bits = bits_for(p.cols), row_bits = bits_for(out_rows), z_bits = bits_for(p.n_slices);
     const bool grow = smax >= 5;
-    if (grow && col_bits + row_bits + z_bits > 32) return cudaErrorInvalidValue;  // queue id overflow
     CUtensorMap tm_src;
     cudaError_t e = make_tmap_u8(&tm_src, p.src, p.cols, p.rows, p.n_slices, p.spitch, p.sslice, BS, BH);
     if (e != cudaSuccess) return e;
-    const int nlev = grow ? (smax - 3) / 2 : 0;
-    if (grow) {
-        e = cudaMemsetAsync(work.counts, 0, sizeof(int) * (nlev + 1), stream);
-        if (e != cudaSuccess) return e;
-    }
     K3Args a;
     a.dst = p.dst;
     a.dpitch = p.dpitch;
@@ -696,10 +808,7 @@ cudaError_t launch_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, si
     a.tiles_x = (p.cols + TW - 1) / TW;
     a.tiles_y = (out_rows + TH - 1) / TH;
     a.grow = grow;
-    a.queue = work.queue[0];
-    a.queue_n = work.counts;
-    a.col_bits = col_bits;
-    a.row_bits = row_bits;
+    a.bitmap = work.bitmap;
     static int per_sm = 0;
     if (!per_sm) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, amf_k3_kernel<false>, NT, SMEM);
@@ -710,46 +819,51 @@ cudaError_t launch_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, si
     if (fin) amf_k3_kernel<true><<<grid, NT, SMEM, stream>>>(tm_src, a);
     else amf_k3_kernel<false><<<grid, NT, SMEM, stream>>>(tm_src, a);
     count_launch();
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = cudaGetLastError()) != cudaSuccess || !grow) return e;
 
-    // growth levels: queue[l & 1] holds the pixels still open at k = 5 + 2 l
-    GrowArgs g;
-    g.src = p.src;
-    g.spitch = p.spitch;
-    g.sslice = p.sslice;
+    // ---- growth: one tile-wise launch for every window size k = 5..smax ----
+    const GGeo geo = make_ggeo(smax);
+    const size_t gsm = grow_smem(geo);
+    static size_t gconfigured = 0;
+    if (gsm > gconfigured) {
+        e = cudaFuncSetAttribute(amf_grow_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(amf_grow_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm);
+        if (e != cudaSuccess) return e;
+        gconfigured = gsm;
+    }
+    CUtensorMap tm_g;
+    e = make_tmap_u8(&tm_g, p.src, p.cols, p.rows, p.n_slices, p.spitch, p.sslice, geo.box_w, geo.box_h);
+    if (e != cudaSuccess) return e;
+    GArgs g;
+    g.geo = geo;
     g.dst = p.dst;
     g.dpitch = p.dpitch;
     g.dslice = p.dslice;
     g.fin = fin;
     g.fpitch = fpitch;
     g.fslice = fslice;
+    g.bitmap = work.bitmap;
     g.rows = p.rows;
     g.cols = p.cols;
     g.row_begin = p.row_begin;
-    g.col_bits = col_bits;
-    g.row_bits = row_bits;
-    const long long npix = (long long)out_rows * p.cols * p.n_slices;
-    for (int l = 0; l < nlev; ++l) {
-        const int k = 5 + 2 * l;
-        g.qin = work.queue[l & 1];
-        g.nin = work.counts + l;
-        g.qout = (l + 1 < nlev) ? work.queue[(l + 1) & 1] : nullptr;
-        g.nout = work.counts + l + 1;
-        // grid sized for the worst case of this level, capped at a few waves (grid-stride loops)
-        const long long items = (k <= 7) ? (npix + 1) / 2 : npix;
-        const int blocks =
-            (int)std::max<long long>(1, std::min<long long>((items + 255) / 256, (long long)g_num_sms * 4));
-        switch (k) {
-            case 5: amf_grow_pair_kernel<5><<<blocks, 256, 0, stream>>>(g); break;
-            case 7: amf_grow_pair_kernel<7><<<blocks, 256, 0, stream>>>(g); break;
-            case 9: amf_grow_radix_kernel<9><<<blocks, 256, 0, stream>>>(g); break;
-            case 11: amf_grow_radix_kernel<11><<<blocks, 256, 0, stream>>>(g); break;
-            default: amf_grow_generic_kernel<<<blocks, 256, 0, stream>>>(g, k); break;
-        }
-        count_launch();
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    g.row_end = p.row_end;
+    g.n_slices = p.n_slices;
+    g.smax = smax;
+    g.tiles_x = a.tiles_x;
+    g.tiles_y = a.tiles_y;
+    static size_t gocc_smem = 0;
+    static int gper_sm = 1;
+    if (gocc_smem != gsm) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&gper_sm, amf_grow_kernel<false>, GNT, gsm);
+        if (gper_sm < 1) gper_sm = 1;
+        gocc_smem = gsm;
     }
-    return cudaSuccess;
+    const int ggrid = (int)std::min<long long>(ntiles, (long long)g_num_sms * gper_sm);
+    if (fin) amf_grow_kernel<true><<<ggrid, GNT, gsm, stream>>>(tm_g, g);
+    else amf_grow_kernel<false><<<ggrid, GNT, gsm, stream>>>(tm_g, g);
+    count_launch();
+    return cudaGetLastError();
 }
 
 }  // namespace hyb

@@ -58,7 +58,7 @@ struct hyb_ctx {
     cudaStream_t stream = nullptr;
     std::string err;
     DevBuf in, out, fin, f, wsum;      // staging / scratch
-    DevBuf amf_q[2], amf_cnt;          // AMF growth work queues
+    DevBuf amf_q[2], amf_cnt;          // AMF growth workspace (failure bitmap)
     std::vector<DevBuf> strip_g, strip_f;
     long long* host_w = nullptr;       // pinned readback of noise sums
     size_t host_w_n = 0;
@@ -167,15 +167,10 @@ cudaError_t copy2d(hyb_ctx* ctx, void* dst, size_t dp, const void* src, size_t s
 
 // AMF launch with the context's growth workspace.
 cudaError_t run_amf(hyb_ctx* ctx, const hyb::Plane& p, int smax, uint8_t* fin, size_t fpitch, size_t fslice) {
-    const size_t words = hyb::amf_queue_words(p);
     cudaError_t e;
-    if ((e = ctx->amf_q[0].ensure(words * 4)) != cudaSuccess) return e;
-    if ((e = ctx->amf_q[1].ensure(words * 4)) != cudaSuccess) return e;
-    if ((e = ctx->amf_cnt.ensure(128 * sizeof(int))) != cudaSuccess) return e;
+    if ((e = ctx->amf_q[0].ensure(hyb::amf_bitmap_bytes(p))) != cudaSuccess) return e;
     hyb::AmfWork w;
-    w.queue[0] = reinterpret_cast<uint32_t*>(ctx->amf_q[0].ptr);
-    w.queue[1] = reinterpret_cast<uint32_t*>(ctx->amf_q[1].ptr);
-    w.counts = reinterpret_cast<int*>(ctx->amf_cnt.ptr);
+    w.bitmap = ctx->amf_q[0].ptr;
     return hyb::launch_amf(p, smax, fin, fpitch, fslice, w, ctx->stream);
 }
 

@@ -20,15 +20,14 @@ struct Plane {
     int n_slices;
 };
 
-// Device workspace of the AMF growth stage: two ping-pong work queues (u32 pixel ids, capacity
-// amf_queue_words(p) each) and one int counter per growth level (smax <= 255 -> 127 levels).
+// Device workspace of the AMF growth stage: the per-tile level-A failure bitmap written by the
+// k = 3 kernel (amf_bitmap_bytes(p) bytes, 512 per 128 x 32 tile).
 struct AmfWork {
-    uint32_t* queue[2];
-    int* counts;
+    uint8_t* bitmap;
 };
-size_t amf_queue_words(const Plane& p);
+size_t amf_bitmap_bytes(const Plane& p);
 
-// AMF launch (amf.cu): k = 3 tile kernel + one growth kernel per k = 5..smax.  fin may be null.
+// AMF launch (amf.cu): k = 3 tile kernel + one tile-wise growth kernel (k = 5..smax).  fin may be null.
 cudaError_t launch_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, size_t fslice,
                        const AmfWork& work, cudaStream_t stream);
 
