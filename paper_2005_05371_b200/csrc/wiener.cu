@@ -224,11 +224,11 @@ cudaError_t launch(const Plane& p, int win, unsigned long long* wsum, const long
 // integer ops; statistics stay exact int32 per pixel.
 // ------------------------------------------------------------------------------------------
 constexpr int FW = 128;          // tile columns
-constexpr int FH = 16;           // tile rows
+constexpr int FH_MAX = 16;       // tile rows (8 for small images: shorter per-warp chains)
 constexpr int FCP = 16;          // column pad (TMA box x offsets must be 16-byte aligned)
 constexpr int FBS = FW + 2 * FCP;  // staged row bytes (160)
 constexpr int FNW = 8;           // warps per CTA
-__host__ __device__ constexpr int kFastSmemSlot(int rw) { return ((FBS * (FH + 2 * rw)) + 127) / 128 * 128; }
+__host__ __device__ constexpr int kFastSmemSlot(int rw, int fh) { return ((FBS * (fh + 2 * rw)) + 127) / 128 * 128; }
 
 struct FastArgs {
     uint8_t* dst;
@@ -309,13 +309,13 @@ __device__ __forceinline__ int win_count(int r, int lo, int hi, int n, int RW) {
     return cnt;
 }
 
-template <int RW, bool GAIN>
+template <int RW, bool GAIN, int FH>
 __global__ void __launch_bounds__(FNW * 32) wiener_fast_kernel(const __grid_constant__ CUtensorMap tm,
                                                                const __grid_constant__ FastArgs a) {
     constexpr int N = 2 * RW + 1;
     constexpr int NN = N * N;
     constexpr int SROWS = FH + 2 * RW;
-    constexpr int SLOT = kFastSmemSlot(RW);
+    constexpr int SLOT = kFastSmemSlot(RW, FH);
     extern __shared__ __align__(128) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -570,14 +570,14 @@ __global__ void __launch_bounds__(FNW * 32) wiener_fast_kernel(const __grid_cons
 
 int g_wsms = 0;
 
-template <int RW, bool GAIN>
+template <int RW, bool GAIN, int FH>
 cudaError_t launch_fast(const Plane& p, unsigned long long* wsum, const long long* wread, long long pixel_count,
                         cudaStream_t stream) {
-    constexpr int SLOT = kFastSmemSlot(RW);
+    constexpr int SLOT = kFastSmemSlot(RW, FH);
     constexpr size_t smem = 128 + (size_t)FNW * 2 * SLOT + 128;
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(wiener_fast_kernel<RW, GAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(wiener_fast_kernel<RW, GAIN, FH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
         if (e != cudaSuccess) return e;
         configured = true;
@@ -606,13 +606,13 @@ cudaError_t launch_fast(const Plane& p, unsigned long long* wsum, const long lon
     a.pixel_count = pixel_count;
     static int per_sm = 0;
     if (!per_sm) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, wiener_fast_kernel<RW, GAIN>, FNW * 32, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, wiener_fast_kernel<RW, GAIN, FH>, FNW * 32, smem);
         if (per_sm < 1) per_sm = 1;
     }
     const long long ntiles = (long long)a.tiles_x * a.tiles_y * a.n_slices;
     const long long warps = std::min<long long>(ntiles, (long long)g_wsms * per_sm * FNW);
     const int grid = (int)((warps + FNW - 1) / FNW);
-    wiener_fast_kernel<RW, GAIN><<<grid, FNW * 32, smem, stream>>>(tm, a);
+    wiener_fast_kernel<RW, GAIN, FH><<<grid, FNW * 32, smem, stream>>>(tm, a);
     count_launch();
     return cudaGetLastError();
 }
@@ -621,11 +621,18 @@ template <bool GAIN>
 cudaError_t dispatch(const Plane& p, int win, unsigned long long* wsum, const long long* wread,
                      long long pixel_count, cudaStream_t stream) {
     if (tma_compatible(p.src, p.spitch, p.sslice)) {
+        const long long px = (long long)(p.row_end - p.row_begin) * p.cols * p.n_slices;
+        const bool small = px < (16ll << 20);
         switch (win) {
-            case 1: return launch_fast<0, GAIN>(p, wsum, wread, pixel_count, stream);
-            case 3: return launch_fast<1, GAIN>(p, wsum, wread, pixel_count, stream);
-            case 5: return launch_fast<2, GAIN>(p, wsum, wread, pixel_count, stream);
-            case 7: return launch_fast<3, GAIN>(p, wsum, wread, pixel_count, stream);
+            // small images: 8-row tiles, twice the warps in flight and half the per-warp chain
+            case 1: return small ? launch_fast<0, GAIN, 8>(p, wsum, wread, pixel_count, stream)
+                                 : launch_fast<0, GAIN, 16>(p, wsum, wread, pixel_count, stream);
+            case 3: return small ? launch_fast<1, GAIN, 8>(p, wsum, wread, pixel_count, stream)
+                                 : launch_fast<1, GAIN, 16>(p, wsum, wread, pixel_count, stream);
+            case 5: return small ? launch_fast<2, GAIN, 8>(p, wsum, wread, pixel_count, stream)
+                                 : launch_fast<2, GAIN, 16>(p, wsum, wread, pixel_count, stream);
+            case 7: return small ? launch_fast<3, GAIN, 8>(p, wsum, wread, pixel_count, stream)
+                                 : launch_fast<3, GAIN, 16>(p, wsum, wread, pixel_count, stream);
             default: break;
         }
     }
