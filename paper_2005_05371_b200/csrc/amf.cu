@@ -331,14 +331,18 @@ __global__ void __launch_bounds__(NT, 3)
 // growth kernel (k = 5..smax): tile-wise, all levels from shared memory
 // ------------------------------------------------------------------------------------------
 
-// Tile geometry of the growth kernel: the 128 x 32 tile plus a halo of R = (smax-1)/2.
+constexpr int GNT = 256;         // threads per growth CTA
+constexpr int GK_MAX = 4;        // k = 3 tiles stacked in one growth tile (pools more failures per level)
+constexpr int GTH_MAX = GK_MAX * TH;
+
+// Tile geometry of the growth kernel: the 128 x 64 tile plus a halo of R = (smax-1)/2.
 struct GGeo {
     int R, CP, BS, BH;          // halo, column pad (multiple of 16), row stride, rows
     int box_w, nbx, box_h, nby;  // TMA boxes (<= 256 per dimension)
     int b_bytes;                 // bytes per tile buffer (128-aligned)
 };
 
-inline GGeo make_ggeo(int smax) {
+inline GGeo make_ggeo(int smax, int gk) {
     GGeo g;
     g.R = (smax - 1) / 2;
     g.CP = 16 * ((g.R + 15) / 16 > 0 ? (g.R + 15) / 16 : 1);
@@ -346,18 +350,17 @@ inline GGeo make_ggeo(int smax) {
     g.box_w = need <= 256 ? need : 128;
     g.nbx = (need + g.box_w - 1) / g.box_w;
     g.BS = g.box_w * g.nbx;
-    g.BH = TH + 2 * g.R;
+    g.BH = gk * TH + 2 * g.R;
     g.box_h = g.BH <= 256 ? g.BH : 128;
     g.nby = (g.BH + g.box_h - 1) / g.box_h;
     g.b_bytes = (g.BS * g.box_h * g.nby + 127) / 128 * 128;
     return g;
 }
 
-constexpr int GNT = 256;         // threads per growth CTA
 constexpr int GHDR = 1024;       // mbarriers, tile coordinates, level counters, scan scratch
 constexpr int MAX_LEVELS = 128;
 
-inline size_t grow_smem(const GGeo& g) { return GHDR + 2 * (size_t)g.b_bytes + 2 * TH * TW * 2 + 128; }
+inline size_t grow_smem(const GGeo& g, int gk) { return GHDR + 2 * (size_t)g.b_bytes + 2 * gk * TH * TW * 2 + 128; }
 
 struct GArgs {
     GGeo geo;
@@ -367,7 +370,8 @@ struct GArgs {
     size_t fpitch, fslice;
     const uint8_t* bitmap;
     int rows, cols, row_begin, row_end, n_slices, smax;
-    int tiles_x, tiles_y;
+    int tiles_x, tiles_y;    // k = 3 tiles
+    int gtiles_y;            // growth tiles per column (ceil(tiles_y / GK))
 };
 
 template <int K>
@@ -569,7 +573,7 @@ __device__ __forceinline__ void grow_tile_load(const CUtensorMap* tm, const GGeo
 // Persistent over tiles: the tile's failure bitmap (written by amf_k3_kernel) is compacted into a
 // shared-memory queue; if non-empty, the tile plus an R halo (TMA, double-buffered: the next tile
 // streams in meanwhile) serves every window size k = 5..smax, survivors re-compacted per level.
-template <bool FIN>
+template <bool FIN, int GK3>
 __global__ void __launch_bounds__(GNT) amf_grow_kernel(const __grid_constant__ CUtensorMap tm,
                                                       const __grid_constant__ GArgs args) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -581,17 +585,19 @@ __global__ void __launch_bounds__(GNT) amf_grow_kernel(const __grid_constant__ C
     int* wsum = reinterpret_cast<int*>(smem + 64 + 4 * MAX_LEVELS);  // [8] warp totals
     uint8_t* bufs = smem + GHDR;
     uint16_t* Q0 = reinterpret_cast<uint16_t*>(bufs + 2 * (size_t)geo.b_bytes);
-    uint16_t* Q1 = Q0 + TH * TW;
+    constexpr int GTH = GK3 * TH;
+    uint16_t* Q1 = Q0 + GTH * TW;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int per_slice = args.tiles_x * args.tiles_y;
+    const int per_slice = args.tiles_x * args.gtiles_y;
     const int ntiles = per_slice * args.n_slices;
     if ((int)blockIdx.x >= ntiles) return;
     auto coords = [&](int t, int* info) {
         const int z = t / per_slice, rem = t - z * per_slice;
         const int by = rem / args.tiles_x;
         info[0] = (rem - by * args.tiles_x) * TW;
-        info[1] = args.row_begin + by * TH;
+        info[1] = args.row_begin + by * GTH;
         info[2] = z;
+        info[3] = (z * args.tiles_y + by * GK3) * args.tiles_x + (rem - by * args.tiles_x);  // first k = 3 tile
     };
     if (tid == 0) {
         prefetch_tmap(&tm);
@@ -612,10 +618,22 @@ __global__ void __launch_bounds__(GNT) amf_grow_kernel(const __grid_constant__ C
                            tinfo[4 * (s ^ 1) + 1], tinfo[4 * (s ^ 1) + 2]);
         }
         if (tid < MAX_LEVELS) qcount[tid] = 0;
-        // ---- bitmap -> queue 0 (block scan; 16 bits per thread) ----
-        const uint32_t word = reinterpret_cast<const uint32_t*>(args.bitmap + (size_t)t * 512)[tid >> 1];
-        uint32_t bits = (word >> (16 * (tid & 1))) & 0xFFFFu;
-        const int nf = __popc(bits);
+        // ---- bitmap -> queue 0 (block scan; WPT words of 32 pixels per thread, raster order) ----
+        constexpr int WPT = (GK3 * 128 + GNT - 1) / GNT;
+        int kinfo[4];
+        coords(t, kinfo);
+        const int by3_0 = (kinfo[1] - args.row_begin) / TH;
+        uint32_t wbits[WPT];
+        int nf = 0;
+#pragma unroll
+        for (int j = 0; j < WPT; ++j) {
+            const int w = tid * WPT + j, sub_tile = w >> 7;
+            wbits[j] = w < GK3 * 128 && by3_0 + sub_tile < args.tiles_y
+                           ? reinterpret_cast<const uint32_t*>(args.bitmap +
+                                                               (size_t)(kinfo[3] + sub_tile * args.tiles_x) * 512)[w & 127]
+                           : 0u;
+            nf += __popc(wbits[j]);
+        }
         int incl = nf;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
@@ -633,11 +651,16 @@ __global__ void __launch_bounds__(GNT) amf_grow_kernel(const __grid_constant__ C
         }
         {
             int pos = wbase + incl - nf;
-            const int row = tid >> 3, colb = 16 * (tid & 7);  // 16 bits = row, columns colb..colb+15
-            while (bits) {
-                const int b = __ffs(bits) - 1;
-                bits &= bits - 1;
-                Q0[pos++] = (uint16_t)(row * TW + colb + b);
+#pragma unroll
+            for (int j = 0; j < WPT; ++j) {
+                const int w = tid * WPT + j;
+                const int row = (w >> 7) * TH + ((w & 127) >> 2), colb = 32 * (w & 3);
+                uint32_t bits = wbits[j];
+                while (bits) {
+                    const int b = __ffs(bits) - 1;
+                    bits &= bits - 1;
+                    Q0[pos++] = (uint16_t)(row * TW + colb + b);
+                }
             }
         }
         mbar_wait(&bar[s], (uint32_t)(it >> 1) & 1u);  // every thread observes the phase (keeps parity in step)
@@ -822,15 +845,19 @@ cudaError_t launch_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, si
     if ((e = cudaGetLastError()) != cudaSuccess || !grow) return e;
 
     // ---- growth: one tile-wise launch for every window size k = 5..smax ----
-    const GGeo geo = make_ggeo(smax);
-    const size_t gsm = grow_smem(geo);
-    static size_t gconfigured = 0;
-    if (gsm > gconfigured) {
-        e = cudaFuncSetAttribute(amf_grow_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(amf_grow_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm);
+    // small images: one k = 3 tile per growth tile (more CTAs in flight); large: four (more failures
+    // pooled per level round)
+    const int gk = (long long)out_rows * p.cols < (16ll << 20) ? 1 : GK_MAX;  // per image (stacks: per slice)
+    const GGeo geo = make_ggeo(smax, gk);
+    const size_t gsm = grow_smem(geo, gk);
+    auto kern = fin ? (gk == 1 ? amf_grow_kernel<true, 1> : amf_grow_kernel<true, GK_MAX>)
+                    : (gk == 1 ? amf_grow_kernel<false, 1> : amf_grow_kernel<false, GK_MAX>);
+    static size_t gconfigured[2][2] = {{0, 0}, {0, 0}};
+    size_t& conf = gconfigured[fin ? 1 : 0][gk == 1 ? 0 : 1];
+    if (gsm > conf) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm);
         if (e != cudaSuccess) return e;
-        gconfigured = gsm;
+        conf = gsm;
     }
     CUtensorMap tm_g;
     e = make_tmap_u8(&tm_g, p.src, p.cols, p.rows, p.n_slices, p.spitch, p.sslice, geo.box_w, geo.box_h);
@@ -852,16 +879,18 @@ cudaError_t launch_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, si
     g.smax = smax;
     g.tiles_x = a.tiles_x;
     g.tiles_y = a.tiles_y;
-    static size_t gocc_smem = 0;
-    static int gper_sm = 1;
-    if (gocc_smem != gsm) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&gper_sm, amf_grow_kernel<false>, GNT, gsm);
+    g.gtiles_y = (a.tiles_y + gk - 1) / gk;
+    static size_t occ_key[2][2] = {{0, 0}, {0, 0}};
+    static int occ_val[2][2] = {{1, 1}, {1, 1}};
+    int& gper_sm = occ_val[fin ? 1 : 0][gk == 1 ? 0 : 1];
+    if (occ_key[fin ? 1 : 0][gk == 1 ? 0 : 1] != gsm) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&gper_sm, kern, GNT, gsm);
         if (gper_sm < 1) gper_sm = 1;
-        gocc_smem = gsm;
+        occ_key[fin ? 1 : 0][gk == 1 ? 0 : 1] = gsm;
     }
-    const int ggrid = (int)std::min<long long>(ntiles, (long long)g_num_sms * gper_sm);
-    if (fin) amf_grow_kernel<true><<<ggrid, GNT, gsm, stream>>>(tm_g, g);
-    else amf_grow_kernel<false><<<ggrid, GNT, gsm, stream>>>(tm_g, g);
+    const long long gtiles = (long long)a.tiles_x * g.gtiles_y * a.n_slices;
+    const int ggrid = (int)std::min<long long>(gtiles, (long long)g_num_sms * gper_sm);
+    kern<<<ggrid, GNT, gsm, stream>>>(tm_g, g);
     count_launch();
     return cudaGetLastError();
 }
