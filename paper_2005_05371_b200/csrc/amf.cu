@@ -332,8 +332,6 @@ __global__ void __launch_bounds__(NT, 3)
 // ------------------------------------------------------------------------------------------
 
 constexpr int GNT = 256;         // threads per growth CTA
-constexpr int GK_MAX = 4;        // k = 3 tiles stacked in one growth tile (pools more failures per level)
-constexpr int GTH_MAX = GK_MAX * TH;
 
 // Tile geometry of the growth kernel: the 128 x 64 tile plus a halo of R = (smax-1)/2.
 struct GGeo {
@@ -342,7 +340,7 @@ struct GGeo {
     int b_bytes;                 // bytes per tile buffer (128-aligned)
 };
 
-inline GGeo make_ggeo(int smax, int gk) {
+inline GGeo make_ggeo(int smax) {
     GGeo g;
     g.R = (smax - 1) / 2;
     g.CP = 16 * ((g.R + 15) / 16 > 0 ? (g.R + 15) / 16 : 1);
@@ -350,7 +348,7 @@ inline GGeo make_ggeo(int smax, int gk) {
     g.box_w = need <= 256 ? need : 128;
     g.nbx = (need + g.box_w - 1) / g.box_w;
     g.BS = g.box_w * g.nbx;
-    g.BH = gk * TH + 2 * g.R;
+    g.BH = TH + 2 * g.R;
     g.box_h = g.BH <= 256 ? g.BH : 128;
     g.nby = (g.BH + g.box_h - 1) / g.box_h;
     g.b_bytes = (g.BS * g.box_h * g.nby + 127) / 128 * 128;
@@ -360,7 +358,7 @@ inline GGeo make_ggeo(int smax, int gk) {
 constexpr int GHDR = 1024;       // mbarriers, tile coordinates, level counters, scan scratch
 constexpr int MAX_LEVELS = 128;
 
-inline size_t grow_smem(const GGeo& g, int gk) { return GHDR + 2 * (size_t)g.b_bytes + 2 * gk * TH * TW * 2 + 128; }
+inline size_t grow_smem(const GGeo& g);
 
 struct GArgs {
     GGeo geo;
@@ -371,7 +369,6 @@ struct GArgs {
     const uint8_t* bitmap;
     int rows, cols, row_begin, row_end, n_slices, smax;
     int tiles_x, tiles_y;    // k = 3 tiles
-    int gtiles_y;            // growth tiles per column (ceil(tiles_y / GK))
 };
 
 template <int K>
@@ -425,6 +422,35 @@ __device__ __forceinline__ void level_pair(const uint8_t* __restrict__ B, const 
     uint32_t A[K][W::AW], Bw[K][W::AW];
     load_window<K>(B, geo, pa >> 7, pa & 127, A);
     load_window<K>(B, geo, pb >> 7, pb & 127, Bw);
+    uint32_t v[K * K];
+#pragma unroll
+    for (int r = 0; r < K; ++r)
+#pragma unroll
+        for (int e = 0; e < K; ++e) v[r * K + e] = pairw_rt(A[r][e >> 2], Bw[r][e >> 2], e & 3);
+    const uint32_t g = v[W::RK * K + W::RK];
+    uint32_t zmin, zmed, zmax;
+    select_net<K>(v, zmin, zmed, zmax);
+    done = 0;
+    outw = 0;
+#pragma unroll
+    for (int l = 0; l < 2; ++l) {
+        const uint32_t zn = (zmin >> (16 * l)) & 0xFFu, zd = (zmed >> (16 * l)) & 0xFFu;
+        const uint32_t zx = (zmax >> (16 * l)) & 0xFFu, gl = (g >> (16 * l)) & 0xFFu;
+        if (zn < zd && zd < zx) {
+            done |= 1u << l;
+            outw |= ((zn < gl && gl < zx) ? gl : zd) << (8 * l);
+        }
+    }
+}
+
+// Same with the two pixels in different tile slots.
+template <int K>
+__device__ __forceinline__ void level_pair2(const uint8_t* __restrict__ BA, const uint8_t* __restrict__ BB,
+                                            const GGeo& geo, int pa, int pb, uint32_t& done, uint32_t& outw) {
+    using W = Win<K>;
+    uint32_t A[K][W::AW], Bw[K][W::AW];
+    load_window<K>(BA, geo, pa >> 7, pa & 127, A);
+    load_window<K>(BB, geo, pb >> 7, pb & 127, Bw);
     uint32_t v[K * K];
 #pragma unroll
     for (int r = 0; r < K; ++r)
@@ -570,219 +596,272 @@ __device__ __forceinline__ void grow_tile_load(const CUtensorMap* tm, const GGeo
                         x0 - geo.CP + bx * geo.box_w, y0 - geo.R + by * geo.box_h, z);
 }
 
-// Persistent over tiles: the tile's failure bitmap (written by amf_k3_kernel) is compacted into a
-// shared-memory queue; if non-empty, the tile plus an R halo (TMA, double-buffered: the next tile
-// streams in meanwhile) serves every window size k = 5..smax, survivors re-compacted per level.
-template <bool FIN, int GK3>
+// Batched sparse growth.  Each CTA owns a contiguous range of k = 3 tiles.  Per batch it counts the
+// failures of the next GSLOTS tiles (their bitmaps, written by amf_k3_kernel), skips empty tiles
+// without loading them, TMA-loads the non-empty ones (tile + R halo, one slot each) and pools all
+// their failures into one shared-memory queue (entry = slot << 12 | pixel), so every level round
+// k = 5..smax runs full warps no matter how sparse the failures are.
+constexpr int GSLOTS = 8;
+constexpr int GCAP = 8192;  // pooled queue capacity (a single tile has at most 4096 entries)
+
+inline size_t grow_smem(const GGeo& g) { return GHDR + (size_t)GSLOTS * g.b_bytes + 2 * GCAP * 2 + 128; }
+
+template <bool FIN>
 __global__ void __launch_bounds__(GNT) amf_grow_kernel(const __grid_constant__ CUtensorMap tm,
                                                       const __grid_constant__ GArgs args) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
     const GGeo& geo = args.geo;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);  // [2]
-    int* tinfo = reinterpret_cast<int*>(smem + 16);       // [2][4]
-    int* qcount = reinterpret_cast<int*>(smem + 64);      // [MAX_LEVELS]
-    int* wsum = reinterpret_cast<int*>(smem + 64 + 4 * MAX_LEVELS);  // [8] warp totals
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);            // [GSLOTS]
+    int* sinfo = reinterpret_cast<int*>(smem + 64);                // [GSLOTS][4]: x0, y0, z, tile
+    int* cnt = reinterpret_cast<int*>(smem + 192);                 // [GSLOTS] failures per candidate tile
+    int* ctl = reinterpret_cast<int*>(smem + 224);                 // slots used, consumed, queue n, border mask
+    int* wsum = reinterpret_cast<int*>(smem + 256);                // [8] scan scratch
+    int* cinfo = reinterpret_cast<int*>(smem + 320);               // [GSLOTS][4] candidate coordinates
+    int* qcount = reinterpret_cast<int*>(smem + 448);              // [MAX_LEVELS]
     uint8_t* bufs = smem + GHDR;
-    uint16_t* Q0 = reinterpret_cast<uint16_t*>(bufs + 2 * (size_t)geo.b_bytes);
-    constexpr int GTH = GK3 * TH;
-    uint16_t* Q1 = Q0 + GTH * TW;
+    uint16_t* Q0 = reinterpret_cast<uint16_t*>(bufs + (size_t)GSLOTS * geo.b_bytes);
+    uint16_t* Q1 = Q0 + GCAP;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int per_slice = args.tiles_x * args.gtiles_y;
-    const int ntiles = per_slice * args.n_slices;
-    if ((int)blockIdx.x >= ntiles) return;
-    auto coords = [&](int t, int* info) {
-        const int z = t / per_slice, rem = t - z * per_slice;
-        const int by = rem / args.tiles_x;
-        info[0] = (rem - by * args.tiles_x) * TW;
-        info[1] = args.row_begin + by * GTH;
-        info[2] = z;
-        info[3] = (z * args.tiles_y + by * GK3) * args.tiles_x + (rem - by * args.tiles_x);  // first k = 3 tile
-    };
-    if (tid == 0) {
-        prefetch_tmap(&tm);
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        fence_mbar_init();
-        coords(blockIdx.x, tinfo);
-        grow_tile_load(&tm, geo, bufs, &bar[0], tinfo[0], tinfo[1], tinfo[2]);
-    }
+    const int per_slice = args.tiles_x * args.tiles_y;
+    const long long ntiles = (long long)per_slice * args.n_slices;
+    const int chunk = (int)((ntiles + gridDim.x - 1) / gridDim.x);
+    int cursor = blockIdx.x * chunk;
+    const int end = (int)(ntiles < (long long)cursor + chunk ? ntiles : (long long)cursor + chunk);
+    if (tid < GSLOTS) mbar_init(&bar[tid], 1);
+    if (tid == 0) fence_mbar_init();
+    uint32_t phases = 0;  // per-slot mbarrier parity
     __syncthreads();
-    int it = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-        const int s = it & 1;
-        if (tid == 0 && t + (int)gridDim.x < ntiles) {  // prefetch the next tile (its slot was freed last iteration)
-            coords(t + gridDim.x, tinfo + 4 * (s ^ 1));
-            fence_proxy_async_smem();
-            grow_tile_load(&tm, geo, bufs + (size_t)(s ^ 1) * geo.b_bytes, &bar[s ^ 1], tinfo[4 * (s ^ 1)],
-                           tinfo[4 * (s ^ 1) + 1], tinfo[4 * (s ^ 1) + 2]);
-        }
+
+    while (cursor < end) {
+        // ---- 1. failures and coordinates of the next GSLOTS tiles (warp w: tile cursor + w) ----
         if (tid < MAX_LEVELS) qcount[tid] = 0;
-        // ---- bitmap -> queue 0 (block scan; WPT words of 32 pixels per thread, raster order) ----
-        constexpr int WPT = (GK3 * 128 + GNT - 1) / GNT;
-        int kinfo[4];
-        coords(t, kinfo);
-        const int by3_0 = (kinfo[1] - args.row_begin) / TH;
-        uint32_t wbits[WPT];
-        int nf = 0;
-#pragma unroll
-        for (int j = 0; j < WPT; ++j) {
-            const int w = tid * WPT + j, sub_tile = w >> 7;
-            wbits[j] = w < GK3 * 128 && by3_0 + sub_tile < args.tiles_y
-                           ? reinterpret_cast<const uint32_t*>(args.bitmap +
-                                                               (size_t)(kinfo[3] + sub_tile * args.tiles_x) * 512)[w & 127]
-                           : 0u;
-            nf += __popc(wbits[j]);
-        }
-        int incl = nf;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const int v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
-            if (lane >= d) incl += v;
-        }
-        if (lane == 31) wsum[warp] = incl;
-        __syncthreads();
-        int wbase = 0, n = 0;
-#pragma unroll
-        for (int w = 0; w < GNT / 32; ++w) {
-            const int v = wsum[w];
-            wbase += w < warp ? v : 0;
-            n += v;
-        }
         {
-            int pos = wbase + incl - nf;
+            const int t = cursor + warp;
+            int c = 0;
+            if (t < end) {
+                const uint4 w4 = reinterpret_cast<const uint4*>(args.bitmap + (size_t)t * 512)[lane];
+                c = __popc(w4.x) + __popc(w4.y) + __popc(w4.z) + __popc(w4.w);
+            }
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) c += __shfl_down_sync(0xFFFFFFFFu, c, d);
+            if (lane == 0) {
+                cnt[warp] = t < end ? c : -1;
+                const int z = t / per_slice, rem = t - z * per_slice, by = rem / args.tiles_x;
+                int* ci = cinfo + 4 * warp;
+                ci[0] = (rem - by * args.tiles_x) * TW;
+                ci[1] = args.row_begin + by * TH;
+                ci[2] = z;
+                ci[3] = t;
+            }
+        }
+        __syncthreads();
+        // ---- 2. choose the batch (non-empty tiles within capacity) and issue their TMA loads ----
+        if (tid == 0) {
+            int ns = 0, total = 0, consumed = 0, borders = 0;
+            for (int w = 0; w < GSLOTS; ++w) {
+                if (cnt[w] < 0) break;
+                if (cnt[w] > 0) {
+                    if (total + cnt[w] > GCAP) break;
+                    const int* ci = cinfo + 4 * w;
+                    int* si = sinfo + 4 * ns;
+                    si[0] = ci[0];
+                    si[1] = ci[1];
+                    si[2] = ci[2];
+                    si[3] = ci[3];
+                    grow_tile_load(&tm, geo, bufs + (size_t)ns * geo.b_bytes, &bar[ns], ci[0], ci[1], ci[2]);
+                    const int sx0 = ci[0] - geo.CP, sy0 = ci[1] - geo.R;
+                    if (sx0 < 0 || sx0 + geo.BS > args.cols || sy0 < 0 || sy0 + geo.BH > args.rows) borders |= 1 << ns;
+                    total += cnt[w];
+                    ++ns;
+                }
+                consumed = w + 1;
+            }
+            ctl[0] = ns;
+            ctl[1] = consumed;
+            ctl[3] = borders;
+        }
+        __syncthreads();
+        const int ns = ctl[0];
+        cursor += ctl[1];
+        if (ns == 0) continue;  // (the loop-top writes of qcount/cnt happen after this barrier)
+        // ---- 3. pooled queue: entries slot << 12 | pixel, raster order within each tile ----
+        {
+            constexpr int WPT = GSLOTS * 128 / GNT;  // words per thread (4)
+            uint32_t wb[WPT];
+            int nf = 0;
+#pragma unroll
+            for (int j = 0; j < WPT; ++j) {
+                const int w = tid * WPT + j, sl = w >> 7;
+                wb[j] = sl < ns ? reinterpret_cast<const uint32_t*>(args.bitmap + (size_t)sinfo[4 * sl + 3] * 512)[w & 127]
+                                : 0u;
+                nf += __popc(wb[j]);
+            }
+            int incl = nf;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+                if (lane >= d) incl += v;
+            }
+            if (lane == 31) wsum[warp] = incl;
+            __syncthreads();
+            int pos = incl - nf;
+#pragma unroll
+            for (int w = 0; w < GNT / 32; ++w) pos += w < warp ? wsum[w] : 0;
+            if (tid == 0) {
+                int n = 0;
+#pragma unroll
+                for (int w = 0; w < GNT / 32; ++w) n += wsum[w];
+                ctl[2] = n;
+            }
 #pragma unroll
             for (int j = 0; j < WPT; ++j) {
                 const int w = tid * WPT + j;
-                const int row = (w >> 7) * TH + ((w & 127) >> 2), colb = 32 * (w & 3);
-                uint32_t bits = wbits[j];
+                const uint32_t base = ((uint32_t)(w >> 7) << 12) | (uint32_t)(((w & 127) >> 2) * TW + 32 * (w & 3));
+                uint32_t bits = wb[j];
                 while (bits) {
                     const int b = __ffs(bits) - 1;
                     bits &= bits - 1;
-                    Q0[pos++] = (uint16_t)(row * TW + colb + b);
+                    Q0[pos++] = (uint16_t)(base + b);
                 }
             }
         }
-        mbar_wait(&bar[s], (uint32_t)(it >> 1) & 1u);  // every thread observes the phase (keeps parity in step)
-        const int x0 = tinfo[4 * s], y0 = tinfo[4 * s + 1], z = tinfo[4 * s + 2];
-        uint8_t* B = bufs + (size_t)s * geo.b_bytes;
-        if (n > 0) {
-            // ---- border tiles: edge replication in place of TMA's zero fill ----
-            const int sx0 = x0 - geo.CP, sy0 = y0 - geo.R;
-            if (sx0 < 0 || sx0 + geo.BS > args.cols || sy0 < 0 || sy0 + geo.BH > args.rows) {
+        // ---- 4. tiles landed; border tiles get edge replication (whole CTA, columns then rows) ----
+        for (int sl = 0; sl < ns; ++sl) mbar_wait(&bar[sl], (phases >> sl) & 1u);
+        phases ^= (1u << ns) - 1u;
+        const int borders = ctl[3];
+        if (borders) {
+            for (int m = borders; m; m &= m - 1) {
+                const int sl = __ffs(m) - 1;
+                uint8_t* B = bufs + (size_t)sl * geo.b_bytes;
+                const int sx0 = sinfo[4 * sl] - geo.CP, sy0 = sinfo[4 * sl + 1] - geo.R;
                 const int c_lo = max(0, -sx0), c_hi = min(geo.BS, args.cols - sx0);
                 const int r_lo = max(0, -sy0), r_hi = min(geo.BH, args.rows - sy0);
-                if (c_lo > 0 || c_hi < geo.BS) {
-                    for (int rr = r_lo + warp; rr < r_hi; rr += GNT / 32) {
-                        uint8_t* row = B + (size_t)rr * geo.BS;
-                        const uint8_t lv = row[c_lo], rv = row[c_hi - 1];
-                        for (int cc = lane; cc < geo.BS; cc += 32) {
-                            if (cc < c_lo) row[cc] = lv;
-                            else if (cc >= c_hi) row[cc] = rv;
-                        }
-                    }
-                }
-                __syncthreads();
-                const int words = geo.BS >> 2;
-                for (int idx = tid; idx < geo.BH * words; idx += GNT) {
-                    const int rr = idx / words, q = idx - rr * words;
-                    const int src_r = rr < r_lo ? r_lo : (rr >= r_hi ? r_hi - 1 : rr);
-                    if (src_r != rr)
-                        reinterpret_cast<uint32_t*>(B + (size_t)rr * geo.BS)[q] =
-                            reinterpret_cast<const uint32_t*>(B + (size_t)src_r * geo.BS)[q];
+                const int nl = c_lo, nfix = c_lo + (geo.BS - c_hi);
+                if (nfix == 0) continue;
+                for (int i = tid; i < (r_hi - r_lo) * nfix; i += GNT) {
+                    const int rr = r_lo + i / nfix, j = i - (rr - r_lo) * nfix;
+                    uint8_t* row = B + (size_t)rr * geo.BS;
+                    if (j < nl) row[j] = row[c_lo];
+                    else row[c_hi + (j - nl)] = row[c_hi - 1];
                 }
             }
             __syncthreads();
-            uint8_t* dtile = args.dst + (size_t)z * args.dslice + (size_t)(y0 - args.row_begin) * args.dpitch + x0;
-            uint8_t* ftile = FIN ? args.fin + (size_t)z * args.fslice + (size_t)(y0 - args.row_begin) * args.fpitch + x0
-                                 : nullptr;
-            int lvl = 0;
-            for (int k = 5; k <= args.smax; k += 2, ++lvl) {
-                const uint16_t* qin = (lvl & 1) ? Q1 : Q0;
-                uint16_t* qout = (lvl & 1) ? Q0 : Q1;
-                const bool last = k + 2 > args.smax;
-                if (k <= 7) {
-                    const int npairs = (n + 1) >> 1;
-                    for (int base = warp * 32; base < npairs; base += GNT) {
-                        const int i = base + lane;
-                        uint32_t keep = 0;
-                        int pa = 0, pb = 0;
-                        if (i < npairs) {
-                            pa = qin[2 * i];
-                            const bool hasb = 2 * i + 1 < n;
-                            pb = hasb ? qin[2 * i + 1] : pa;
-                            uint32_t done, outw;
-                            if (k == 5) level_pair<5>(B, geo, pa, pb, done, outw);
-                            else level_pair<7>(B, geo, pa, pb, done, outw);
-                            if (done & 1u) {
-                                dtile[(size_t)(pa >> 7) * args.dpitch + (pa & 127)] = (uint8_t)outw;
-                                if (FIN) ftile[(size_t)(pa >> 7) * args.fpitch + (pa & 127)] = (uint8_t)k;
-                            } else {
-                                keep |= 1u;
-                            }
-                            if (hasb) {
-                                if (done & 2u) {
-                                    dtile[(size_t)(pb >> 7) * args.dpitch + (pb & 127)] = (uint8_t)(outw >> 8);
-                                    if (FIN) ftile[(size_t)(pb >> 7) * args.fpitch + (pb & 127)] = (uint8_t)k;
-                                } else {
-                                    keep |= 2u;
-                                }
-                            }
+            for (int m = borders; m; m &= m - 1) {
+                const int sl = __ffs(m) - 1;
+                uint8_t* B = bufs + (size_t)sl * geo.b_bytes;
+                const int sy0 = sinfo[4 * sl + 1] - geo.R;
+                const int r_lo = max(0, -sy0), r_hi = min(geo.BH, args.rows - sy0);
+                const int nfr = geo.BH - (r_hi - r_lo), wpr = geo.BS / 4;
+                for (int i = tid; i < nfr * wpr; i += GNT) {
+                    const int k = i / wpr, q = i - k * wpr;
+                    const int rr = k < r_lo ? k : r_hi + (k - r_lo);
+                    const int src_r = rr < r_lo ? r_lo : r_hi - 1;
+                    reinterpret_cast<uint32_t*>(B + (size_t)rr * geo.BS)[q] =
+                        reinterpret_cast<const uint32_t*>(B + (size_t)src_r * geo.BS)[q];
+                }
+            }
+        }
+        __syncthreads();
+        // ---- 5. levels, pooled over the batch ----
+        int n = ctl[2];
+        auto out_ptr = [&](int sl, int pix, bool f) -> uint8_t* {
+            const int* si = sinfo + 4 * sl;
+            return f ? args.fin + (size_t)si[2] * args.fslice + (size_t)(si[1] - args.row_begin + (pix >> 7)) * args.fpitch +
+                           si[0] + (pix & 127)
+                     : args.dst + (size_t)si[2] * args.dslice + (size_t)(si[1] - args.row_begin + (pix >> 7)) * args.dpitch +
+                           si[0] + (pix & 127);
+        };
+        int lvl = 0;
+        for (int k = 5; k <= args.smax; k += 2, ++lvl) {
+            const uint16_t* qin = (lvl & 1) ? Q1 : Q0;
+            uint16_t* qout = (lvl & 1) ? Q0 : Q1;
+            const bool last = k + 2 > args.smax;
+            if (k <= 7) {
+                const int npairs = (n + 1) >> 1;
+                for (int base = warp * 32; base < npairs; base += GNT) {
+                    const int i = base + lane;
+                    uint32_t keep = 0;
+                    int ea = 0, eb = 0;
+                    if (i < npairs) {
+                        ea = qin[2 * i];
+                        const bool hasb = 2 * i + 1 < n;
+                        eb = hasb ? qin[2 * i + 1] : ea;
+                        const int sa = ea >> 12, pa = ea & 4095, sb = eb >> 12, pb = eb & 4095;
+                        uint32_t done, outw;
+                        const uint8_t* BA = bufs + (size_t)sa * geo.b_bytes;
+                        const uint8_t* BB = bufs + (size_t)sb * geo.b_bytes;
+                        if (k == 5) level_pair2<5>(BA, BB, geo, pa, pb, done, outw);
+                        else level_pair2<7>(BA, BB, geo, pa, pb, done, outw);
+                        if (done & 1u) {
+                            *out_ptr(sa, pa, false) = (uint8_t)outw;
+                            if (FIN) *out_ptr(sa, pa, true) = (uint8_t)k;
+                        } else {
+                            keep |= 1u;
                         }
-                        if (!last) {
-                            const uint32_t balA = __ballot_sync(0xFFFFFFFFu, keep & 1u);
-                            const uint32_t balB = __ballot_sync(0xFFFFFFFFu, keep & 2u);
-                            const int cnt = __popc(balA) + __popc(balB);
-                            if (cnt) {
-                                int qb = 0;
-                                if (lane == 0) qb = atomicAdd(&qcount[lvl + 1], cnt);
-                                qb = __shfl_sync(0xFFFFFFFFu, qb, 0);
-                                const uint32_t below = (1u << lane) - 1u;
-                                if (keep & 1u) qout[qb + __popc(balA & below)] = (uint16_t)pa;
-                                if (keep & 2u) qout[qb + __popc(balA) + __popc(balB & below)] = (uint16_t)pb;
+                        if (hasb) {
+                            if (done & 2u) {
+                                *out_ptr(sb, pb, false) = (uint8_t)(outw >> 8);
+                                if (FIN) *out_ptr(sb, pb, true) = (uint8_t)k;
+                            } else {
+                                keep |= 2u;
                             }
                         }
                     }
-                } else {
-                    for (int base = warp * 32; base < n; base += GNT) {
-                        const int i = base + lane;
-                        bool keep = false;
-                        int pix = 0;
-                        if (i < n) {
-                            pix = qin[i];
-                            const int ty = pix >> 7, tx = pix & 127;
-                            uint8_t o = 0;
-                            bool done;
-                            switch (k) {
-                                case 9: done = level_radix<9>(B, geo, ty, tx, &o); break;
-                                case 11: done = level_radix<11>(B, geo, ty, tx, &o); break;
-                                default: done = level_generic(B, geo, ty, tx, k, &o); break;
-                            }
-                            if (done) {
-                                dtile[(size_t)ty * args.dpitch + tx] = o;
-                                if (FIN) ftile[(size_t)ty * args.fpitch + tx] = (uint8_t)k;
-                            } else {
-                                keep = true;
-                            }
-                        }
-                        if (!last) {
-                            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, keep);
-                            if (bal) {
-                                int qb = 0;
-                                if (lane == 0) qb = atomicAdd(&qcount[lvl + 1], __popc(bal));
-                                qb = __shfl_sync(0xFFFFFFFFu, qb, 0);
-                                if (keep) qout[qb + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)pix;
-                            }
+                    if (!last) {
+                        const uint32_t balA = __ballot_sync(0xFFFFFFFFu, keep & 1u);
+                        const uint32_t balB = __ballot_sync(0xFFFFFFFFu, keep & 2u);
+                        const int c = __popc(balA) + __popc(balB);
+                        if (c) {
+                            int qb = 0;
+                            if (lane == 0) qb = atomicAdd(&qcount[lvl + 1], c);
+                            qb = __shfl_sync(0xFFFFFFFFu, qb, 0);
+                            const uint32_t below = (1u << lane) - 1u;
+                            if (keep & 1u) qout[qb + __popc(balA & below)] = (uint16_t)ea;
+                            if (keep & 2u) qout[qb + __popc(balA) + __popc(balB & below)] = (uint16_t)eb;
                         }
                     }
                 }
-                __syncthreads();
-                if (last) break;
-                n = qcount[lvl + 1];
-                if (n == 0) break;
+            } else {
+                for (int base = warp * 32; base < n; base += GNT) {
+                    const int i = base + lane;
+                    bool keep = false;
+                    int e = 0;
+                    if (i < n) {
+                        e = qin[i];
+                        const int sl = e >> 12, pix = e & 4095, ty = pix >> 7, tx = pix & 127;
+                        const uint8_t* B = bufs + (size_t)sl * geo.b_bytes;
+                        uint8_t o = 0;
+                        bool done;
+                        switch (k) {
+                            case 9: done = level_radix<9>(B, geo, ty, tx, &o); break;
+                            case 11: done = level_radix<11>(B, geo, ty, tx, &o); break;
+                            default: done = level_generic(B, geo, ty, tx, k, &o); break;
+                        }
+                        if (done) {
+                            *out_ptr(sl, pix, false) = o;
+                            if (FIN) *out_ptr(sl, pix, true) = (uint8_t)k;
+                        } else {
+                            keep = true;
+                        }
+                    }
+                    if (!last) {
+                        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, keep);
+                        if (bal) {
+                            int qb = 0;
+                            if (lane == 0) qb = atomicAdd(&qcount[lvl + 1], __popc(bal));
+                            qb = __shfl_sync(0xFFFFFFFFu, qb, 0);
+                            if (keep) qout[qb + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)e;
+                        }
+                    }
+                }
             }
+            __syncthreads();
+            if (last) break;
+            n = qcount[lvl + 1];
+            if (n == 0) break;
         }
-        __syncthreads();  // this slot, the queues and the level counters are reused next iteration
+        __syncthreads();  // slots, queues and counters are reused by the next batch
     }
 }
 
@@ -844,20 +923,15 @@ cudaError_t launch_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, si
     count_launch();
     if ((e = cudaGetLastError()) != cudaSuccess || !grow) return e;
 
-    // ---- growth: one tile-wise launch for every window size k = 5..smax ----
-    // small images: one k = 3 tile per growth tile (more CTAs in flight); large: four (more failures
-    // pooled per level round)
-    const int gk = (long long)out_rows * p.cols < (16ll << 20) ? 1 : GK_MAX;  // per image (stacks: per slice)
-    const GGeo geo = make_ggeo(smax, gk);
-    const size_t gsm = grow_smem(geo, gk);
-    auto kern = fin ? (gk == 1 ? amf_grow_kernel<true, 1> : amf_grow_kernel<true, GK_MAX>)
-                    : (gk == 1 ? amf_grow_kernel<false, 1> : amf_grow_kernel<false, GK_MAX>);
-    static size_t gconfigured[2][2] = {{0, 0}, {0, 0}};
-    size_t& conf = gconfigured[fin ? 1 : 0][gk == 1 ? 0 : 1];
-    if (gsm > conf) {
+    // ---- growth: one batched launch for every window size k = 5..smax ----
+    const GGeo geo = make_ggeo(smax);
+    const size_t gsm = grow_smem(geo);
+    auto kern = fin ? amf_grow_kernel<true> : amf_grow_kernel<false>;
+    static size_t gconfigured[2] = {0, 0};
+    if (gsm > gconfigured[fin ? 1 : 0]) {
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm);
         if (e != cudaSuccess) return e;
-        conf = gsm;
+        gconfigured[fin ? 1 : 0] = gsm;
     }
     CUtensorMap tm_g;
     e = make_tmap_u8(&tm_g, p.src, p.cols, p.rows, p.n_slices, p.spitch, p.sslice, geo.box_w, geo.box_h);
@@ -879,17 +953,16 @@ cudaError_t launch_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, si
     g.smax = smax;
     g.tiles_x = a.tiles_x;
     g.tiles_y = a.tiles_y;
-    g.gtiles_y = (a.tiles_y + gk - 1) / gk;
-    static size_t occ_key[2][2] = {{0, 0}, {0, 0}};
-    static int occ_val[2][2] = {{1, 1}, {1, 1}};
-    int& gper_sm = occ_val[fin ? 1 : 0][gk == 1 ? 0 : 1];
-    if (occ_key[fin ? 1 : 0][gk == 1 ? 0 : 1] != gsm) {
+    static size_t occ_key[2] = {0, 0};
+    static int occ_val[2] = {1, 1};
+    int& gper_sm = occ_val[fin ? 1 : 0];
+    if (occ_key[fin ? 1 : 0] != gsm) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&gper_sm, kern, GNT, gsm);
         if (gper_sm < 1) gper_sm = 1;
-        occ_key[fin ? 1 : 0][gk == 1 ? 0 : 1] = gsm;
+        occ_key[fin ? 1 : 0] = gsm;
     }
-    const long long gtiles = (long long)a.tiles_x * g.gtiles_y * a.n_slices;
-    const int ggrid = (int)std::min<long long>(gtiles, (long long)g_num_sms * gper_sm);
+    // every resident CTA slot busy; each CTA takes a contiguous run of tiles
+    const int ggrid = (int)std::min<long long>(ntiles, (long long)g_num_sms * gper_sm);
     kern<<<ggrid, GNT, gsm, stream>>>(tm_g, g);
     count_launch();
     return cudaGetLastError();

@@ -36,7 +36,8 @@ def main(path, npx, top=40, fsub=""):
     tot = sum(v[0] for v in data.values())
     tots = sum(v[1] for v in data.values())
     print(f"thread-instr/px {tot / npx:.1f}  stall samples {tots:.0f}")
-    for (f, ln), (v, s, src) in sorted(data.items(), key=lambda kv: -kv[1][0])[:top]:
+    col = 1 if __import__("os").environ.get("SORT") == "stall" else 0
+    for (f, ln), (v, s, src) in sorted(data.items(), key=lambda kv: -kv[1][col])[:top]:
         print(f"{v / max(tot, 1):6.1%} instr {s / max(tots, 1):6.1%} stall  {f}:{ln:>4} {src}")
 
 
