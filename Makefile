@@ -26,11 +26,16 @@ $(LIB): $(SRCS) $(HDRS)
 	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRCS) 2> build_ptxas.log || (cat build_ptxas.log; exit 1)
 	@grep -E "registers|spill" build_ptxas.log | sed 's/^ptxas info    : //' | head -40
 
+# phase-timestamp build of the same library (tools/trace_amf.py); not used by tests or bench
+trace: $(PKG)/libhybrid_cuda_trace.so
+$(PKG)/libhybrid_cuda_trace.so: $(SRCS) $(HDRS)
+	$(NVCC) $(NVFLAGS) -DHYB_TRACE -shared -o $@ $(SRCS) 2> /dev/null
+
 oracle:
 	$(MAKE) -C oracle --no-print-directory
 
 clean:
-	rm -f $(LIB) $(HOSTLIB) $(CPPTEST) build_ptxas.log
+	rm -f $(LIB) $(PKG)/libhybrid_cuda_trace.so $(HOSTLIB) $(CPPTEST) build_ptxas.log
 	$(MAKE) -C oracle clean
 
-.PHONY: all oracle clean
+.PHONY: all oracle clean trace

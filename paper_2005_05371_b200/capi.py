@@ -16,7 +16,9 @@ import numpy as np
 
 HYB_OK, HYB_EINVAL, HYB_ECUDA, HYB_ENCCL, HYB_ENOMEM = 0, 1, 2, 3, 4
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhybrid_cuda.so")
+# HYB_LIB selects a debug build of the same library in this directory (e.g. the `make trace` one)
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                        os.path.basename(os.environ.get("HYB_LIB", "libhybrid_cuda.so")))
 
 # Every symbol include/hybrid_cuda.h declares (checked by tests/test_capi_symbols.py).
 EXPORTED = (

@@ -44,7 +44,8 @@ constexpr int BS = TW + 2 * CP;  // byte-tile row stride = TMA box width (160)
 constexpr int BH = TH + 2;       // byte-tile rows (1-pixel halo)
 constexpr int BBYTES = (BS * BH + 127) / 128 * 128;  // ring slot (TMA destinations are 128-byte aligned)
 constexpr int NBUF = 4;          // TMA ring depth
-constexpr int HDR = 128;         // mbarriers, release counters, tile coordinates
+constexpr int HDR = 256;         // mbarriers, counters, tile coordinates
+constexpr int K3T = NT + 32;     // + one producer warp (tile claims and TMA loads)
 constexpr int WAREA = 2 * WPIX;  // per warp: output strip, finalized_at strip
 constexpr size_t SMEM = HDR + NBUF * BBYTES + NW * WAREA + 128;
 
@@ -101,7 +102,15 @@ struct K3Args {
     int tiles_x, tiles_y;
     int grow;                // record level-A failures (smax >= 5)
     uint8_t* bitmap;         // per tile 32 rows x 16 bytes: bit c%8 of byte c/8 = pixel (row, c) failed level A
+    int dynamic;             // tiles claimed from `claim` (else blockIdx.x + i * gridDim.x)
+    int* claim;              // global tile-claim counter (reset by the last CTA to finish)
+    int* done;               // CTAs finished
+    unsigned long long* rec_ctr;  // (records << 40) | failures, advanced once per tile with failures
+    unsigned long long* records;  // [record] = (failure offset << 24) | tile
 };
+
+constexpr int REC_SHIFT = 40;
+constexpr unsigned long long REC_MASK = (1ull << REC_SHIFT) - 1;
 
 __device__ __forceinline__ void issue_tile_load(const CUtensorMap* tm, uint8_t* Bbuf, uint64_t* bar, int x0, int y0,
                                                 int z) {
@@ -118,50 +127,103 @@ __device__ __forceinline__ void tile_coords(const K3Args& a, int t, int* info) {
     info[2] = z;
 }
 
+#ifdef HYB_TRACE
+// Debug builds only (make trace): per-CTA phase timestamps, read back with hyb_trace_read.
+__device__ unsigned long long g_trace[2 * 1024 * 16];
+__device__ __forceinline__ void trace_mark(int kid, int slot) {
+    if (threadIdx.x == 0 && blockIdx.x < 1024) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_trace[(kid * 1024 + blockIdx.x) * 16 + slot] = t;
+    }
+}
+#ifndef HYB_TRACE_MASK
+#define HYB_TRACE_MASK 3
+#endif
+#define TRACE(kid, slot)                                  \
+    do {                                                  \
+        if ((HYB_TRACE_MASK >> (kid)) & 1) trace_mark(kid, slot); \
+    } while (0)
+#else
+#define TRACE(kid, slot) \
+    do {                 \
+    } while (0)
+#endif
+
 template <bool FIN>
-__global__ void __launch_bounds__(NT, 3)
+__global__ void __launch_bounds__(K3T, 3)
     amf_k3_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ K3Args args) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // [NBUF]
-    int* done_cnt = reinterpret_cast<int*>(smem + 32);     // [NBUF]
-    int* next_strip = reinterpret_cast<int*>(smem + 48);   // dynamic strip counter
-    int* tinfo = reinterpret_cast<int*>(smem + 64);        // [NBUF][4]
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);        // [NBUF] tile landed (or: no tile)
+    uint64_t* empty = reinterpret_cast<uint64_t*>(smem + 32);  // [NBUF] all strips of the slot done
+    int* done_cnt = reinterpret_cast<int*>(smem + 64);           // [NBUF] strips finished
+    int* fcount = reinterpret_cast<int*>(smem + 80);             // [NBUF] level-A failures of the slot's tile
+    int* next_strip = reinterpret_cast<int*>(smem + 96);         // dynamic strip counter
+    int* tinfo = reinterpret_cast<int*>(smem + 128);             // [NBUF][4]: x0, y0, z, tile (-1: none)
     uint8_t* bufs = smem + HDR;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    uint8_t* O = bufs + NBUF * BBYTES + warp * WAREA;
-    uint8_t* F = O + WPIX;
 
     const int rows = args.rows, cols = args.cols;
     const int ntiles = args.tiles_x * args.tiles_y * args.n_slices;
-    if ((int)blockIdx.x >= ntiles) return;
-    const int my_tiles = (ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
 
     if (tid == 0) {
         prefetch_tmap(&tm_src);
         for (int s = 0; s < NBUF; ++s) {
             mbar_init(&full[s], 1);
+            mbar_init(&empty[s], TH / WR);
             done_cnt[s] = 0;
+            fcount[s] = 0;
         }
         *next_strip = 0;
         fence_mbar_init();
-        for (int s = 0; s < NBUF && s < my_tiles; ++s) {
-            tile_coords(args, blockIdx.x + s * gridDim.x, tinfo + 4 * s);
-            issue_tile_load(&tm_src, bufs + s * BBYTES, &full[s], tinfo[4 * s], tinfo[4 * s + 1], tinfo[4 * s + 2]);
-        }
     }
     __syncthreads();
+    grid_dep_wait();  // the previous grid (e.g. the last step's gain reading dst) has completed
+    TRACE(0, 0);
 
-    // Strips (4-row slices of this CTA's tiles, in order) are claimed dynamically by warps.
+    if (warp == NW) {
+        // ---- producer: claims tiles from the global counter in ring order (so the first empty
+        //      claim ends the CTA's sequence) and TMA-loads them ----
+        if (lane == 0) {
+            for (int ti = 0;; ++ti) {
+                const int s = ti & (NBUF - 1);
+                if (ti >= NBUF) mbar_wait(&empty[s], (uint32_t)(ti / NBUF - 1) & 1u);
+                // few tiles per CTA: static round-robin (a prefetching dynamic claimer would grab up
+                // to NBUF tiles per CTA up front); many: dynamic claims balance the SMs
+                const int t = args.dynamic ? atomicAdd(args.claim, 1) : (int)blockIdx.x + ti * (int)gridDim.x;
+                if (t >= ntiles) {
+                    tinfo[4 * s + 3] = -1;
+                    mbar_arrive(&full[s]);
+                    break;
+                }
+                tile_coords(args, t, tinfo + 4 * s);
+                tinfo[4 * s + 3] = t;
+                fence_proxy_async_smem();
+                issue_tile_load(&tm_src, bufs + s * BBYTES, &full[s], tinfo[4 * s], tinfo[4 * s + 1],
+                                tinfo[4 * s + 2]);
+            }
+            __threadfence();
+            if (args.dynamic && atomicAdd(args.done, 1) == (int)gridDim.x - 1) {  // every CTA stopped claiming
+                *args.claim = 0;
+                *args.done = 0;
+            }
+        }
+        return;
+    }
+    uint8_t* O = bufs + NBUF * BBYTES + warp * WAREA;
+    uint8_t* F = O + WPIX;
+
+    // Strips (4-row slices of this CTA's tiles, in ring order) are claimed dynamically by warps.
     for (;;) {
         int claim = 0;
         if (lane == 0) claim = atomicAdd(next_strip, 1);
         claim = __shfl_sync(0xFFFFFFFFu, claim, 0);
         const int ti = claim >> 3, sub = claim & 7;
-        if (ti >= my_tiles) break;
-        const int t = blockIdx.x + ti * gridDim.x;
         const int s = ti & (NBUF - 1);
-        mbar_wait(&full[s], (uint32_t)(ti / NBUF) & 1u);
+        mbar_wait_warp(&full[s], (uint32_t)(ti / NBUF) & 1u);
+        const int t = tinfo[4 * s + 3];
+        if (t < 0) break;
         const int x0 = tinfo[4 * s], y0 = tinfo[4 * s + 1], z = tinfo[4 * s + 2];
         uint8_t* B = bufs + s * BBYTES;
 
@@ -289,6 +351,8 @@ __global__ void __launch_bounds__(NT, 3)
             uint8_t* bm = args.bitmap + (size_t)t * 512 + (sub * WR + lr) * 16 + (c0 >> 3);
             bm[0] = (uint8_t)m;
             bm[16] = (uint8_t)(m >> 8);
+            const int nf = __reduce_add_sync(0xFFFFFFFFu, __popc(m));
+            if (lane == 0 && nf) atomicAdd(&fcount[s], nf);
         }
         __syncwarp();
 
@@ -312,19 +376,22 @@ __global__ void __launch_bounds__(NT, 3)
         }
         __syncwarp();
 
-        // ---- release the byte buffer; the last warp refills it with this CTA's tile ti + NBUF ----
+        // ---- release the slot; the tile's last strip publishes its failure record ----
         if (lane == 0) {
             __threadfence_block();
-            if (atomicAdd(&done_cnt[s], 1) == NW - 1) {
+            if (atomicAdd(&done_cnt[s], 1) == TH / WR - 1) {
                 done_cnt[s] = 0;
-                if (ti + NBUF < my_tiles) {
-                    tile_coords(args, blockIdx.x + (ti + NBUF) * gridDim.x, tinfo + 4 * s);
-                    fence_proxy_async_smem();
-                    issue_tile_load(&tm_src, B, &full[s], tinfo[4 * s], tinfo[4 * s + 1], tinfo[4 * s + 2]);
+                const int c = fcount[s];
+                fcount[s] = 0;
+                if (c) {
+                    const unsigned long long old = atomicAdd(args.rec_ctr, (1ull << REC_SHIFT) | (unsigned)c);
+                    args.records[old >> REC_SHIFT] = ((old & REC_MASK) << 24) | (unsigned)t;
                 }
             }
+            mbar_arrive(&empty[s]);
         }
     }
+    TRACE(0, 15);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -369,6 +436,9 @@ struct GArgs {
     const uint8_t* bitmap;
     int rows, cols, row_begin, row_end, n_slices, smax;
     int tiles_x, tiles_y;    // k = 3 tiles
+    unsigned long long* rec_ctr;        // written by amf_k3_kernel; reset here by the last CTA
+    const unsigned long long* records;  // (failure offset << 24) | tile, offsets increasing
+    int* done;
 };
 
 template <int K>
@@ -596,15 +666,20 @@ __device__ __forceinline__ void grow_tile_load(const CUtensorMap* tm, const GGeo
                         x0 - geo.CP + bx * geo.box_w, y0 - geo.R + by * geo.box_h, z);
 }
 
-// Batched sparse growth.  Each CTA owns a contiguous range of k = 3 tiles.  Per batch it counts the
-// failures of the next GSLOTS tiles (their bitmaps, written by amf_k3_kernel), skips empty tiles
-// without loading them, TMA-loads the non-empty ones (tile + R halo, one slot each) and pools all
-// their failures into one shared-memory queue (entry = slot << 12 | pixel), so every level round
-// k = 5..smax runs full warps no matter how sparse the failures are.
+// Sparse growth, balanced by failures.  amf_k3_kernel publishes one record per tile with level-A
+// failures (its failure offset in a global order); CTA j takes the failures [jT/G, (j+1)T/G) and
+// walks the records covering them in batches of up to GSLOTS tile segments / GCAP failures: each
+// segment's tile (+ R halo) is TMA-loaded into its own slot, its failures (bitmap bits whose
+// in-tile rank falls in the segment) are pooled into one shared-memory queue (entry = slot << 12 |
+// pixel), and every level round k = 5..smax runs over the whole pool.
 constexpr int GSLOTS = 8;
-constexpr int GCAP = 8192;  // pooled queue capacity (a single tile has at most 4096 entries)
+constexpr int GCAP = 8192;  // pooled queue capacity
 
 inline size_t grow_smem(const GGeo& g) { return GHDR + (size_t)GSLOTS * g.b_bytes + 2 * GCAP * 2 + 128; }
+
+__device__ __forceinline__ long long rec_off(const unsigned long long* rec, long long i) {
+    return (long long)(__ldcg(rec + i) >> 24);
+}
 
 template <bool FIN>
 __global__ void __launch_bounds__(GNT) amf_grow_kernel(const __grid_constant__ CUtensorMap tm,
@@ -613,128 +688,137 @@ __global__ void __launch_bounds__(GNT) amf_grow_kernel(const __grid_constant__ C
     uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
     const GGeo& geo = args.geo;
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem);            // [GSLOTS]
-    int* sinfo = reinterpret_cast<int*>(smem + 64);                // [GSLOTS][4]: x0, y0, z, tile
-    int* cnt = reinterpret_cast<int*>(smem + 192);                 // [GSLOTS] failures per candidate tile
-    int* ctl = reinterpret_cast<int*>(smem + 224);                 // slots used, consumed, queue n, border mask
-    int* wsum = reinterpret_cast<int*>(smem + 256);                // [8] scan scratch
-    int* cinfo = reinterpret_cast<int*>(smem + 320);               // [GSLOTS][4] candidate coordinates
-    int* qcount = reinterpret_cast<int*>(smem + 448);              // [MAX_LEVELS]
+    int* sinfo = reinterpret_cast<int*>(smem + 64);                // [GSLOTS][8]: x0 y0 z tile lo hi qbase border
+    long long* cur = reinterpret_cast<long long*>(smem + 320);     // [0] record, [1] global failure position
+    int* ctl = reinterpret_cast<int*>(smem + 336);                 // [0] segments, [1] queue n
+    int* qcount = reinterpret_cast<int*>(smem + 384);              // [MAX_LEVELS]
     uint8_t* bufs = smem + GHDR;
     uint16_t* Q0 = reinterpret_cast<uint16_t*>(bufs + (size_t)GSLOTS * geo.b_bytes);
     uint16_t* Q1 = Q0 + GCAP;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int per_slice = args.tiles_x * args.tiles_y;
-    const long long ntiles = (long long)per_slice * args.n_slices;
-    const int chunk = (int)((ntiles + gridDim.x - 1) / gridDim.x);
-    int cursor = blockIdx.x * chunk;
-    const int end = (int)(ntiles < (long long)cursor + chunk ? ntiles : (long long)cursor + chunk);
-    if (tid < GSLOTS) mbar_init(&bar[tid], 1);
-    if (tid == 0) fence_mbar_init();
-    uint32_t phases = 0;  // per-slot mbarrier parity
-    __syncthreads();
-
-    while (cursor < end) {
-        // ---- 1. failures and coordinates of the next GSLOTS tiles (warp w: tile cursor + w) ----
-        if (tid < MAX_LEVELS) qcount[tid] = 0;
-        {
-            const int t = cursor + warp;
-            int c = 0;
-            if (t < end) {
-                const uint4 w4 = reinterpret_cast<const uint4*>(args.bitmap + (size_t)t * 512)[lane];
-                c = __popc(w4.x) + __popc(w4.y) + __popc(w4.z) + __popc(w4.w);
-            }
-#pragma unroll
-            for (int d = 16; d > 0; d >>= 1) c += __shfl_down_sync(0xFFFFFFFFu, c, d);
-            if (lane == 0) {
-                cnt[warp] = t < end ? c : -1;
-                const int z = t / per_slice, rem = t - z * per_slice, by = rem / args.tiles_x;
-                int* ci = cinfo + 4 * warp;
-                ci[0] = (rem - by * args.tiles_x) * TW;
-                ci[1] = args.row_begin + by * TH;
-                ci[2] = z;
-                ci[3] = t;
-            }
+    if (tid == 0) {
+        for (int i = 0; i < GSLOTS; ++i) mbar_init(&bar[i], 1);
+        prefetch_tmap(&tm);
+        fence_mbar_init();
+    }
+    grid_dep_wait();  // records and bitmap come from the k = 3 grid
+    const unsigned long long ctr = __ldcg(args.rec_ctr);
+    const long long R = (long long)(ctr >> REC_SHIFT), T = (long long)(ctr & REC_MASK);
+    const long long gbeg = T * blockIdx.x / gridDim.x, gend = T * (blockIdx.x + 1) / gridDim.x;
+    if (warp == 0 && gbeg < gend) {
+        // 32-ary search: the last record whose offset is <= gbeg
+        long long lo = 0, hi = R;
+        while (hi - lo > 1) {
+            const long long step = (hi - lo + 31) / 32, idx = lo + lane * step;
+            const bool le = idx < hi && rec_off(args.records, idx) <= gbeg;
+            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, le);
+            const int last = 31 - __clz(bal);  // lane 0 always qualifies
+            lo += last * step;
+            hi = min(hi, lo + step);
         }
-        __syncthreads();
-        // ---- 2. choose the batch (non-empty tiles within capacity) and issue their TMA loads ----
-        if (tid == 0) {
-            int ns = 0, total = 0, consumed = 0, borders = 0;
-            for (int w = 0; w < GSLOTS; ++w) {
-                if (cnt[w] < 0) break;
-                if (cnt[w] > 0) {
-                    if (total + cnt[w] > GCAP) break;
-                    const int* ci = cinfo + 4 * w;
-                    int* si = sinfo + 4 * ns;
-                    si[0] = ci[0];
-                    si[1] = ci[1];
-                    si[2] = ci[2];
-                    si[3] = ci[3];
-                    grow_tile_load(&tm, geo, bufs + (size_t)ns * geo.b_bytes, &bar[ns], ci[0], ci[1], ci[2]);
-                    const int sx0 = ci[0] - geo.CP, sy0 = ci[1] - geo.R;
-                    if (sx0 < 0 || sx0 + geo.BS > args.cols || sy0 < 0 || sy0 + geo.BH > args.rows) borders |= 1 << ns;
-                    total += cnt[w];
-                    ++ns;
-                }
-                consumed = w + 1;
+        if (lane == 0) {
+            cur[0] = lo;
+            cur[1] = gbeg;
+        }
+    }
+    uint32_t phases = 0;
+    __syncthreads();
+    TRACE(1, 1);
+
+    while (gbeg < gend) {
+        // ---- 1. warp 0: the next segments (lane l: record cur + l), their TMA loads ----
+        if (tid < MAX_LEVELS) qcount[tid] = 0;
+        if (warp == 0) {
+            const long long rec = cur[0] + lane, pos = cur[1];
+            long long take = 0, off = 0;
+            int tile = 0;
+            if (rec < R && lane < GSLOTS) {
+                const unsigned long long rv = __ldcg(args.records + rec);
+                off = (long long)(rv >> 24);
+                tile = (int)(rv & 0xFFFFFFu);
+                const long long nxt = rec + 1 < R ? rec_off(args.records, rec + 1) : T;
+                const long long s0 = max(off, pos), s1 = min(nxt, gend);
+                take = max(0ll, s1 - s0);
             }
-            ctl[0] = ns;
-            ctl[1] = consumed;
-            ctl[3] = borders;
+            // inclusive prefix of the segment sizes, capped by the queue capacity
+            long long incl = take;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const long long v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+                if (lane >= d) incl += v;
+            }
+            const long long excl = incl - take;
+            const long long mine = max(0ll, min(take, (long long)GCAP - excl));
+            const uint32_t segs = __ballot_sync(0xFFFFFFFFu, mine > 0);
+            const int ns = __popc(segs);  // a prefix of the lanes
+            if (mine > 0) {
+                const long long s0 = max(off, pos);
+                const int z = tile / per_slice, rem = tile - z * per_slice, by = rem / args.tiles_x;
+                int* si = sinfo + 8 * lane;
+                si[0] = (rem - by * args.tiles_x) * TW;
+                si[1] = args.row_begin + by * TH;
+                si[2] = z;
+                si[3] = tile;
+                si[4] = (int)(s0 - off);         // in-tile rank range [lo, hi)
+                si[5] = (int)(s0 - off + mine);
+                si[6] = (int)excl;               // queue base
+                const int sx0 = si[0] - geo.CP, sy0 = si[1] - geo.R;
+                si[7] = sx0 < 0 || sx0 + geo.BS > args.cols || sy0 < 0 || sy0 + geo.BH > args.rows;
+                fence_proxy_async_smem();  // the slot's previous generic reads/writes before the async write
+                grow_tile_load(&tm, geo, bufs + (size_t)lane * geo.b_bytes, &bar[lane], si[0], si[1], z);
+            }
+            if (lane == 0) ctl[0] = ns;
+            if (lane == ns - 1) {
+                ctl[1] = (int)(excl + mine);
+                const long long end_pos = max(off, pos) + mine;
+                cur[1] = end_pos;
+                cur[0] = rec + (end_pos >= (rec + 1 < R ? rec_off(args.records, rec + 1) : T) ? 1 : 0);
+            }
         }
         __syncthreads();
         const int ns = ctl[0];
-        cursor += ctl[1];
-        if (ns == 0) continue;  // (the loop-top writes of qcount/cnt happen after this barrier)
-        // ---- 3. pooled queue: entries slot << 12 | pixel, raster order within each tile ----
-        {
-            constexpr int WPT = GSLOTS * 128 / GNT;  // words per thread (4)
-            uint32_t wb[WPT];
-            int nf = 0;
-#pragma unroll
-            for (int j = 0; j < WPT; ++j) {
-                const int w = tid * WPT + j, sl = w >> 7;
-                wb[j] = sl < ns ? reinterpret_cast<const uint32_t*>(args.bitmap + (size_t)sinfo[4 * sl + 3] * 512)[w & 127]
-                                : 0u;
-                nf += __popc(wb[j]);
-            }
+        if (ns == 0) break;  // (cannot happen: the cursor always lies inside a record)
+        // ---- 2. queue: warp w collects slot w's failures with in-tile rank in [lo, hi) ----
+        if (warp < ns) {
+            const int* si = sinfo + 8 * warp;
+            const uint4 w4 = __ldcg(reinterpret_cast<const uint4*>(args.bitmap + (size_t)si[3] * 512) + lane);
+            const uint32_t wb[4] = {w4.x, w4.y, w4.z, w4.w};
+            const int nf = __popc(w4.x) + __popc(w4.y) + __popc(w4.z) + __popc(w4.w);
             int incl = nf;
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
                 const int v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
                 if (lane >= d) incl += v;
             }
-            if (lane == 31) wsum[warp] = incl;
-            __syncthreads();
-            int pos = incl - nf;
+            int rank = incl - nf;
+            const int lo = si[4], hi = si[5], qb = si[6] - lo;
+            const uint32_t sbase = (uint32_t)warp << 12;
+            if (rank < hi && incl > lo) {
 #pragma unroll
-            for (int w = 0; w < GNT / 32; ++w) pos += w < warp ? wsum[w] : 0;
-            if (tid == 0) {
-                int n = 0;
-#pragma unroll
-                for (int w = 0; w < GNT / 32; ++w) n += wsum[w];
-                ctl[2] = n;
-            }
-#pragma unroll
-            for (int j = 0; j < WPT; ++j) {
-                const int w = tid * WPT + j;
-                const uint32_t base = ((uint32_t)(w >> 7) << 12) | (uint32_t)(((w & 127) >> 2) * TW + 32 * (w & 3));
-                uint32_t bits = wb[j];
-                while (bits) {
-                    const int b = __ffs(bits) - 1;
-                    bits &= bits - 1;
-                    Q0[pos++] = (uint16_t)(base + b);
+                for (int j = 0; j < 4; ++j) {
+                    const int w = lane * 4 + j;  // bitmap word: tile row w >> 2, columns 32 (w & 3) ..
+                    const uint32_t base = sbase | (uint32_t)((w >> 2) * TW + 32 * (w & 3));
+                    uint32_t bits = wb[j];
+                    while (bits) {
+                        const int b = __ffs(bits) - 1;
+                        bits &= bits - 1;
+                        if (rank >= lo && rank < hi) Q0[qb + rank] = (uint16_t)(base + b);
+                        ++rank;
+                    }
                 }
             }
         }
-        // ---- 4. tiles landed; border tiles get edge replication (whole CTA, columns then rows) ----
+        // ---- 3. tiles landed; border tiles get edge replication (whole CTA, columns then rows) ----
         for (int sl = 0; sl < ns; ++sl) mbar_wait(&bar[sl], (phases >> sl) & 1u);
         phases ^= (1u << ns) - 1u;
-        const int borders = ctl[3];
-        if (borders) {
-            for (int m = borders; m; m &= m - 1) {
-                const int sl = __ffs(m) - 1;
+        bool any_border = false;
+        for (int sl = 0; sl < ns; ++sl) any_border |= sinfo[8 * sl + 7] != 0;
+        if (any_border) {
+            for (int sl = 0; sl < ns; ++sl) {
+                if (!sinfo[8 * sl + 7]) continue;
                 uint8_t* B = bufs + (size_t)sl * geo.b_bytes;
-                const int sx0 = sinfo[4 * sl] - geo.CP, sy0 = sinfo[4 * sl + 1] - geo.R;
+                const int sx0 = sinfo[8 * sl] - geo.CP, sy0 = sinfo[8 * sl + 1] - geo.R;
                 const int c_lo = max(0, -sx0), c_hi = min(geo.BS, args.cols - sx0);
                 const int r_lo = max(0, -sy0), r_hi = min(geo.BH, args.rows - sy0);
                 const int nl = c_lo, nfix = c_lo + (geo.BS - c_hi);
@@ -747,10 +831,10 @@ __global__ void __launch_bounds__(GNT) amf_grow_kernel(const __grid_constant__ C
                 }
             }
             __syncthreads();
-            for (int m = borders; m; m &= m - 1) {
-                const int sl = __ffs(m) - 1;
+            for (int sl = 0; sl < ns; ++sl) {
+                if (!sinfo[8 * sl + 7]) continue;
                 uint8_t* B = bufs + (size_t)sl * geo.b_bytes;
-                const int sy0 = sinfo[4 * sl + 1] - geo.R;
+                const int sy0 = sinfo[8 * sl + 1] - geo.R;
                 const int r_lo = max(0, -sy0), r_hi = min(geo.BH, args.rows - sy0);
                 const int nfr = geo.BH - (r_hi - r_lo), wpr = geo.BS / 4;
                 for (int i = tid; i < nfr * wpr; i += GNT) {
@@ -763,10 +847,11 @@ __global__ void __launch_bounds__(GNT) amf_grow_kernel(const __grid_constant__ C
             }
         }
         __syncthreads();
-        // ---- 5. levels, pooled over the batch ----
-        int n = ctl[2];
+        TRACE(1, 4);
+        // ---- 4. levels, pooled over the batch ----
+        int n = ctl[1];
         auto out_ptr = [&](int sl, int pix, bool f) -> uint8_t* {
-            const int* si = sinfo + 4 * sl;
+            const int* si = sinfo + 8 * sl;
             return f ? args.fin + (size_t)si[2] * args.fslice + (size_t)(si[1] - args.row_begin + (pix >> 7)) * args.fpitch +
                            si[0] + (pix & 127)
                      : args.dst + (size_t)si[2] * args.dslice + (size_t)(si[1] - args.row_begin + (pix >> 7)) * args.dpitch +
@@ -857,11 +942,24 @@ __global__ void __launch_bounds__(GNT) amf_grow_kernel(const __grid_constant__ C
                 }
             }
             __syncthreads();
+            TRACE(1, 5 + lvl);
             if (last) break;
             n = qcount[lvl + 1];
             if (n == 0) break;
         }
+        const bool more = cur[1] < gend;
         __syncthreads();  // slots, queues and counters are reused by the next batch
+        TRACE(1, 14);
+        if (!more) break;
+    }
+    TRACE(1, 15);
+    // the last CTA resets the record counter for the next k = 3 launch
+    if (tid == 0) {
+        __threadfence();
+        if (atomicAdd(args.done, 1) == (int)gridDim.x - 1) {
+            *args.rec_ctr = 0;
+            *args.done = 0;
+        }
     }
 }
 
@@ -869,9 +967,18 @@ int g_num_sms = 0;
 
 }  // namespace
 
-size_t amf_bitmap_bytes(const Plane& p) {
+size_t amf_work_bytes(const Plane& p) {
     const size_t tiles = (size_t)((p.cols + TW - 1) / TW) * ((p.row_end - p.row_begin + TH - 1) / TH) * p.n_slices;
-    return tiles * 512;
+    return 64 + (tiles * 8 + 63) / 64 * 64 + tiles * 512;
+}
+
+AmfWork amf_work(uint8_t* base, const Plane& p) {
+    const size_t tiles = (size_t)((p.cols + TW - 1) / TW) * ((p.row_end - p.row_begin + TH - 1) / TH) * p.n_slices;
+    AmfWork w;
+    w.counters = reinterpret_cast<int*>(base);
+    w.records = reinterpret_cast<unsigned long long*>(base + 64);
+    w.bitmap = base + 64 + (tiles * 8 + 63) / 64 * 64;
+    return w;
 }
 
 cudaError_t launch_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, size_t fslice, const AmfWork& work,
@@ -911,17 +1018,21 @@ cudaError_t launch_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, si
     a.tiles_y = (out_rows + TH - 1) / TH;
     a.grow = grow;
     a.bitmap = work.bitmap;
+    a.claim = work.counters + 2;
+    a.done = work.counters + 3;
+    a.rec_ctr = reinterpret_cast<unsigned long long*>(work.counters);
+    a.records = work.records;
     static int per_sm = 0;
     if (!per_sm) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, amf_k3_kernel<false>, NT, SMEM);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, amf_k3_kernel<false>, K3T, SMEM);
         if (per_sm < 1) per_sm = 1;
     }
     const long long ntiles = (long long)a.tiles_x * a.tiles_y * a.n_slices;
     const int grid = (int)std::min<long long>(ntiles, (long long)g_num_sms * per_sm);
-    if (fin) amf_k3_kernel<true><<<grid, NT, SMEM, stream>>>(tm_src, a);
-    else amf_k3_kernel<false><<<grid, NT, SMEM, stream>>>(tm_src, a);
+    a.dynamic = ntiles > 8ll * grid;
+    e = launch_pdl(fin ? amf_k3_kernel<true> : amf_k3_kernel<false>, dim3(grid), dim3(K3T), SMEM, stream, tm_src, a);
     count_launch();
-    if ((e = cudaGetLastError()) != cudaSuccess || !grow) return e;
+    if (e != cudaSuccess || !grow) return e;
 
     // ---- growth: one batched launch for every window size k = 5..smax ----
     const GGeo geo = make_ggeo(smax);
@@ -953,6 +1064,9 @@ cudaError_t launch_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, si
     g.smax = smax;
     g.tiles_x = a.tiles_x;
     g.tiles_y = a.tiles_y;
+    g.rec_ctr = a.rec_ctr;
+    g.records = work.records;
+    g.done = work.counters + 4;
     static size_t occ_key[2] = {0, 0};
     static int occ_val[2] = {1, 1};
     int& gper_sm = occ_val[fin ? 1 : 0];
@@ -963,9 +1077,19 @@ cudaError_t launch_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, si
     }
     // every resident CTA slot busy; each CTA takes a contiguous run of tiles
     const int ggrid = (int)std::min<long long>(ntiles, (long long)g_num_sms * gper_sm);
-    kern<<<ggrid, GNT, gsm, stream>>>(tm_g, g);
+    e = launch_pdl(kern, dim3(ggrid), dim3(GNT), gsm, stream, tm_g, g);
     count_launch();
-    return cudaGetLastError();
+    return e;
 }
 
 }  // namespace hyb
+
+#ifdef HYB_TRACE
+extern "C" int hyb_trace_read(unsigned long long* host) {
+    return (int)cudaMemcpyFromSymbol(host, hyb::g_trace, sizeof(hyb::g_trace));
+}
+extern "C" int hyb_trace_clear() {
+    static unsigned long long zero[2 * 1024 * 16];
+    return (int)cudaMemcpyToSymbol(hyb::g_trace, zero, sizeof(zero));
+}
+#endif

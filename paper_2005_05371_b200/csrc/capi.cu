@@ -168,10 +168,11 @@ cudaError_t copy2d(hyb_ctx* ctx, void* dst, size_t dp, const void* src, size_t s
 // AMF launch with the context's growth workspace.
 cudaError_t run_amf(hyb_ctx* ctx, const hyb::Plane& p, int smax, uint8_t* fin, size_t fpitch, size_t fslice) {
     cudaError_t e;
-    if ((e = ctx->amf_q[0].ensure(hyb::amf_bitmap_bytes(p))) != cudaSuccess) return e;
-    hyb::AmfWork w;
-    w.bitmap = ctx->amf_q[0].ptr;
-    return hyb::launch_amf(p, smax, fin, fpitch, fslice, w, ctx->stream);
+    const size_t need = hyb::amf_work_bytes(p);
+    const bool fresh = need > ctx->amf_q[0].bytes;
+    if ((e = ctx->amf_q[0].ensure(need)) != cudaSuccess) return e;
+    if (fresh && (e = cudaMemsetAsync(ctx->amf_q[0].ptr, 0, 64, ctx->stream)) != cudaSuccess) return e;
+    return hyb::launch_amf(p, smax, fin, fpitch, fslice, hyb::amf_work(ctx->amf_q[0].ptr, p), ctx->stream);
 }
 
 // Core of hyb_hybrid_u8 on device-resident buffers.

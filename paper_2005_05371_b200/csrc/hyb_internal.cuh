@@ -20,12 +20,35 @@ struct Plane {
     int n_slices;
 };
 
-// Device workspace of the AMF growth stage: the per-tile level-A failure bitmap written by the
-// k = 3 kernel (amf_bitmap_bytes(p) bytes, 512 per 128 x 32 tile).
+// Device workspace of the AMF (amf_work_bytes(p) bytes, carved by amf_work): 64 bytes of counters
+// (zero when allocated; every launch leaves them zero), one failure record per k = 3 tile with
+// level-A failures, and the per-tile failure bitmap (512 bytes per 128 x 32 tile).
 struct AmfWork {
+    int* counters;                 // [0..1] record counter (u64), [2] tile claims, [3] / [4] CTAs done
+    unsigned long long* records;   // (failure offset << 24) | tile
     uint8_t* bitmap;
 };
-size_t amf_bitmap_bytes(const Plane& p);
+size_t amf_work_bytes(const Plane& p);
+AmfWork amf_work(uint8_t* base, const Plane& p);
+
+// Launch with programmatic stream serialization: the kernel's prologue may overlap the previous
+// kernel's tail; every kernel launched this way calls griddepcontrol.wait before touching memory
+// the previous grids produce or consume.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                       Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<Args&&>(args)...);
+}
 
 // AMF launch (amf.cu): k = 3 tile kernel + one tile-wise growth kernel (k = 5..smax).  fin may be null.
 cudaError_t launch_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, size_t fslice,

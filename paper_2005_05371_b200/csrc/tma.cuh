@@ -39,9 +39,25 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
     return ok != 0;
 }
 
+// Plain arrival (release semantics at CTA scope).
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Programmatic dependent launch: wait for the preceding grid's memory (no-op without the attribute),
+// and let the next grid start its prologue early.
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // Waits for the phase with the given parity; backs off so waiting warps leave issue slots free.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     while (!mbar_try_wait(bar, parity)) __nanosleep(64);
+}
+
+// Warp-convergent wait: the warp leaves the loop together (every lane has observed the completed
+// phase itself, i.e. has its own acquire), so code after it may rely on a converged warp.
+__device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
+    while (!__all_sync(0xFFFFFFFFu, mbar_try_wait(bar, parity))) __nanosleep(32);
 }
 
 // 3-D tiled TMA load (x = column, y = row, z = slice); out-of-bounds elements read as zero.

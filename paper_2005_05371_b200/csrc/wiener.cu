@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(FNW * 32) wiener_fast_kernel(const __grid_cons
     int it = 0;
     for (int t = gw; t < ntiles; t += nw, ++it) {
         const int slot = it & 1;
-        mbar_wait(&bar[slot], (uint32_t)(it >> 1) & 1u);
+        mbar_wait_warp(&bar[slot], (uint32_t)(it >> 1) & 1u);
         int x0, y0, z;
         coords(t, x0, y0, z);
         uint8_t* T = slots + slot * SLOT;

@@ -6,6 +6,7 @@ the north_star tolerance (<= 1 LSB, >= 99.99 % exact), which is asserted as well
 """
 import numpy as np
 import pytest
+import torch
 
 import oracle
 from paper_2005_05371_b200 import CONFIGS, FilterConfig, capi, denoise
@@ -108,6 +109,25 @@ def test_amf_baseline_configs(ctx, cfg):
     c = CONFIGS[cfg]
     img = capi.make_phantom(c["rows"], c["cols"], c["ellipses"], c["sigma"], c["density"], 0)
     np.testing.assert_array_equal(denoise.adaptive_median_serial(img, c["smax"]), oracle.amf(img, c["smax"]))
+
+
+def test_amf_repeated_calls_keep_workspace_consistent(ctx):
+    # the growth stage's device counters (tile claims, failure records) must come back to zero after
+    # every launch: alternate smax and sizes on one context with device buffers
+    c = CONFIGS[1]
+    img = capi.make_phantom(c["rows"], c["cols"], c["ellipses"], c["sigma"], c["density"], 0)
+    small = np.ascontiguousarray(img[:300, :700])
+    g, gs = torch.from_numpy(img).cuda(), torch.from_numpy(small).cuda()
+    want = {s: oracle.amf(img, s) for s in (3, 7, 11)}
+    want_small = oracle.amf(small, 7)
+    for rep in range(2):
+        for smax in (7, 3, 11):
+            out = denoise.adaptive_median_serial(g, smax)
+            torch.cuda.synchronize()
+            np.testing.assert_array_equal(out.cpu().numpy(), want[smax], err_msg=f"rep {rep} smax {smax}")
+        out = denoise.adaptive_median_serial(gs, 7)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(out.cpu().numpy(), want_small, err_msg=f"rep {rep} small")
 
 
 def test_amf_worst_case_growth(ctx):
