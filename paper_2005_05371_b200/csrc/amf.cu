@@ -105,11 +105,12 @@ struct K3Args {
     int dynamic;             // tiles claimed from `claim` (else blockIdx.x + i * gridDim.x)
     int* claim;              // global tile-claim counter (reset by the last CTA to finish)
     int* done;               // CTAs finished
-    unsigned long long* rec_ctr;  // (records << 40) | failures, advanced once per tile with failures
-    unsigned long long* records;  // [record] = (failure offset << 24) | tile
+    unsigned long long* rec_ctr;  // (records << 40) | weighted failures (+REC_W per tile), once per tile with failures
+    unsigned long long* records;  // [record] = (weighted offset << 24) | tile
 };
 
 constexpr int REC_SHIFT = 40;
+constexpr int REC_W = 128;  // growth balancing weight of one tile load, in failures
 constexpr unsigned long long REC_MASK = (1ull << REC_SHIFT) - 1;
 
 __device__ __forceinline__ void issue_tile_load(const CUtensorMap* tm, uint8_t* Bbuf, uint64_t* bar, int x0, int y0,
@@ -229,29 +230,9 @@ __global__ void __launch_bounds__(K3T, 3)
 
         // ---- border tiles: edge replication (this strip's rows) in place of TMA's zero fill ----
         const int sx0 = x0 - CP, sy0 = y0 - 1;
-        if (sx0 < 0 || sx0 + BS > cols || sy0 < 0 || sy0 + BH > rows) {
-            const int c_lo = max(0, -sx0), c_hi = min(BS, cols - sx0);
-            const int r_lo = max(0, -sy0), r_hi = min(BH, rows - sy0);
-            const int wr0 = sub * WR, wr1 = sub * WR + WR + 2;  // byte-tile rows this strip reads
-            if (c_lo > 0 || c_hi < BS) {
-                for (int rr = max(wr0, r_lo); rr < min(wr1, r_hi); ++rr) {
-                    uint8_t* row = B + rr * BS;
-                    const uint8_t lv = row[c_lo], rv = row[c_hi - 1];
-                    for (int cc = lane; cc < BS; cc += 32) {
-                        if (cc < c_lo) row[cc] = lv;
-                        else if (cc >= c_hi) row[cc] = rv;
-                    }
-                }
-                __syncwarp();
-            }
-            for (int rr = wr0; rr < wr1; ++rr) {
-                const int src_r = rr < r_lo ? r_lo : (rr >= r_hi ? r_hi - 1 : rr);
-                if (src_r == rr) continue;
-                for (int q = lane; q < BS / 4; q += 32)
-                    reinterpret_cast<uint32_t*>(B + rr * BS)[q] = reinterpret_cast<const uint32_t*>(B + src_r * BS)[q];
-            }
-            __syncwarp();
-        }
+        if (sx0 < 0 || sx0 + BS > cols || sy0 < 0 || sy0 + BH > rows)
+            warp_replicate_edges(B, BS, max(0, -sx0), min(BS, cols - sx0), max(0, -sy0), min(BH, rows - sy0),
+                                 sub * WR, sub * WR + WR + 2);
 
         // ---- k = 3: lane = rows (r0, r0+1) x columns c0..c0+7, u16x2 lanes = the two rows ----
         const int lr = 2 * (lane >> 4);  // local row within the strip
@@ -367,9 +348,12 @@ __global__ void __launch_bounds__(K3T, 3)
                     *reinterpret_cast<uint4*>(drow) = *reinterpret_cast<const uint4*>(O + sr * TW + sc);
                     if (FIN) *reinterpret_cast<uint4*>(frow) = *reinterpret_cast<const uint4*>(F + sr * TW + sc);
                 } else {
-                    for (int c = 0; c < 16 && sc + c < col_lim; ++c) {
-                        drow[c] = O[sr * TW + sc + c];
-                        if (FIN) frow[c] = F[sr * TW + sc + c];
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) {
+                        if (sc + c < col_lim) {
+                            drow[c] = O[sr * TW + sc + c];
+                            if (FIN) frow[c] = F[sr * TW + sc + c];
+                        }
                     }
                 }
             }
@@ -384,7 +368,8 @@ __global__ void __launch_bounds__(K3T, 3)
                 const int c = fcount[s];
                 fcount[s] = 0;
                 if (c) {
-                    const unsigned long long old = atomicAdd(args.rec_ctr, (1ull << REC_SHIFT) | (unsigned)c);
+                    const unsigned long long old =
+                        atomicAdd(args.rec_ctr, (1ull << REC_SHIFT) | (unsigned)(c + REC_W));
                     args.records[old >> REC_SHIFT] = ((old & REC_MASK) << 24) | (unsigned)t;
                 }
             }
@@ -727,19 +712,25 @@ __global__ void __launch_bounds__(GNT) amf_grow_kernel(const __grid_constant__ C
     TRACE(1, 1);
 
     while (gbeg < gend) {
-        // ---- 1. warp 0: the next segments (lane l: record cur + l), their TMA loads ----
+        // ---- 1. warp 0: the next segments (lane l: record cur + l), their TMA loads.  Positions are
+        //      weighted: record r spans [off, next) = REC_W units for its tile load, then its failures ----
         if (tid < MAX_LEVELS) qcount[tid] = 0;
         if (warp == 0) {
             const long long rec = cur[0] + lane, pos = cur[1];
-            long long take = 0, off = 0;
+            long long take = 0, off = 0, nxt = 0, flo = 0, whi = 0;
             int tile = 0;
+            bool valid = false;
             if (rec < R && lane < GSLOTS) {
                 const unsigned long long rv = __ldcg(args.records + rec);
                 off = (long long)(rv >> 24);
                 tile = (int)(rv & 0xFFFFFFu);
-                const long long nxt = rec + 1 < R ? rec_off(args.records, rec + 1) : T;
-                const long long s0 = max(off, pos), s1 = min(nxt, gend);
-                take = max(0ll, s1 - s0);
+                nxt = rec + 1 < R ? rec_off(args.records, rec + 1) : T;
+                const long long wlo = max(off, pos);
+                whi = min(nxt, gend);
+                valid = wlo < whi;
+                const long long c = nxt - off - REC_W;  // failures of the tile
+                flo = min(max(wlo - off - REC_W, 0ll), c);
+                take = valid ? min(max(whi - off - REC_W, 0ll), c) - flo : 0;
             }
             // inclusive prefix of the segment sizes, capped by the queue capacity
             long long incl = take;
@@ -749,36 +740,46 @@ __global__ void __launch_bounds__(GNT) amf_grow_kernel(const __grid_constant__ C
                 if (lane >= d) incl += v;
             }
             const long long excl = incl - take;
-            const long long mine = max(0ll, min(take, (long long)GCAP - excl));
+            const bool within = valid && excl < GCAP;
+            const long long mine = within ? min(take, (long long)GCAP - excl) : 0;
             const uint32_t segs = __ballot_sync(0xFFFFFFFFu, mine > 0);
-            const int ns = __popc(segs);  // a prefix of the lanes
+            const uint32_t inside = __ballot_sync(0xFFFFFFFFu, within);  // lanes 0..k (lane 0 always)
+            const int ns = __popc(segs);
             if (mine > 0) {
-                const long long s0 = max(off, pos);
+                const int sl = __popc(segs & ((1u << lane) - 1u));
                 const int z = tile / per_slice, rem = tile - z * per_slice, by = rem / args.tiles_x;
-                int* si = sinfo + 8 * lane;
+                int* si = sinfo + 8 * sl;
                 si[0] = (rem - by * args.tiles_x) * TW;
                 si[1] = args.row_begin + by * TH;
                 si[2] = z;
                 si[3] = tile;
-                si[4] = (int)(s0 - off);         // in-tile rank range [lo, hi)
-                si[5] = (int)(s0 - off + mine);
-                si[6] = (int)excl;               // queue base
+                si[4] = (int)flo;  // in-tile failure rank range [lo, hi)
+                si[5] = (int)(flo + mine);
+                si[6] = (int)excl;  // queue base
                 const int sx0 = si[0] - geo.CP, sy0 = si[1] - geo.R;
                 si[7] = sx0 < 0 || sx0 + geo.BS > args.cols || sy0 < 0 || sy0 + geo.BH > args.rows;
                 fence_proxy_async_smem();  // the slot's previous generic reads/writes before the async write
-                grow_tile_load(&tm, geo, bufs + (size_t)lane * geo.b_bytes, &bar[lane], si[0], si[1], z);
+                grow_tile_load(&tm, geo, bufs + (size_t)sl * geo.b_bytes, &bar[sl], si[0], si[1], z);
             }
-            if (lane == 0) ctl[0] = ns;
-            if (lane == ns - 1) {
-                ctl[1] = (int)(excl + mine);
-                const long long end_pos = max(off, pos) + mine;
+            const int last = 31 - __clz(inside);
+            if (lane == last) {
+                const long long end_pos = mine == take ? whi : off + REC_W + flo + mine;
                 cur[1] = end_pos;
-                cur[0] = rec + (end_pos >= (rec + 1 < R ? rec_off(args.records, rec + 1) : T) ? 1 : 0);
+                cur[0] = rec + (end_pos >= nxt ? 1 : 0);
+                ctl[0] = ns;
+                ctl[1] = (int)(excl + mine);
+                ctl[2] = end_pos < gend;
             }
         }
         __syncthreads();
+        TRACE(1, 2);
         const int ns = ctl[0];
-        if (ns == 0) break;  // (cannot happen: the cursor always lies inside a record)
+        const bool more = ctl[2] != 0;
+        if (ns == 0) {  // only tile-load weight in this stretch of the range
+            __syncthreads();
+            if (!more) break;
+            continue;
+        }
         // ---- 2. queue: warp w collects slot w's failures with in-tile rank in [lo, hi) ----
         if (warp < ns) {
             const int* si = sinfo + 8 * warp;
@@ -810,8 +811,10 @@ __global__ void __launch_bounds__(GNT) amf_grow_kernel(const __grid_constant__ C
             }
         }
         // ---- 3. tiles landed; border tiles get edge replication (whole CTA, columns then rows) ----
+        TRACE(1, 3);
         for (int sl = 0; sl < ns; ++sl) mbar_wait(&bar[sl], (phases >> sl) & 1u);
         phases ^= (1u << ns) - 1u;
+        TRACE(1, 12);
         bool any_border = false;
         for (int sl = 0; sl < ns; ++sl) any_border |= sinfo[8 * sl + 7] != 0;
         if (any_border) {
@@ -947,7 +950,6 @@ __global__ void __launch_bounds__(GNT) amf_grow_kernel(const __grid_constant__ C
             n = qcount[lvl + 1];
             if (n == 0) break;
         }
-        const bool more = cur[1] < gend;
         __syncthreads();  // slots, queues and counters are reused by the next batch
         TRACE(1, 14);
         if (!more) break;

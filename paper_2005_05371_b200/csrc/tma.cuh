@@ -60,6 +60,44 @@ __device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
     while (!__all_sync(0xFFFFFFFFu, mbar_try_wait(bar, parity))) __nanosleep(32);
 }
 
+// Edge replication in a TMA-loaded byte tile (`width` bytes per row, out-of-image bytes zero-filled
+// by TMA): within rows [row0, row1), columns < c_lo take column c_lo and columns >= c_hi take column
+// c_hi - 1, then rows outside [r_lo, r_hi) copy the nearest in-image row.  Warp-cooperative with
+// warp-uniform trip counts (a lane-strided loop with a ragged tail would leave the warp diverged
+// while the caller reads the tile), ending with __syncwarp.
+__device__ __forceinline__ void warp_replicate_edges(uint8_t* T, int width, int c_lo, int c_hi, int r_lo, int r_hi,
+                                                     int row0, int row1) {
+    const int lane = threadIdx.x & 31;
+    const int nl = c_lo, nfix = c_lo + (width - c_hi);
+    const int ra = max(row0, r_lo), rb = min(row1, r_hi);
+    if (nfix > 0 && rb > ra) {
+        const int n = (rb - ra) * nfix;
+        for (int i0 = 0; i0 < n; i0 += 32) {
+            const int i = i0 + lane;
+            if (i < n) {
+                const int rr = ra + i / nfix, j = i - (rr - ra) * nfix;
+                uint8_t* row = T + rr * width;
+                if (j < nl) row[j] = row[c_lo];
+                else row[c_hi + (j - nl)] = row[c_hi - 1];
+            }
+        }
+        __syncwarp();
+    }
+    const int wpr = width / 4;
+    const int above = max(0, min(row1, r_lo) - row0), below = max(0, row1 - max(row0, r_hi));
+    const int n = (above + below) * wpr;
+    for (int i0 = 0; i0 < n; i0 += 32) {
+        const int i = i0 + lane;
+        if (i < n) {
+            const int k = i / wpr, q = i - k * wpr;
+            const int rr = k < above ? row0 + k : max(row0, r_hi) + (k - above);
+            const int src = rr < r_lo ? r_lo : r_hi - 1;
+            reinterpret_cast<uint32_t*>(T + rr * width)[q] = reinterpret_cast<const uint32_t*>(T + src * width)[q];
+        }
+    }
+    __syncwarp();
+}
+
 // 3-D tiled TMA load (x = column, y = row, z = slice); out-of-bounds elements read as zero.
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y,
                                             int z) {

@@ -384,28 +384,9 @@ __global__ void __launch_bounds__(FNW * 32) wiener_fast_kernel(const __grid_cons
 
         // ---- border tiles: replicate edges into the zero-filled halo (warp-private slot) ----
         const int sx0 = x0 - FCP, sy0 = y0 - RW;
-        if (sx0 < 0 || sx0 + FBS > a.cols || sy0 < 0 || sy0 + SROWS > a.rows) {
-            const int c_lo = max(0, -sx0), c_hi = min(FBS, a.cols - sx0);
-            const int r_lo = max(0, -sy0), r_hi = min(SROWS, a.rows - sy0);
-            if (c_lo > 0 || c_hi < FBS) {
-                for (int rr = r_lo; rr < r_hi; ++rr) {
-                    uint8_t* row = T + rr * FBS;
-                    const uint8_t lv = row[c_lo], rv = row[c_hi - 1];
-                    for (int cc = lane; cc < FBS; cc += 32) {
-                        if (cc < c_lo) row[cc] = lv;
-                        else if (cc >= c_hi) row[cc] = rv;
-                    }
-                }
-                __syncwarp();
-            }
-            for (int rr = 0; rr < SROWS; ++rr) {
-                const int src_r = rr < r_lo ? r_lo : (rr >= r_hi ? r_hi - 1 : rr);
-                if (src_r == rr) continue;
-                for (int q = lane; q < FBS / 4; q += 32)
-                    reinterpret_cast<uint32_t*>(T + rr * FBS)[q] = reinterpret_cast<const uint32_t*>(T + src_r * FBS)[q];
-            }
-            __syncwarp();
-        }
+        if (sx0 < 0 || sx0 + FBS > a.cols || sy0 < 0 || sy0 + SROWS > a.rows)
+            warp_replicate_edges(T, FBS, max(0, -sx0), min(FBS, a.cols - sx0), max(0, -sy0),
+                                 min(SROWS, a.rows - sy0), 0, SROWS);
 
         const int c = 4 * lane;
         const int col_lim = a.cols - x0, row_lim = a.row_end - y0;
@@ -547,7 +528,9 @@ __global__ void __launch_bounds__(FNW * 32) wiener_fast_kernel(const __grid_cons
                     if (vec_store) {
                         *reinterpret_cast<uint32_t*>(drow) = out;
                     } else {
-                        for (int i = 0; i < 4 && c + i < col_lim; ++i) drow[i] = (uint8_t)(out >> (8 * i));
+#pragma unroll
+                        for (int i = 0; i < 4; ++i)
+                            if (c + i < col_lim) drow[i] = (uint8_t)(out >> (8 * i));
                     }
                 }
                 drow += a.dpitch;

@@ -1,5 +1,5 @@
 """Full-size AMF parity spot check: GPU hyb_amf_u8 vs the C oracle on one BASELINE config
-(optionally a row crop).  usage: amf_check.py <config> [rows] [repeats]"""
+(optionally a row crop / another smax).  usage: amf_check.py <config> [rows] [repeats] [smax]"""
 import sys
 
 import numpy as np
@@ -13,6 +13,8 @@ cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 c = CONFIGS[cfg]
 rows = int(sys.argv[2]) if len(sys.argv) > 2 else c["rows"]
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+if len(sys.argv) > 4:
+    c = dict(c, smax=int(sys.argv[4]))
 g = capi.make_phantom(c["rows"], c["cols"], c["ellipses"], c["sigma"], c["density"], 0)[:rows].copy()
 want, wfin = oracle.amf(g, c["smax"], finalized_at=True)
 gd = torch.from_numpy(g).cuda()

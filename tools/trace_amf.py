@@ -30,7 +30,7 @@ lib.hyb_trace_read(buf)
 t = np.frombuffer(buf, dtype=np.uint64).reshape(2, 1024, 16).astype(np.int64)
 k3, gr = t[0], t[1]
 k3 = k3[k3[:, 0] > 0]
-gr = gr[gr[:, 0] > 0]
+gr = gr[gr[:, 15] > 0]
 t0 = k3[:, 0].min()
 
 
@@ -42,9 +42,14 @@ def q(x):
 print(f"config {cfg}: {len(k3)} k3 CTAs, {len(gr)} growth CTAs   quantiles 0/10/50/90/100 (us)")
 print("k3 start      ", q(k3[:, 0]))
 print("k3 end        ", q(k3[:, 15]))
-names = {0: "grow start", 1: "counted", 2: "chosen", 4: "tiles ready", 14: "batch end", 15: "grow end"}
-for s in (0, 1, 2, 4, 5, 6, 7, 8, 14, 15):
+names = {1: "grow located", 2: "batch chosen", 3: "queue built", 12: "tiles landed", 4: "tiles ready", 14: "batch end", 15: "grow end"}
+for s in (1, 2, 3, 12, 4, 5, 6, 7, 8, 14, 15):
     col = gr[:, s]
     col = col[col > 0]
     if len(col):
         print(f"{names.get(s, f'level {2 * (s - 5) + 5} done'):14s}", q(col))
+if len(sys.argv) > 2:
+    order = np.argsort(-(t[1][:, 2]))[:6]
+    for b in order:
+        row = t[1][b]
+        print("cta", b, " ".join(f"{s}:{(row[s] - t0) / 1e3:.2f}" for s in (1, 9, 10, 11, 2, 3, 12, 4, 5, 6, 15) if row[s] > 0))
