@@ -187,9 +187,9 @@ int hybrid_device(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int co
         const size_t fp = round_pitch(cols);
         HYB_CHECK(ctx->f.ensure(fp * rows));
         hyb::Plane a{g, pitch, 0, ctx->f.ptr, fp, 0, rows, cols, 0, rows, 1};
+        HYB_CHECK(cudaMemsetAsync(W, 0, sizeof(long long), ctx->stream));  // first: kernels chain by PDL
         HYB_CHECK(run_amf(ctx, a, smax, nullptr, 0, 0));
         if (timed) HYB_CHECK(cudaEventRecord(ctx->ev[1], ctx->stream));
-        HYB_CHECK(cudaMemsetAsync(W, 0, sizeof(long long), ctx->stream));
         hyb::Plane w{ctx->f.ptr, fp, 0, y, ypitch, 0, rows, cols, 0, rows, 1};
         HYB_CHECK(hyb::launch_wiener_stats(w, win, W, ctx->stream));
         HYB_CHECK(hyb::launch_wiener_gain(w, win, reinterpret_cast<const long long*>(W), P, ctx->stream));
@@ -760,8 +760,8 @@ int hyb_hybrid_batch_u8(hyb_ctx* ctx, const uint8_t* g, size_t pitch, size_t sli
     HYB_CHECK(ctx->wsum.ensure(sizeof(long long) * n_slices));
     unsigned long long* W = reinterpret_cast<unsigned long long*>(ctx->wsum.ptr);
     hyb::Plane a{s, sp, ss, ctx->f.ptr, pp, ps, rows, cols, 0, rows, n_slices};
-    HYB_CHECK(run_amf(ctx, a, smax, nullptr, 0, 0));
     HYB_CHECK(cudaMemsetAsync(W, 0, sizeof(long long) * n_slices, ctx->stream));
+    HYB_CHECK(run_amf(ctx, a, smax, nullptr, 0, 0));
     hyb::Plane w{ctx->f.ptr, pp, ps, d, dp, ds, rows, cols, 0, rows, n_slices};
     HYB_CHECK(hyb::launch_wiener_stats(w, win, W, ctx->stream));
     HYB_CHECK(hyb::launch_wiener_gain(w, win, reinterpret_cast<const long long*>(W), (long long)rows * cols,

@@ -78,6 +78,7 @@ __global__ void __launch_bounds__(NT) wiener_kernel(Plane p, int win,
                                                     const long long* __restrict__ wread,
                                                     long long pixel_count) {
     extern __shared__ __align__(16) uint8_t smem[];
+    grid_dep_wait();  // f (and the zeroed noise sums) come from the previous grids
     const WGeo geo = make_wgeo(win);
     uint8_t* Ft = smem;
     size_t off = ((size_t)geo.FH * geo.FS + 15) & ~(size_t)15;
@@ -209,7 +210,9 @@ cudaError_t launch(const Plane& p, int win, unsigned long long* wsum, const long
         configured = smem;
     }
     const dim3 grid((p.cols + TW - 1) / TW, (p.row_end - p.row_begin + TH - 1) / TH, p.n_slices);
-    wiener_kernel<GAIN><<<grid, NT, smem, stream>>>(p, win, wsum, wread, pixel_count);
+    cudaError_t e = launch_pdl(wiener_kernel<GAIN>, dim3(grid), dim3(NT), smem, stream, p, win, wsum, wread,
+                               pixel_count);
+    if (e != cudaSuccess) return e;
     count_launch();
     return cudaGetLastError();
 }
@@ -338,6 +341,7 @@ __global__ void __launch_bounds__(FNW * 32) wiener_fast_kernel(const __grid_cons
         mbar_expect_tx(&bar[slot], FBS * SROWS);
         tma_load_3d(slots + slot * SLOT, &tm, &bar[slot], x0 - FCP, y0 - RW, z);
     };
+    grid_dep_wait();  // f (and the zeroed noise sums) come from the previous grids
     if (lane == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
@@ -595,7 +599,9 @@ cudaError_t launch_fast(const Plane& p, unsigned long long* wsum, const long lon
     const long long ntiles = (long long)a.tiles_x * a.tiles_y * a.n_slices;
     const long long warps = std::min<long long>(ntiles, (long long)g_wsms * per_sm * FNW);
     const int grid = (int)((warps + FNW - 1) / FNW);
-    wiener_fast_kernel<RW, GAIN, FH><<<grid, FNW * 32, smem, stream>>>(tm, a);
+    const cudaError_t le =
+        launch_pdl(wiener_fast_kernel<RW, GAIN, FH>, dim3(grid), dim3(FNW * 32), smem, stream, tm, a);
+    if (le != cudaSuccess) return le;
     count_launch();
     return cudaGetLastError();
 }
