@@ -19,6 +19,7 @@
 
 #include "hyb_internal.cuh"
 #include "tma.cuh"
+#include "w1_core.cuh"
 
 namespace hyb {
 namespace {
@@ -26,7 +27,6 @@ namespace {
 constexpr int TW = 128;
 constexpr int TH = 32;
 constexpr int NT = 256;
-constexpr float kTieEps = 1.0f / 2048.0f;
 
 struct WGeo {
     int RW;    // window radius
@@ -226,10 +226,6 @@ cudaError_t launch(const Plane& p, int win, unsigned long long* wsum, const long
 // and slides them down the tile through an N-deep register ring, so every pixel costs a few
 // integer ops; statistics stay exact int32 per pixel.
 // ------------------------------------------------------------------------------------------
-constexpr int FW = 128;          // tile columns
-constexpr int FH_MAX = 16;       // tile rows (8 for small images: shorter per-warp chains)
-constexpr int FCP = 16;          // column pad (TMA box x offsets must be 16-byte aligned)
-constexpr int FBS = FW + 2 * FCP;  // staged row bytes (160)
 constexpr int FNW = 8;           // warps per CTA
 __host__ __device__ constexpr int kFastSmemSlot(int rw, int fh) { return ((FBS * (fh + 2 * rw)) + 127) / 128 * 128; }
 
@@ -243,77 +239,8 @@ struct FastArgs {
     long long pixel_count;
 };
 
-// 4 bytes starting at byte S of the 12-byte window [w0 w1 w2] (S compile-time, 0..11).
-template <int S>
-__device__ __forceinline__ uint32_t bytes4(uint32_t w0, uint32_t w1, uint32_t w2) {
-    if (S == 0) return w0;
-    if (S == 4) return w1;
-    if (S == 8) return w2;
-    if (S < 4) return __funnelshift_r(w0, w1, 8 * S);
-    if (S < 8) return __funnelshift_r(w1, w2, 8 * (S - 4));
-    return w2 >> (8 * (S - 8));  // only the low 12 - S bytes are meaningful
-}
-
-// Horizontal window sums (f, f^2) of pixel I (0..3) of the lane's 4 columns.
-template <int RW, int I>
-__device__ __forceinline__ void hsums(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t& h1, uint32_t& h2) {
-    constexpr int N = 2 * RW + 1;
-    constexpr int S = 4 + I - RW;  // first window byte in [w0 w1 w2] (w1 = the lane's own word)
-    if (N == 1) {
-        const uint32_t x = (bytes4<S>(w0, w1, w2)) & 0xFFu;
-        h1 = x;
-        h2 = x * x;
-    } else if (N == 3) {
-        const uint32_t x = bytes4<S>(w0, w1, w2) & 0x00FFFFFFu;
-        h1 = __dp4a(x, 0x01010101u, 0u);
-        h2 = __dp4a(x, x, 0u);
-    } else {
-        const uint32_t lo = bytes4<S>(w0, w1, w2);
-        constexpr uint32_t hm = N == 5 ? 0x000000FFu : 0x00FFFFFFu;
-        const uint32_t hi = bytes4<S + 4>(w0, w1, w2) & hm;
-        h1 = __dp4a(hi, 0x01010101u, __dp4a(lo, 0x01010101u, 0u));
-        h2 = __dp4a(hi, hi, __dp4a(lo, lo, 0u));
-    }
-}
-
-// Horizontal window sum of f only (statistics pass); window bytes beyond N get weight 0.
-template <int RW, int I>
-__device__ __forceinline__ uint32_t hsum1(uint32_t w0, uint32_t w1, uint32_t w2) {
-    constexpr int N = 2 * RW + 1;
-    constexpr int S = 4 + I - RW;
-    if (N == 1) return bytes4<S>(w0, w1, w2) & 0xFFu;
-    if (N == 3) return __dp4a(bytes4<S>(w0, w1, w2), 0x00010101u, 0u);
-    constexpr uint32_t hw = N == 5 ? 0x00000001u : 0x00010101u;
-    return __dp4a(bytes4<S + 4>(w0, w1, w2), hw, __dp4a(bytes4<S>(w0, w1, w2), 0x01010101u, 0u));
-}
-
-// Number of (output position p in [lo, hi), offset d in [-RW, RW]) pairs whose clamped coordinate
-// clamp(p + d, 0, n - 1) equals r: how many output windows cover row (or column) r.
-__device__ __forceinline__ int win_count(int r, int lo, int hi, int n, int RW) {
-    int cnt = 0;
-    for (int d = -RW; d <= RW; ++d) {
-        int plo, phi;
-        if (n == 1) {
-            plo = lo;
-            phi = hi - 1;
-        } else if (r == 0) {
-            plo = lo;
-            phi = -d;
-        } else if (r == n - 1) {
-            plo = n - 1 - d;
-            phi = hi - 1;
-        } else {
-            plo = phi = r - d;
-        }
-        plo = max(plo, lo);
-        phi = min(phi, hi - 1);
-        cnt += max(0, phi - plo + 1);
-    }
-    return cnt;
-}
-
 template <int RW, bool GAIN, int FH>
-__global__ void __launch_bounds__(FNW * 32) wiener_fast_kernel(const __grid_constant__ CUtensorMap tm,
+__global__ void __launch_bounds__(FNW * 32, GAIN ? 4 : 3) wiener_fast_kernel(const __grid_constant__ CUtensorMap tm,
                                                                const __grid_constant__ FastArgs a) {
     constexpr int N = 2 * RW + 1;
     constexpr int NN = N * N;
@@ -351,14 +278,7 @@ __global__ void __launch_bounds__(FNW * 32) wiener_fast_kernel(const __grid_cons
     }
     __syncwarp();
 
-    constexpr int n = N * N;
-    long long W = 0;
-    int wq32 = 0;  // floor(W / P), clamped: V <= wq32 <=> V P <= W
-    float kn = 0.f, kq = 0.f;
-    const float inv_n = 1.0f / (float)NN;
-    if (GAIN) {
-        W = a.wread[0];  // per-slice values are re-read below when n_slices > 1
-    }
+    W1Gain kg = {};
     unsigned long long vsum = 0;
     int zprev = -1;
     int it = 0;
@@ -368,12 +288,8 @@ __global__ void __launch_bounds__(FNW * 32) wiener_fast_kernel(const __grid_cons
         int x0, y0, z;
         coords(t, x0, y0, z);
         uint8_t* T = slots + slot * SLOT;
-        if (GAIN && z != zprev) {
-            W = a.wread[z];
-            const long long wq = W / a.pixel_count;
-            wq32 = wq > 0x7FFFFFFFll ? 0x7FFFFFFF : (int)wq;
-            kn = (float)((double)W / ((double)a.pixel_count * (double)n));
-            kq = (float)((double)W / (double)a.pixel_count);
+        if (GAIN && z != zprev) {  // per-slice noise sums
+            kg = w1_gain_consts(a.wread[z], a.pixel_count);
             zprev = z;
         }
         if (!GAIN && z != zprev) {
@@ -392,154 +308,12 @@ __global__ void __launch_bounds__(FNW * 32) wiener_fast_kernel(const __grid_cons
             warp_replicate_edges(T, FBS, max(0, -sx0), min(FBS, a.cols - sx0), max(0, -sy0),
                                  min(SROWS, a.rows - sy0), 0, SROWS);
 
-        const int c = 4 * lane;
         const int col_lim = a.cols - x0, row_lim = a.row_end - y0;
-        const uint32_t* base = reinterpret_cast<const uint32_t*>(T + FCP + c - 4);
         if (!GAIN) {
-            // ---- statistics: W = n * sum_p S2(p) - sum_p S1(p)^2 with sum_p S2(p) = sum_q f(q)^2 WR(q_r) WC(q_c)
-            // (WR / WC = how many output windows cover a row / column, clamping included), so only S1
-            // needs a per-pixel box sum.  Each image pixel's f^2 is owned by exactly one tile: its output
-            // rows, plus the RW halo rows outside the output range for the first / last tile.
-            uint32_t wc[4];
-            bool wc_full = true;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int cc = x0 + c + i;
-                wc[i] = cc < a.cols ? (uint32_t)win_count(cc, 0, a.cols, a.cols, RW) : 0u;
-                wc_full &= wc[i] == (uint32_t)N;
-            }
-            const int own_lo = (y0 == a.row_begin) ? max(0, a.row_begin - RW) : y0;
-            const int own_hi = (y0 + FH >= a.row_end) ? min(a.rows, a.row_end + RW) : y0 + FH;
-            uint32_t r1[N][4], s1[4] = {0, 0, 0, 0};
-            long long tile_sq = 0, tile_s1sq = 0;
-            auto take_row = [&](int rr, uint32_t (&h)[4]) {
-                const uint32_t* rp = base + rr * (FBS / 4);
-                const uint32_t w0 = rp[0], w1 = rp[1], w2 = rp[2];
-                h[0] = hsum1<RW, 0>(w0, w1, w2);
-                h[1] = hsum1<RW, 1>(w0, w1, w2);
-                h[2] = hsum1<RW, 2>(w0, w1, w2);
-                h[3] = hsum1<RW, 3>(w0, w1, w2);
-                const int r = y0 - RW + rr;  // image row of this tile row
-                if (r >= own_lo && r < own_hi) {
-                    const bool interior = r - RW >= max(a.row_begin, 0) && r + RW < min(a.row_end, a.rows);
-                    const uint32_t wr = interior ? (uint32_t)N : (uint32_t)win_count(r, a.row_begin, a.row_end, a.rows, RW);
-                    uint32_t q;
-                    if (wc_full) {
-                        q = (uint32_t)N * __dp4a(w1, w1, 0u);
-                    } else {
-                        q = 0;
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) {
-                            const uint32_t f = (w1 >> (8 * i)) & 0xFFu;
-                            q += wc[i] * f * f;
-                        }
-                    }
-                    tile_sq += (long long)wr * q;
-                }
-            };
-#pragma unroll
-            for (int rr = 0; rr < N - 1; ++rr) {
-                take_row(rr, r1[rr]);
-#pragma unroll
-                for (int i = 0; i < 4; ++i) s1[i] += r1[rr][i];
-            }
-#pragma unroll 1
-            for (int yg = 0; yg < FH; yg += N) {
-#pragma unroll
-                for (int u = 0; u < N; ++u) {
-                    const int y = yg + u;
-                    if (y >= FH) break;
-                    uint32_t h[4];
-                    take_row(y + N - 1, h);
-                    uint32_t sq4 = 0;
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        s1[i] += h[i];
-                        r1[(u + N - 1) % N][i] = h[i];
-                        if (c + i < col_lim) sq4 += s1[i] * s1[i];  // <= 4 * 12495^2 < 2^32
-                    }
-                    if (y < row_lim) tile_s1sq += sq4;
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) s1[i] -= r1[u][i];
-                }
-            }
-            // the last rows of the tile box (below the window of the last output row) hold halo f^2
-#pragma unroll
-            for (int rr = FH + N - 1; rr < SROWS; ++rr) {
-                uint32_t h[4];
-                take_row(rr, h);
-            }
-            vsum += (unsigned long long)((long long)NN * tile_sq - tile_s1sq);  // two's complement sum
+            vsum += (unsigned long long)w1_tile_stats<RW, FH>(T, x0, y0, a.rows, a.cols, a.row_begin, a.row_end);
         } else {
-            // ---- gain: per-pixel S1, S2 by horizontal dp4a sums slid down the tile; the leaving row is
-            // re-read from the tile (small code, high occupancy) rather than kept in a register ring ----
-            uint32_t s1[4] = {0, 0, 0, 0}, s2[4] = {0, 0, 0, 0};
-            auto add_row = [&](int rr, bool sub) {
-                const uint32_t* rp = base + rr * (FBS / 4);
-                const uint32_t w0 = rp[0], w1 = rp[1], w2 = rp[2];
-                uint32_t h1[4], h2[4];
-                hsums<RW, 0>(w0, w1, w2, h1[0], h2[0]);
-                hsums<RW, 1>(w0, w1, w2, h1[1], h2[1]);
-                hsums<RW, 2>(w0, w1, w2, h1[2], h2[2]);
-                hsums<RW, 3>(w0, w1, w2, h1[3], h2[3]);
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    s1[i] = sub ? s1[i] - h1[i] : s1[i] + h1[i];
-                    s2[i] = sub ? s2[i] - h2[i] : s2[i] + h2[i];
-                }
-            };
-#pragma unroll
-            for (int rr = 0; rr < N - 1; ++rr) add_row(rr, false);
-            uint8_t* drow = a.dst + (size_t)z * a.dslice + (size_t)(y0 - a.row_begin) * a.dpitch + x0 + c;
-            const bool vec_store = c + 4 <= col_lim && ((reinterpret_cast<uintptr_t>(drow) & 3) == 0) && (a.dpitch & 3) == 0;
-#pragma unroll 1
-            for (int y = 0; y < FH; ++y) {
-                add_row(y + N - 1, false);  // window of output row y = tile rows y .. y + N - 1
-                const uint32_t own = *(base + (y + RW) * (FBS / 4) + 1);  // f of the 4 output pixels
-                uint32_t out = 0;
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const uint32_t f = (own >> (8 * i)) & 0xFFu;
-                    const uint32_t S1 = s1[i];
-                    const int V = (int)(NN * s2[i] - S1 * S1);
-                    const int d = (int)(NN * f) - (int)S1;  // n (f - mu), |d| <= 49 * 255 < 2^14
-                    // y + 1/2 = (S1 + g d) / n + 1/2, g = max(0, 1 - (W/P) / V): one FFMA chain, exponent-trick
-                    // conversions; within 2^-11 of a rounding boundary the exact integer test decides.
-                    const float s1f = __int_as_float(0x4B000000 | S1) - 8388608.0f;
-                    const float df = __int_as_float(0x4B000000 + d + 16384) - 8404992.0f;
-                    float rv;
-                    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rv) : "f"((float)V));
-                    const float gg = fmaxf(0.0f, 1.0f - kq * rv);
-                    const float hh = fmaf(fmaf(gg, df, s1f), inv_n, 0.5f);
-                    const int hb = __float_as_int(__fadd_rd(hh, 12582912.0f));  // floor in the mantissa
-                    const float fr = hh - (__int_as_float(hb) - 12582912.0f);
-                    int q = hb - 0x4B400000;
-                    if (fabsf(fr - 0.5f) > 0.5f - kTieEps) {
-                        if (V <= wq32) {
-                            q = (int)((2u * S1 + NN) / (2u * NN));  // v <= nu: y = mu, half up
-                        } else {
-                            // y >= m - 1/2  <=>  (2 (f - m) + 1) n V P >= 2 D W
-                            const int m = fr < 0.5f ? q : q + 1;
-                            const __int128 Q = (__int128)((long long)NN * V) * a.pixel_count;
-                            const __int128 lhs = (__int128)(2 * ((int)f - m) + 1) * Q;
-                            const __int128 rhs = (__int128)(2 * (long long)d) * W;
-                            q = lhs >= rhs ? m : m - 1;
-                        }
-                    }
-                    out |= (uint32_t)q << (8 * i);  // y in [min(mu, f), max(mu, f)] -> 0..255
-                }
-                if (y < row_lim) {
-                    if (vec_store) {
-                        *reinterpret_cast<uint32_t*>(drow) = out;
-                    } else {
-#pragma unroll
-                        for (int i = 0; i < 4; ++i)
-                            if (c + i < col_lim) drow[i] = (uint8_t)(out >> (8 * i));
-                    }
-                }
-                drow += a.dpitch;
-                add_row(y, true);  // drop tile row y
-            }
+            w1_tile_gain<RW, FH>(T, x0, col_lim, row_lim, kg,
+                                 a.dst + (size_t)z * a.dslice + (size_t)(y0 - a.row_begin) * a.dpitch + x0, a.dpitch);
         }
         __syncwarp();
         // refill this slot with the warp's tile after next
