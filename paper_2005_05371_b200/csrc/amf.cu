@@ -29,6 +29,7 @@
 #include "amf_core.cuh"
 #include "hyb_internal.cuh"
 #include "tma.cuh"
+#include "trace.cuh"
 
 namespace hyb {
 namespace {
@@ -62,9 +63,6 @@ struct K3Args {
     unsigned long long* records;  // [record] = (weighted offset << 24) | tile
 };
 
-constexpr int REC_SHIFT = 40;
-constexpr int REC_W = 128;  // growth balancing weight of one tile load, in failures
-constexpr unsigned long long REC_MASK = (1ull << REC_SHIFT) - 1;
 
 __device__ __forceinline__ void issue_tile_load(const CUtensorMap* tm, uint8_t* Bbuf, uint64_t* bar, int x0, int y0,
                                                 int z) {
@@ -81,28 +79,6 @@ __device__ __forceinline__ void tile_coords(const K3Args& a, int t, int* info) {
     info[2] = z;
 }
 
-#ifdef HYB_TRACE
-// Debug builds only (make trace): per-CTA phase timestamps, read back with hyb_trace_read.
-__device__ unsigned long long g_trace[2 * 1024 * 16];
-__device__ __forceinline__ void trace_mark(int kid, int slot) {
-    if (threadIdx.x == 0 && blockIdx.x < 1024) {
-        unsigned long long t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        g_trace[(kid * 1024 + blockIdx.x) * 16 + slot] = t;
-    }
-}
-#ifndef HYB_TRACE_MASK
-#define HYB_TRACE_MASK 3
-#endif
-#define TRACE(kid, slot)                                  \
-    do {                                                  \
-        if ((HYB_TRACE_MASK >> (kid)) & 1) trace_mark(kid, slot); \
-    } while (0)
-#else
-#define TRACE(kid, slot) \
-    do {                 \
-    } while (0)
-#endif
 
 template <bool FIN>
 __global__ void __launch_bounds__(K3T, 3)
@@ -221,7 +197,6 @@ __global__ void __launch_bounds__(K3T, 3)
 constexpr int GNT = 256;         // threads per growth CTA
 
 constexpr int GHDR = 1024;       // mbarriers, tile coordinates, level counters, scan scratch
-constexpr int MAX_LEVELS = 128;
 
 inline size_t grow_smem(const GGeo& g);
 
@@ -239,14 +214,6 @@ struct GArgs {
     int* done;
 };
 
-__device__ __forceinline__ void grow_tile_load(const CUtensorMap* tm, const GGeo& geo, uint8_t* Bbuf, uint64_t* bar,
-                                               int x0, int y0, int z) {
-    mbar_expect_tx(bar, (uint32_t)(geo.box_w * geo.nbx * geo.box_h * geo.nby));
-    for (int by = 0; by < geo.nby; ++by)
-        for (int bx = 0; bx < geo.nbx; ++bx)
-            tma_load_3d(Bbuf + (size_t)by * geo.box_h * geo.BS + (size_t)bx * geo.box_w, tm, bar,
-                        x0 - geo.CP + bx * geo.box_w, y0 - geo.R + by * geo.box_h, z);
-}
 
 // Sparse growth, balanced by failures.  amf_k3_kernel publishes one record per tile with level-A
 // failures (its failure offset in a global order); CTA j takes the failures [jT/G, (j+1)T/G) and
@@ -254,14 +221,9 @@ __device__ __forceinline__ void grow_tile_load(const CUtensorMap* tm, const GGeo
 // segment's tile (+ R halo) is TMA-loaded into its own slot, its failures (bitmap bits whose
 // in-tile rank falls in the segment) are pooled into one shared-memory queue (entry = slot << 12 |
 // pixel), and every level round k = 5..smax runs over the whole pool.
-constexpr int GSLOTS = 8;
-constexpr int GCAP = 8192;  // pooled queue capacity
 
 inline size_t grow_smem(const GGeo& g) { return GHDR + (size_t)GSLOTS * g.b_bytes + 2 * GCAP * 2 + 128; }
 
-__device__ __forceinline__ long long rec_off(const unsigned long long* rec, long long i) {
-    return (long long)(__ldcg(rec + i) >> 24);
-}
 
 template <bool FIN>
 __global__ void __launch_bounds__(GNT, 2) amf_grow_kernel(const __grid_constant__ CUtensorMap tm,
@@ -288,269 +250,17 @@ __global__ void __launch_bounds__(GNT, 2) amf_grow_kernel(const __grid_constant_
     const unsigned long long ctr = __ldcg(args.rec_ctr);
     const long long R = (long long)(ctr >> REC_SHIFT), T = (long long)(ctr & REC_MASK);
     const long long gbeg = T * blockIdx.x / gridDim.x, gend = T * (blockIdx.x + 1) / gridDim.x;
-    if (warp == 0 && gbeg < gend) {
-        // 32-ary search: the last record whose offset is <= gbeg
-        long long lo = 0, hi = R;
-        while (hi - lo > 1) {
-            const long long step = (hi - lo + 31) / 32, idx = lo + lane * step;
-            const bool le = idx < hi && rec_off(args.records, idx) <= gbeg;
-            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, le);
-            const int last = 31 - __clz(bal);  // lane 0 always qualifies
-            lo += last * step;
-            hi = min(hi, lo + step);
-        }
-        if (lane == 0) {
-            cur[0] = lo;
-            cur[1] = gbeg;
-        }
-    }
     uint32_t phases = 0;
-    __syncthreads();
-    TRACE(1, 1);
-
-    while (gbeg < gend) {
-        // ---- 1. warp 0: the next segments (lane l: record cur + l), their TMA loads.  Positions are
-        //      weighted: record r spans [off, next) = REC_W units for its tile load, then its failures ----
-        if (tid < MAX_LEVELS) qcount[tid] = 0;
-        if (warp == 0) {
-            const long long rec = cur[0] + lane, pos = cur[1];
-            long long take = 0, off = 0, nxt = 0, flo = 0, whi = 0;
-            int tile = 0;
-            bool valid = false;
-            if (rec < R && lane < GSLOTS) {
-                const unsigned long long rv = __ldcg(args.records + rec);
-                off = (long long)(rv >> 24);
-                tile = (int)(rv & 0xFFFFFFu);
-                nxt = rec + 1 < R ? rec_off(args.records, rec + 1) : T;
-                const long long wlo = max(off, pos);
-                whi = min(nxt, gend);
-                valid = wlo < whi;
-                const long long c = nxt - off - REC_W;  // failures of the tile
-                flo = min(max(wlo - off - REC_W, 0ll), c);
-                take = valid ? min(max(whi - off - REC_W, 0ll), c) - flo : 0;
-            }
-            // inclusive prefix of the segment sizes, capped by the queue capacity
-            long long incl = take;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const long long v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
-                if (lane >= d) incl += v;
-            }
-            const long long excl = incl - take;
-            const bool within = valid && excl < GCAP;
-            const long long mine = within ? min(take, (long long)GCAP - excl) : 0;
-            const uint32_t segs = __ballot_sync(0xFFFFFFFFu, mine > 0);
-            const uint32_t inside = __ballot_sync(0xFFFFFFFFu, within);  // lanes 0..k (lane 0 always)
-            const int ns = __popc(segs);
-            if (mine > 0) {
-                const int sl = __popc(segs & ((1u << lane) - 1u));
-                const int z = tile / per_slice, rem = tile - z * per_slice, by = rem / args.tiles_x;
-                int* si = sinfo + 8 * sl;
-                si[0] = (rem - by * args.tiles_x) * TW;
-                si[1] = args.row_begin + by * TH;
-                si[2] = z;
-                si[3] = tile;
-                si[4] = (int)flo;  // in-tile failure rank range [lo, hi)
-                si[5] = (int)(flo + mine);
-                si[6] = (int)excl;  // queue base
-                const int sx0 = si[0] - geo.CP, sy0 = si[1] - geo.R;
-                si[7] = sx0 < 0 || sx0 + geo.BS > args.cols || sy0 < 0 || sy0 + geo.BH > args.rows;
-                fence_proxy_async_smem();  // the slot's previous generic reads/writes before the async write
-                grow_tile_load(&tm, geo, bufs + (size_t)sl * geo.b_bytes, &bar[sl], si[0], si[1], z);
-            }
-            const int last = 31 - __clz(inside);
-            if (lane == last) {
-                const long long end_pos = mine == take ? whi : off + REC_W + flo + mine;
-                cur[1] = end_pos;
-                cur[0] = rec + (end_pos >= nxt ? 1 : 0);
-                ctl[0] = ns;
-                ctl[1] = (int)(excl + mine);
-                ctl[2] = end_pos < gend;
-            }
-        }
-        __syncthreads();
-        TRACE(1, 2);
-        const int ns = ctl[0];
-        const bool more = ctl[2] != 0;
-        if (ns == 0) {  // only tile-load weight in this stretch of the range
-            __syncthreads();
-            if (!more) break;
-            continue;
-        }
-        // ---- 2. queue: warp w collects slot w's failures with in-tile rank in [lo, hi) ----
-        if (warp < ns) {
-            const int* si = sinfo + 8 * warp;
-            const uint4 w4 = __ldcg(reinterpret_cast<const uint4*>(args.bitmap + (size_t)si[3] * 512) + lane);
-            const uint32_t wb[4] = {w4.x, w4.y, w4.z, w4.w};
-            const int nf = __popc(w4.x) + __popc(w4.y) + __popc(w4.z) + __popc(w4.w);
-            int incl = nf;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const int v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
-                if (lane >= d) incl += v;
-            }
-            int rank = incl - nf;
-            const int lo = si[4], hi = si[5], qb = si[6] - lo;
-            const uint32_t sbase = (uint32_t)warp << 12;
-            if (rank < hi && incl > lo) {
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int w = lane * 4 + j;  // bitmap word: tile row w >> 2, columns 32 (w & 3) ..
-                    const uint32_t base = sbase | (uint32_t)((w >> 2) * TW + 32 * (w & 3));
-                    uint32_t bits = wb[j];
-                    while (bits) {
-                        const int b = __ffs(bits) - 1;
-                        bits &= bits - 1;
-                        if (rank >= lo && rank < hi) Q0[qb + rank] = (uint16_t)(base + b);
-                        ++rank;
-                    }
-                }
-            }
-        }
-        // ---- 3. tiles landed; border tiles get edge replication (whole CTA, columns then rows) ----
-        TRACE(1, 3);
-        for (int sl = 0; sl < ns; ++sl) mbar_wait(&bar[sl], (phases >> sl) & 1u);
-        phases ^= (1u << ns) - 1u;
-        TRACE(1, 12);
-        bool any_border = false;
-        for (int sl = 0; sl < ns; ++sl) any_border |= sinfo[8 * sl + 7] != 0;
-        if (any_border) {
-            for (int sl = 0; sl < ns; ++sl) {
-                if (!sinfo[8 * sl + 7]) continue;
-                uint8_t* B = bufs + (size_t)sl * geo.b_bytes;
-                const int sx0 = sinfo[8 * sl] - geo.CP, sy0 = sinfo[8 * sl + 1] - geo.R;
-                const int c_lo = max(0, -sx0), c_hi = min(geo.BS, args.cols - sx0);
-                const int r_lo = max(0, -sy0), r_hi = min(geo.BH, args.rows - sy0);
-                const int nl = c_lo, nfix = c_lo + (geo.BS - c_hi);
-                if (nfix == 0) continue;
-                for (int i = tid; i < (r_hi - r_lo) * nfix; i += GNT) {
-                    const int rr = r_lo + i / nfix, j = i - (rr - r_lo) * nfix;
-                    uint8_t* row = B + (size_t)rr * geo.BS;
-                    if (j < nl) row[j] = row[c_lo];
-                    else row[c_hi + (j - nl)] = row[c_hi - 1];
-                }
-            }
-            __syncthreads();
-            for (int sl = 0; sl < ns; ++sl) {
-                if (!sinfo[8 * sl + 7]) continue;
-                uint8_t* B = bufs + (size_t)sl * geo.b_bytes;
-                const int sy0 = sinfo[8 * sl + 1] - geo.R;
-                const int r_lo = max(0, -sy0), r_hi = min(geo.BH, args.rows - sy0);
-                const int nfr = geo.BH - (r_hi - r_lo), wpr = geo.BS / 4;
-                for (int i = tid; i < nfr * wpr; i += GNT) {
-                    const int k = i / wpr, q = i - k * wpr;
-                    const int rr = k < r_lo ? k : r_hi + (k - r_lo);
-                    const int src_r = rr < r_lo ? r_lo : r_hi - 1;
-                    reinterpret_cast<uint32_t*>(B + (size_t)rr * geo.BS)[q] =
-                        reinterpret_cast<const uint32_t*>(B + (size_t)src_r * geo.BS)[q];
-                }
-            }
-        }
-        __syncthreads();
-        TRACE(1, 4);
-        // ---- 4. levels, pooled over the batch ----
-        int n = ctl[1];
-        auto out_ptr = [&](int sl, int pix, bool f) -> uint8_t* {
-            const int* si = sinfo + 8 * sl;
-            return f ? args.fin + (size_t)si[2] * args.fslice + (size_t)(si[1] - args.row_begin + (pix >> 7)) * args.fpitch +
-                           si[0] + (pix & 127)
-                     : args.dst + (size_t)si[2] * args.dslice + (size_t)(si[1] - args.row_begin + (pix >> 7)) * args.dpitch +
-                           si[0] + (pix & 127);
-        };
-        int lvl = 0;
-        for (int k = 5; k <= args.smax; k += 2, ++lvl) {
-            const uint16_t* qin = (lvl & 1) ? Q1 : Q0;
-            uint16_t* qout = (lvl & 1) ? Q0 : Q1;
-            const bool last = k + 2 > args.smax;
-            if (k <= 7) {
-                const int npairs = (n + 1) >> 1;
-                for (int base = warp * 32; base < npairs; base += GNT) {
-                    const int i = base + lane;
-                    uint32_t keep = 0;
-                    int ea = 0, eb = 0;
-                    if (i < npairs) {
-                        ea = qin[2 * i];
-                        const bool hasb = 2 * i + 1 < n;
-                        eb = hasb ? qin[2 * i + 1] : ea;
-                        const int sa = ea >> 12, pa = ea & 4095, sb = eb >> 12, pb = eb & 4095;
-                        uint32_t done, outw;
-                        const uint8_t* BA = bufs + (size_t)sa * geo.b_bytes;
-                        const uint8_t* BB = bufs + (size_t)sb * geo.b_bytes;
-                        if (k == 5) level_pair2<5>(BA, BB, geo, pa, pb, done, outw);
-                        else level_pair2<7>(BA, BB, geo, pa, pb, done, outw);
-                        if (done & 1u) {
-                            *out_ptr(sa, pa, false) = (uint8_t)outw;
-                            if (FIN) *out_ptr(sa, pa, true) = (uint8_t)k;
-                        } else {
-                            keep |= 1u;
-                        }
-                        if (hasb) {
-                            if (done & 2u) {
-                                *out_ptr(sb, pb, false) = (uint8_t)(outw >> 8);
-                                if (FIN) *out_ptr(sb, pb, true) = (uint8_t)k;
-                            } else {
-                                keep |= 2u;
-                            }
-                        }
-                    }
-                    if (!last) {
-                        const uint32_t balA = __ballot_sync(0xFFFFFFFFu, keep & 1u);
-                        const uint32_t balB = __ballot_sync(0xFFFFFFFFu, keep & 2u);
-                        const int c = __popc(balA) + __popc(balB);
-                        if (c) {
-                            int qb = 0;
-                            if (lane == 0) qb = atomicAdd(&qcount[lvl + 1], c);
-                            qb = __shfl_sync(0xFFFFFFFFu, qb, 0);
-                            const uint32_t below = (1u << lane) - 1u;
-                            if (keep & 1u) qout[qb + __popc(balA & below)] = (uint16_t)ea;
-                            if (keep & 2u) qout[qb + __popc(balA) + __popc(balB & below)] = (uint16_t)eb;
-                        }
-                    }
-                }
-            } else {
-                for (int base = warp * 32; base < n; base += GNT) {
-                    const int i = base + lane;
-                    bool keep = false;
-                    int e = 0;
-                    if (i < n) {
-                        e = qin[i];
-                        const int sl = e >> 12, pix = e & 4095, ty = pix >> 7, tx = pix & 127;
-                        const uint8_t* B = bufs + (size_t)sl * geo.b_bytes;
-                        uint8_t o = 0;
-                        bool done;
-                        switch (k) {
-                            case 9: done = level_radix<9>(B, geo, ty, tx, &o); break;
-                            case 11: done = level_radix<11>(B, geo, ty, tx, &o); break;
-                            default: done = level_generic(B, geo, ty, tx, k, &o); break;
-                        }
-                        if (done) {
-                            *out_ptr(sl, pix, false) = o;
-                            if (FIN) *out_ptr(sl, pix, true) = (uint8_t)k;
-                        } else {
-                            keep = true;
-                        }
-                    }
-                    if (!last) {
-                        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, keep);
-                        if (bal) {
-                            int qb = 0;
-                            if (lane == 0) qb = atomicAdd(&qcount[lvl + 1], __popc(bal));
-                            qb = __shfl_sync(0xFFFFFFFFu, qb, 0);
-                            if (keep) qout[qb + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)e;
-                        }
-                    }
-                }
-            }
-            __syncthreads();
-            TRACE(1, 5 + lvl);
-            if (last) break;
-            n = qcount[lvl + 1];
-            if (n == 0) break;
-        }
-        __syncthreads();  // slots, queues and counters are reused by the next batch
-        TRACE(1, 14);
-        if (!more) break;
-    }
+    const GrowSmem sm{bar, sinfo, cur, ctl, qcount, bufs, Q0, Q1};
+    grow_range<FIN, GNT>(&tm, geo, sm, args.bitmap, args.records, R, T, gbeg, gend, per_slice, args.tiles_x,
+                         args.row_begin, args.rows, args.cols, args.smax, phases,
+                         [&](const int* si, int pix, uint8_t v, int k) {
+                             const size_t row = (size_t)(si[1] - args.row_begin + (pix >> 7));
+                             args.dst[(size_t)si[2] * args.dslice + row * args.dpitch + si[0] + (pix & 127)] = v;
+                             if (FIN)
+                                 args.fin[(size_t)si[2] * args.fslice + row * args.fpitch + si[0] + (pix & 127)] =
+                                     (uint8_t)k;
+                         });
     TRACE(1, 15);
     // the last CTA resets the record counter for the next k = 3 launch
     if (tid == 0) {

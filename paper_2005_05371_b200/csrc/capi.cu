@@ -58,6 +58,8 @@ struct hyb_ctx {
     cudaStream_t stream = nullptr;
     std::string err;
     DevBuf in, out, fin, f, wsum;      // staging / scratch
+    DevBuf sbar;                       // fused small-image kernel: grid-barrier words (zeroed once), stamps
+    bool small_used = false;           // the last hybrid call ran the fused kernel
     DevBuf amf_q[2], amf_cnt;          // AMF growth workspace (failure bitmap)
     std::vector<DevBuf> strip_g, strip_f;
     long long* host_w = nullptr;       // pinned readback of noise sums
@@ -166,13 +168,63 @@ cudaError_t copy2d(hyb_ctx* ctx, void* dst, size_t dp, const void* src, size_t s
 }
 
 // AMF launch with the context's growth workspace.
+// AMF growth workspace (bitmaps, records, counters): the counters are zeroed when (re)allocated and
+// every launch leaves them zero.
+cudaError_t ensure_amf_work(hyb_ctx* ctx, const hyb::Plane& p) {
+    const size_t need = hyb::amf_work_bytes(p);
+    if (need <= ctx->amf_q[0].bytes) return cudaSuccess;
+    cudaError_t e = ctx->amf_q[0].ensure(need);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ctx->amf_q[0].ptr, 0, 64, ctx->stream);
+    return e;
+}
+
 cudaError_t run_amf(hyb_ctx* ctx, const hyb::Plane& p, int smax, uint8_t* fin, size_t fpitch, size_t fslice) {
     cudaError_t e;
-    const size_t need = hyb::amf_work_bytes(p);
-    const bool fresh = need > ctx->amf_q[0].bytes;
-    if ((e = ctx->amf_q[0].ensure(need)) != cudaSuccess) return e;
-    if (fresh && (e = cudaMemsetAsync(ctx->amf_q[0].ptr, 0, 64, ctx->stream)) != cudaSuccess) return e;
+    if ((e = ensure_amf_work(ctx, p)) != cudaSuccess) return e;
     return hyb::launch_amf(p, smax, fin, fpitch, fslice, hyb::amf_work(ctx->amf_q[0].ptr, p), ctx->stream);
+}
+
+// The fused single-kernel step (small.cu) when the image qualifies (g TMA-compatible on the device).
+// Timed calls record ev[0] / ev[1] = ev[2] around it and read back the kernel's own stamps (AMF /
+// Wiener split) into host_w[1..3].  Returns false when not taken.
+bool try_small(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int cols, int smax, int win, uint8_t* y,
+               size_t ypitch, bool timed, int* status) {
+    *status = HYB_OK;
+    if (!hyb::tma_compatible(g, pitch, 0)) return false;
+    const hyb::SmallPlan pl = hyb::plan_small(rows, cols, smax, win);
+    if (!pl.ok) return false;
+    const size_t fp = round_pitch(cols);
+    cudaError_t e;
+    if ((e = ctx->f.ensure(fp * rows)) != cudaSuccess || (e = ctx->wsum.ensure(sizeof(long long))) != cudaSuccess) {
+        *status = cuda_fail(ctx, e, "try_small: allocation");
+        return true;
+    }
+    if (!ctx->sbar.ptr) {
+        if ((e = ctx->sbar.ensure(64)) != cudaSuccess || (e = cudaMemset(ctx->sbar.ptr, 0, 64)) != cudaSuccess) {
+            *status = cuda_fail(ctx, e, "try_small: barrier words");
+            return true;
+        }
+    }
+    if (timed && ((*status = ensure_host_w(ctx, 4)) || (e = cudaEventRecord(ctx->ev[0], ctx->stream)) != cudaSuccess)) {
+        if (!*status) *status = cuda_fail(ctx, e, "try_small: event");
+        return true;
+    }
+    const hyb::SmallBufs bufs{g, pitch, ctx->f.ptr, fp, y, ypitch, reinterpret_cast<unsigned long long*>(ctx->wsum.ptr),
+                              reinterpret_cast<unsigned*>(ctx->sbar.ptr)};
+    e = hyb::launch_small(pl, bufs, rows, cols, smax, win, ctx->stream);
+    if (e != cudaSuccess) {
+        *status = cuda_fail(ctx, e, "launch_small");
+        return true;
+    }
+    ctx->small_used = true;
+    if (timed) {
+        if ((e = cudaEventRecord(ctx->ev[1], ctx->stream)) != cudaSuccess ||
+            (e = cudaEventRecord(ctx->ev[2], ctx->stream)) != cudaSuccess ||
+            (e = cudaMemcpyAsync(ctx->host_w + 1, ctx->sbar.ptr + 8, 3 * sizeof(long long), cudaMemcpyDeviceToHost,
+                                 ctx->stream)) != cudaSuccess)
+            *status = cuda_fail(ctx, e, "try_small: stamps");
+    }
+    return true;
 }
 
 // Core of hyb_hybrid_u8 on device-resident buffers.
@@ -182,6 +234,10 @@ int hybrid_device(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int co
     HYB_CHECK(ctx->wsum.ensure(sizeof(long long)));
     unsigned long long* W = reinterpret_cast<unsigned long long*>(ctx->wsum.ptr);
     const long long P = (long long)rows * cols;
+    if (parts == 1) {
+        int st;
+        if (try_small(ctx, g, pitch, rows, cols, smax, win, y, ypitch, timed, &st)) return st;
+    }
     if (timed) HYB_CHECK(cudaEventRecord(ctx->ev[0], ctx->stream));
     if (parts == 1) {
         const size_t fp = round_pitch(cols);
@@ -263,6 +319,16 @@ int hybrid_host_pipelined(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows
     HYB_CHECK(ctx->in.ensure(pp * rows));
     HYB_CHECK(ctx->f.ensure(pp * rows));
     HYB_CHECK(ctx->out.ensure(pp * rows));
+    if (K == 1 && hyb::plan_small(rows, cols, smax, win).ok) {
+        // one piece: upload, the fused kernel, download, all on the compute stream
+        if (timed) HYB_CHECK(cudaEventRecord(ctx->ev[3], ctx->stream));
+        HYB_CHECK(copy2d(ctx, ctx->in.ptr, pp, g, pitch, cols, rows));
+        int st;
+        try_small(ctx, ctx->in.ptr, pp, rows, cols, smax, win, ctx->out.ptr, pp, timed, &st);
+        if (st) return st;
+        HYB_CHECK(copy2d(ctx, y, y_pitch, ctx->out.ptr, pp, cols, rows));
+        return HYB_OK;
+    }
     HYB_CHECK(ctx->wsum.ensure(sizeof(long long)));
     unsigned long long* W = reinterpret_cast<unsigned long long*>(ctx->wsum.ptr);
     std::vector<int> a(K + 1);
@@ -356,6 +422,7 @@ int hyb_destroy(hyb_ctx* ctx) {
     ctx->fin.release();
     ctx->f.release();
     ctx->wsum.release();
+    ctx->sbar.release();
     for (auto& b : ctx->amf_q) b.release();
     ctx->amf_cnt.release();
     for (auto& b : ctx->strip_g) b.release();
@@ -640,9 +707,18 @@ int hyb_hybrid_u8(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int co
     return HYB_OK;
 }
 
+// Fused-kernel runs report the kernel's own AMF / Wiener split (globaltimer stamps, host_w[1..3]).
+static void small_times(hyb_ctx* ctx, hyb_stats* stats) {
+    if (!ctx->small_used) return;
+    const unsigned long long t0 = ctx->host_w[1], t1 = ctx->host_w[2], t2 = ctx->host_w[3];
+    stats->t_adaptive = (double)(t1 - t0) * 1e-9;  // k = 3..smax (to the grid barrier)
+    stats->t_wiener = (double)(t2 - t1) * 1e-9;    // statistics + gain
+}
+
 static int hybrid_u8_impl(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int cols, int smax,
                           int win, int parts, uint8_t* y, size_t y_pitch, hyb_stats* stats, bool capturing) {
     if (!ctx) return HYB_EINVAL;
+    ctx->small_used = false;
     int st;
     if ((st = check_smax(ctx, smax)) || (st = check_win(ctx, win)) || (st = check_dims(ctx, rows, cols)) ||
         (st = check_pitch(ctx, pitch, cols, "g")) || (st = check_pitch(ctx, y_pitch, cols, "y")))
@@ -676,6 +752,7 @@ static int hybrid_u8_impl(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows
             stats->t_adaptive = am * 1e-3;  // AMF + statistics (interleaved with the upload)
             stats->t_wiener = w * 1e-3;     // gains (interleaved with the download)
             stats->t_total = t * 1e-3;
+            small_times(ctx, stats);
         }
         return HYB_OK;
     }
@@ -715,6 +792,7 @@ static int hybrid_u8_impl(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows
         stats->t_adaptive = a * 1e-3;
         stats->t_wiener = w * 1e-3;
         stats->t_total = t * 1e-3;
+        small_times(ctx, stats);
     }
     return HYB_OK;
 }

@@ -61,6 +61,27 @@ cudaError_t launch_wiener_stats(const Plane& p, int win, unsigned long long* noi
 cudaError_t launch_wiener_gain(const Plane& p, int win, const long long* noise_sum,
                                long long pixel_count, cudaStream_t stream);
 
+// Fused single-kernel hybrid step for small single images (small.cu): every CTA keeps its tiles
+// resident; two grid barriers (cooperative launch).  plan_small says whether it applies.
+struct SmallPlan {
+    bool ok;
+    int grid;
+    int slot_bytes;
+};
+SmallPlan plan_small(int rows, int cols, int smax, int win);
+struct SmallBufs {
+    const uint8_t* g;  // TMA-compatible
+    size_t gpitch;
+    uint8_t* f;        // AMF output scratch, TMA-compatible
+    size_t fpitch;
+    uint8_t* y;
+    size_t ypitch;
+    unsigned long long* wsum;      // W (zeroed in the kernel)
+    unsigned* sbar;                // 32 bytes, zero when allocated: barrier / exit counters, 3 globaltimer stamps
+};
+cudaError_t launch_small(const SmallPlan& pl, const SmallBufs& bufs, int rows, int cols, int smax, int win,
+                         cudaStream_t stream);
+
 // Kernel-launch counter (bench evidence), incremented by every launcher.
 void count_launch();
 
