@@ -160,8 +160,8 @@ __global__ void __launch_bounds__(K3T, 3)
         // ---- border tiles: edge replication (this strip's rows) in place of TMA's zero fill ----
         const int sx0 = x0 - CP, sy0 = y0 - 1;
         if (sx0 < 0 || sx0 + BS > cols || sy0 < 0 || sy0 + BH > rows)
-            warp_replicate_edges(B, BS, max(0, -sx0), min(BS, cols - sx0), max(0, -sy0), min(BH, rows - sy0),
-                                 sub * WR, sub * WR + WR + 2);
+            replicate_edges<32>(B, BS, max(0, -sx0), min(BS, cols - sx0), max(0, -sy0), min(BH, rows - sy0),
+                                sub * WR, sub * WR + WR + 2, 1);
 
         const int nf = k3_strip<FIN>(B, O, F, sub, args.grow ? args.bitmap + (size_t)t * 512 : nullptr,
                                      args.dst + (size_t)z * args.dslice + (size_t)(y0 - args.row_begin) * args.dpitch + x0,

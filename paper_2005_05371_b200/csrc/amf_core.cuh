@@ -751,39 +751,11 @@ __device__ __forceinline__ void grow_range(const CUtensorMap* tm, const GGeo& ge
         // ---- 3. tiles landed; border tiles get edge replication (whole CTA, columns then rows) ----
         for (int sl = 0; sl < ns; ++sl) mbar_wait(&bar[sl], (phases >> sl) & 1u);
         phases ^= (1u << ns) - 1u;
-        bool any_border = false;
-        for (int sl = 0; sl < ns; ++sl) any_border |= sinfo[8 * sl + 7] != 0;
-        if (any_border) {
-            for (int sl = 0; sl < ns; ++sl) {
-                if (!sinfo[8 * sl + 7]) continue;
-                uint8_t* B = bufs + (size_t)sl * geo.b_bytes;
-                const int sx0 = sinfo[8 * sl] - geo.CP, sy0 = sinfo[8 * sl + 1] - geo.R;
-                const int c_lo = max(0, -sx0), c_hi = min(geo.BS, cols - sx0);
-                const int r_lo = max(0, -sy0), r_hi = min(geo.BH, rows - sy0);
-                const int nl = c_lo, nfix = c_lo + (geo.BS - c_hi);
-                if (nfix == 0) continue;
-                for (int i = tid; i < (r_hi - r_lo) * nfix; i += NTHR) {
-                    const int rr = r_lo + i / nfix, j = i - (rr - r_lo) * nfix;
-                    uint8_t* row = B + (size_t)rr * geo.BS;
-                    if (j < nl) row[j] = row[c_lo];
-                    else row[c_hi + (j - nl)] = row[c_hi - 1];
-                }
-            }
-            __syncthreads();
-            for (int sl = 0; sl < ns; ++sl) {
-                if (!sinfo[8 * sl + 7]) continue;
-                uint8_t* B = bufs + (size_t)sl * geo.b_bytes;
-                const int sy0 = sinfo[8 * sl + 1] - geo.R;
-                const int r_lo = max(0, -sy0), r_hi = min(geo.BH, rows - sy0);
-                const int nfr = geo.BH - (r_hi - r_lo), wpr = geo.BS / 4;
-                for (int i = tid; i < nfr * wpr; i += NTHR) {
-                    const int k = i / wpr, q = i - k * wpr;
-                    const int rr = k < r_lo ? k : r_hi + (k - r_lo);
-                    const int src_r = rr < r_lo ? r_lo : r_hi - 1;
-                    reinterpret_cast<uint32_t*>(B + (size_t)rr * geo.BS)[q] =
-                        reinterpret_cast<const uint32_t*>(B + (size_t)src_r * geo.BS)[q];
-                }
-            }
+        for (int sl = 0; sl < ns; ++sl) {
+            if (!sinfo[8 * sl + 7]) continue;  // uniform
+            const int sx0 = sinfo[8 * sl] - geo.CP, sy0 = sinfo[8 * sl + 1] - geo.R;
+            replicate_edges<NTHR>(bufs + (size_t)sl * geo.b_bytes, geo.BS, max(0, -sx0), min(geo.BS, cols - sx0),
+                                  max(0, -sy0), min(geo.BH, rows - sy0), 0, geo.BH, geo.R);
         }
         __syncthreads();
         // ---- 4. levels, pooled over the batch ----

@@ -81,52 +81,15 @@ __device__ __forceinline__ void grid_exit(unsigned* count, unsigned* exits) {
     }
 }
 
-// CTA-wide edge replication of the border tiles among the first nt slots (uniform trip counts;
-// columns of in-image rows first, then whole out-of-image rows).  info[i] = {x0 - pad, y0 - halo}.
+// Edge replication of the border tiles among the first nt slots (org[i] = box origin), CTA-wide.
 __device__ __forceinline__ void cta_replicate_edges(uint8_t* slots, int slot_bytes, int nt, const int* org, int width,
-                                                    int height, int rows, int cols) {
-    const int tid = threadIdx.x;
-    bool any = false;
+                                                    int height, int rows, int cols, int reach) {
     for (int i = 0; i < nt; ++i) {
         const int sx0 = org[2 * i], sy0 = org[2 * i + 1];
-        any |= sx0 < 0 || sx0 + width > cols || sy0 < 0 || sy0 + height > rows;
+        if (sx0 < 0 || sx0 + width > cols || sy0 < 0 || sy0 + height > rows)
+            replicate_edges<SNT>(slots + (size_t)i * slot_bytes, width, max(0, -sx0), min(width, cols - sx0),
+                                 max(0, -sy0), min(height, rows - sy0), 0, height, reach);
     }
-    if (!any) return;
-    for (int i = 0; i < nt; ++i) {
-        const int sx0 = org[2 * i], sy0 = org[2 * i + 1];
-        const int c_lo = max(0, -sx0), c_hi = min(width, cols - sx0);
-        const int r_lo = max(0, -sy0), r_hi = min(height, rows - sy0);
-        const int nl = c_lo, nfix = c_lo + (width - c_hi);
-        uint8_t* T = slots + (size_t)i * slot_bytes;
-        const int n = (r_hi - r_lo) * nfix;
-        for (int j0 = 0; j0 < n; j0 += SNT) {
-            const int j = j0 + tid;
-            if (j < n) {
-                const int rr = r_lo + j / nfix, q = j - (rr - r_lo) * nfix;
-                uint8_t* row = T + rr * width;
-                if (q < nl) row[q] = row[c_lo];
-                else row[c_hi + (q - nl)] = row[c_hi - 1];
-            }
-        }
-    }
-    __syncthreads();
-    for (int i = 0; i < nt; ++i) {
-        const int sy0 = org[2 * i + 1];
-        const int r_lo = max(0, -sy0), r_hi = min(height, rows - sy0);
-        const int nfr = height - (r_hi - r_lo), wpr = width / 4;
-        uint8_t* T = slots + (size_t)i * slot_bytes;
-        const int n = nfr * wpr;
-        for (int j0 = 0; j0 < n; j0 += SNT) {
-            const int j = j0 + tid;
-            if (j < n) {
-                const int k = j / wpr, q = j - k * wpr;
-                const int rr = k < r_lo ? k : r_hi + (k - r_lo);
-                const int src = rr < r_lo ? r_lo : r_hi - 1;
-                reinterpret_cast<uint32_t*>(T + rr * width)[q] = reinterpret_cast<const uint32_t*>(T + src * width)[q];
-            }
-        }
-    }
-    __syncthreads();
 }
 
 template <int RW>
@@ -178,7 +141,7 @@ __global__ void __launch_bounds__(SNT, 2) hybrid_small_kernel(const __grid_const
     __syncthreads();
     for (int i = 0; i < nt; ++i) mbar_wait(&bar[i], 0);
     TRACE(0, 1);
-    cta_replicate_edges(slots, a.slot_bytes, nt, org, geo.BS, geo.BH, a.rows, a.cols);
+    cta_replicate_edges(slots, a.slot_bytes, nt, org, geo.BS, geo.BH, a.rows, a.cols, geo.R);
     TRACE(0, 2);
     {
         uint8_t* O = stage + warp * WPIX;
@@ -230,7 +193,7 @@ __global__ void __launch_bounds__(SNT, 2) hybrid_small_kernel(const __grid_const
     __syncthreads();
     for (int i = 0; i < nt; ++i) mbar_wait(&bar[i], 1);
     TRACE(0, 7);
-    cta_replicate_edges(slots, a.slot_bytes, nt, org, FBS, FROWS, a.rows, a.cols);
+    cta_replicate_edges(slots, a.slot_bytes, nt, org, FBS, FROWS, a.rows, a.cols, RW);
     TRACE(0, 8);
     unsigned long long vsum = 0;
     for (int j = warp; j < nt * (TH / SFH); j += NW) {

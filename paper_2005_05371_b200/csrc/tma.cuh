@@ -61,41 +61,49 @@ __device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
 }
 
 // Edge replication in a TMA-loaded byte tile (`width` bytes per row, out-of-image bytes zero-filled
-// by TMA): within rows [row0, row1), columns < c_lo take column c_lo and columns >= c_hi take column
-// c_hi - 1, then rows outside [r_lo, r_hi) copy the nearest in-image row.  Warp-cooperative with
-// warp-uniform trip counts (a lane-strided loop with a ragged tail would leave the warp diverged
-// while the caller reads the tile), ending with __syncwarp.
-__device__ __forceinline__ void warp_replicate_edges(uint8_t* T, int width, int c_lo, int c_hi, int r_lo, int r_hi,
-                                                     int row0, int row1) {
-    const int lane = threadIdx.x & 31;
-    const int nl = c_lo, nfix = c_lo + (width - c_hi);
+// by TMA; in-image columns [c_lo, c_hi), rows [r_lo, r_hi)), restricted to rows [row0, row1) and to
+// the `reach` columns / rows next to the image -- the only out-of-image bytes a window of radius
+// <= reach around an in-image pixel reads: those columns take the nearest in-image column, then
+// those rows copy the nearest in-image row.  NTHR cooperating threads (32: one warp; else the CTA)
+// with uniform trip counts (a lane-strided loop with a ragged tail would leave a warp diverged while
+// the caller reads the tile); ends with a warp / CTA barrier.
+template <int NTHR>
+__device__ __forceinline__ void replicate_edges(uint8_t* T, int width, int c_lo, int c_hi, int r_lo, int r_hi, int row0,
+                                                int row1, int reach) {
+    const int tid = NTHR == 32 ? (int)(threadIdx.x & 31) : (int)threadIdx.x;
+    const int cl0 = max(0, c_lo - reach), cr1 = min(width, c_hi + reach);
+    const int nl = c_lo - cl0, nfix = nl + (cr1 - c_hi);
     const int ra = max(row0, r_lo), rb = min(row1, r_hi);
     if (nfix > 0 && rb > ra) {
         const int n = (rb - ra) * nfix;
-        for (int i0 = 0; i0 < n; i0 += 32) {
-            const int i = i0 + lane;
+        for (int i0 = 0; i0 < n; i0 += NTHR) {
+            const int i = i0 + tid;
             if (i < n) {
                 const int rr = ra + i / nfix, j = i - (rr - ra) * nfix;
                 uint8_t* row = T + rr * width;
-                if (j < nl) row[j] = row[c_lo];
+                if (j < nl) row[cl0 + j] = row[c_lo];
                 else row[c_hi + (j - nl)] = row[c_hi - 1];
             }
         }
-        __syncwarp();
+        if (NTHR == 32) __syncwarp();
+        else __syncthreads();
     }
     const int wpr = width / 4;
-    const int above = max(0, min(row1, r_lo) - row0), below = max(0, row1 - max(row0, r_hi));
+    const int a0 = max(row0, r_lo - reach), a1 = min(row1, r_lo);  // rows above the image
+    const int b0 = max(row0, r_hi), b1 = min(row1, r_hi + reach);  // rows below
+    const int above = max(0, a1 - a0), below = max(0, b1 - b0);
     const int n = (above + below) * wpr;
-    for (int i0 = 0; i0 < n; i0 += 32) {
-        const int i = i0 + lane;
+    for (int i0 = 0; i0 < n; i0 += NTHR) {
+        const int i = i0 + tid;
         if (i < n) {
             const int k = i / wpr, q = i - k * wpr;
-            const int rr = k < above ? row0 + k : max(row0, r_hi) + (k - above);
+            const int rr = k < above ? a0 + k : b0 + (k - above);
             const int src = rr < r_lo ? r_lo : r_hi - 1;
             reinterpret_cast<uint32_t*>(T + rr * width)[q] = reinterpret_cast<const uint32_t*>(T + src * width)[q];
         }
     }
-    __syncwarp();
+    if (NTHR == 32) __syncwarp();
+    else __syncthreads();
 }
 
 // 3-D tiled TMA load (x = column, y = row, z = slice); out-of-bounds elements read as zero.

@@ -305,8 +305,8 @@ __global__ void __launch_bounds__(FNW * 32, GAIN ? 4 : 3) wiener_fast_kernel(con
         // ---- border tiles: replicate edges into the zero-filled halo (warp-private slot) ----
         const int sx0 = x0 - FCP, sy0 = y0 - RW;
         if (sx0 < 0 || sx0 + FBS > a.cols || sy0 < 0 || sy0 + SROWS > a.rows)
-            warp_replicate_edges(T, FBS, max(0, -sx0), min(FBS, a.cols - sx0), max(0, -sy0),
-                                 min(SROWS, a.rows - sy0), 0, SROWS);
+            replicate_edges<32>(T, FBS, max(0, -sx0), min(FBS, a.cols - sx0), max(0, -sy0),
+                                min(SROWS, a.rows - sy0), 0, SROWS, RW);
 
         const int col_lim = a.cols - x0, row_lim = a.row_end - y0;
         if (!GAIN) {
