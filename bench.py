@@ -31,6 +31,16 @@ METRIC = "MPix/s for hybrid AMF+Wiener (uint8) at 1/2/4/8 B200; % of roofline"
 L2_BYTES = 126 * 1024 * 1024
 
 
+def load_traffic(cfg):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum from one ncu --set full capture,
+    summed over a stage's kernels) committed under profiles/ -- measured once, reported beside `achieved`."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(f"config{cfg}", {})
+    except Exception:
+        return {}
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -332,17 +342,32 @@ def run_gpu(args, cfg, c):
 
     # ---------------- roofline of the dominant kernel ----------------
     roofline = None
-    if kern:
+    fused = world == 1 and launches == args.steps  # one kernel per step: the fused small-image kernel
+    traffic = load_traffic(cfg)
+    if fused:
+        # the whole step is one launch; its algorithmic bytes are the hybrid's 4 B/px
+        ach = 4 * px_total / (ms_step * 1e-3) / 1e9
+        roofline = {"bound": "hbm", "kernel": "hybrid_small_kernel (AMF + W1 fused)", "achieved": round(ach, 1),
+                    "peak": hbm, "unit": "GB/s", "frac": round(ach / hbm, 4),
+                    "traffic": traffic.get("hybrid_small_kernel"), "peak_source": hbm_src,
+                    "algorithmic_bytes_per_launch": 4 * px_total,
+                    "step_achieved": round(ach, 1), "step_frac": round(ach / hbm, 4),
+                    "kernel_ms": dict(kern, fused_ms=round(ms_step, 4))}
+    elif kern:
         t_amf = kern["amf_ms"]
-        bytes_amf = 2 * px_total  # read g + write f, 1 B/px each
         t_w = kern["wiener_ms"] or 0.0
         dominant = "amf" if t_amf >= t_w else "wiener"
         if dominant == "amf":
-            ach = bytes_amf / (t_amf * 1e-3) / 1e9
+            nbytes = 2 * px_total  # read g + write f, 1 B/px each
+            ach = nbytes / (t_amf * 1e-3) / 1e9
+            tr = traffic.get("amf")
         else:
-            ach = 3 * px_total / (t_w * 1e-3) / 1e9  # stats reads f, gain reads f + writes y
+            nbytes = 3 * px_total  # stats reads f, gain reads f + writes y
+            ach = nbytes / (t_w * 1e-3) / 1e9
+            tr = traffic.get("wiener")
         roofline = {"bound": "hbm", "kernel": dominant, "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
-                    "frac": round(ach / hbm, 4), "traffic": None, "peak_source": hbm_src,
+                    "frac": round(ach / hbm, 4), "traffic": tr, "peak_source": hbm_src,
+                    "algorithmic_bytes_per_launch": nbytes,
                     "step_achieved": round(4 * px_total / (ms_step * 1e-3) / 1e9, 1),
                     "step_frac": round(4 * px_total / (ms_step * 1e-3) / 1e9 / hbm, 4),
                     "kernel_ms": kern}

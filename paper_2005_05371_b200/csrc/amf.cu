@@ -2,25 +2,18 @@
 //
 // Semantics: detail::adaptive_median_rows, reference proj/src/adaptive_median.cpp:123-215
 // (windows k = 3..smax over the pristine input, edge replication, level A/B, unresolved pixels
-// keep their input).  Design (DESIGN.md 4):
+// keep their input).  Design (DESIGN.md 4.1, 4.2):
 //
-//   * amf_k3_kernel (persistent): 95-99.7 % of pixels finalise at k = 3, so k = 3 runs on every
-//     pixel.  128 x 32 tiles plus a 1-pixel halo arrive in shared memory by TMA (mbarrier
-//     completion, 4-deep ring); warps claim 4-row strips dynamically, so no CTA-wide barrier
-//     sits on the steady-state path, and the last warp done with a buffer refills it.  Pixels
-//     are processed as u16x2 row PAIRS (each lane holds v * 257 so lane order = pixel order and
-//     one PRMT builds a pair word): a lane owns 2 rows x 8 columns, sorts each 3-tall column
-//     once (min / max / xor-median) and reuses it for 3 outputs; level A/B become lane masks
-//     through a sign-replicating PRMT.  Every pixel's k = 3 result (or its input when level A
-//     fails) is stored; level-A failures are appended to a device-wide work queue
-//     (warp-aggregated atomic).
-//   * amf_grow_* kernels, one launch per window size k = 5..smax: each walks the compacted
-//     queue of pixels still open, gathers their k x k windows from global memory (L1/L2
-//     resident: the queue is in raster order) and re-queues survivors for k + 2.  k = 5 and 7
-//     put two queued pixels in the u16x2 lanes of one thread and run a generated pruned
-//     selection network (min / median / max, networks.cuh); k >= 9 (< 2 % of pixels even at
-//     config 4) test level A with SWAR counts of zmin / zmax and take the median by a bitwise
-//     radix select only when it is needed.
+//   * amf_k3_kernel (persistent, 8 compute warps + 1 producer warp): 95-99.7 % of pixels finalise
+//     at k = 3, so k = 3 runs on every pixel.  The producer claims 128 x 32 tiles and TMA-loads
+//     them (+ 1-pixel halo) into a 4-deep full/empty mbarrier ring; compute warps claim 4-row
+//     strips (amf_core.cuh k3_strip: u16x2 row pairs, column sorts reused by 3 outputs, level A/B
+//     as lane masks).  Level-A failures go to a per-tile bitmap; the tile's last strip appends one
+//     weighted work record (64-bit atomic).
+//   * amf_grow_kernel (persistent): every CTA takes an equal weighted range of the records, loads
+//     the tiles it touches (+ R halo) by TMA, pools their failures in shared memory and runs the
+//     levels k = 5..smax over the pool (amf_core.cuh grow_range / grow_levels): pruned selection
+//     networks on u16x2 pairs for k = 5, 7; SWAR level-A counts + radix select for k >= 9.
 #include <cuda.h>
 
 #include <algorithm>

@@ -37,9 +37,9 @@ def main(path, pixels=None):
             v = float(r[idx[k]].replace(",", "") or 0)
             u = units[idx[k]]
             if k.startswith("dram__bytes"):
-                v = v * {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(u, 1.0)
+                v = v * {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "B": 1e-6, "KB": 1e-3, "MB": 1.0, "GB": 1e3}.get(u, 1.0)
             elif k == "gpu__time_duration.sum":
-                v = v * {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(u, 1.0)
+                v = v * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(u, 1.0)
             else:
                 v *= sc
             vals.append(f"{v:.2f}")
