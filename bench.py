@@ -164,7 +164,7 @@ def run_reference(args, cfg, c):
     return 0
 
 
-def workload(cfg, c, n):
+def workload(cfg, c, n, exclusive=True):
     slices = c["slices"]
     d = {"workload": f"config{cfg}: {c['rows']}x{c['cols']} uint8 phantom"
          + (f" x {slices} slices" if slices > 1 else "")
@@ -172,7 +172,9 @@ def workload(cfg, c, n):
            f"Wiener {c['win']}x{c['win']}",
          "pixels_per_step": c["rows"] * c["cols"] * slices,
          "partition": (f"{n} slice shards" if slices > 1 else f"{n} horizontal strips") if n > 1 else "1 GPU",
-         "l2": "rotating input/output buffers > 3x L2 (cold reads every step)"}
+         "l2": "rotating input/output buffers > 3x L2 (cold reads every step)",
+         "device_mode": "exclusive (hyb_set_exclusive: plain persistent launches)" if exclusive
+         else "shared (cooperative launches)"}
     return d
 
 
@@ -198,6 +200,7 @@ def run_gpu(args, cfg, c):
     torch.cuda.set_stream(stream)
     ctx = capi.Context(local)
     ctx.set_stream(stream.cuda_stream)
+    ctx.set_exclusive(not args.shared_gpu)  # the bench owns the GPU (dedicated-device mode)
     lib = capi.lib
 
     rows, cols, slices = c["rows"], c["cols"], c["slices"]
@@ -383,7 +386,7 @@ def run_gpu(args, cfg, c):
         "metric": METRIC, "value": round(value, 3), "unit": "MPix/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True,
         "scaling": "weak" if slices > 1 else "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": workload(cfg, c, world), "clocks": clk.report(), "e2e": e2e, "gpu_launches": int(launches),
+        "config": workload(cfg, c, world, not args.shared_gpu), "clocks": clk.report(), "e2e": e2e, "gpu_launches": int(launches),
         "roofline": roofline, "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)
@@ -402,6 +405,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shared-gpu", action="store_true",
+                    help="do not declare the GPU exclusive (hyb_set_exclusive): cooperative fused launches")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -104,10 +104,11 @@ __device__ __forceinline__ int k3_strip(const uint8_t* __restrict__ B, uint8_t* 
                     gm[i] = w[i];
                     lo[i] = __vminu2(lo[i], w[i]);
                     hi[i] = __vmaxu2(hi[i], w[i]);
-                    mid[i] ^= w[i];
+                    mid[i] = add_fma(mid[i], w[i]);
                 } else {
                     const uint32_t l = __vminu2(lo[i], w[i]), h = __vmaxu2(hi[i], w[i]);
-                    mid[i] = mid[i] ^ w[i] ^ l ^ h;  // median of 3 = a^b^c^min^max
+                    // median of 3 = a + b + c - min - max (IMADs: exact on packed lanes, FMA pipe)
+                    mid[i] = sub_fma(sub_fma(add_fma(mid[i], w[i]), l), h);
                     lo[i] = l;
                     hi[i] = h;
                 }
@@ -124,7 +125,8 @@ __device__ __forceinline__ int k3_strip(const uint8_t* __restrict__ B, uint8_t* 
             const uint32_t bh = __vimax3_u16x2(mid[j], mid[j + 1], mid[j + 2]);
             const uint32_t b = mid[j] ^ mid[j + 1] ^ mid[j + 2] ^ bl ^ bh;
             const uint32_t ml = __vimin3_u16x2(a, b, c), mh = __vimax3_u16x2(a, b, c);
-            const uint32_t zmed = a ^ b ^ c ^ ml ^ mh;  // median of 9 = med3(max lo, med mid, min hi)
+            // median of 9 = med3(max lo, med mid, min hi)
+            const uint32_t zmed = sub_fma(sub_fma(add_fma(add_fma(a, b), c), ml), mh);
             const uint32_t g = gm[j + 1];
             // lane masks (values are v * 257): mA = level A holds, mB = zmin < g < zmax
             const uint32_t mA =

@@ -6,6 +6,7 @@
 // wiener.cu; there is no CPU fallback -- a missing device or a failed launch is an error.
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <map>
 #include <tuple>
 #include <cstdio>
@@ -60,6 +61,7 @@ struct hyb_ctx {
     DevBuf in, out, fin, f, wsum;      // staging / scratch
     DevBuf sbar;                       // fused small-image kernel: grid-barrier words (zeroed once), stamps
     bool small_used = false;           // the last hybrid call ran the fused kernel
+    bool exclusive = false;            // hyb_set_exclusive: plain (non-cooperative) fused launches
     DevBuf amf_q[2], amf_cnt;          // AMF growth workspace (failure bitmap)
     std::vector<DevBuf> strip_g, strip_f;
     long long* host_w = nullptr;       // pinned readback of noise sums
@@ -211,7 +213,7 @@ bool try_small(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int cols,
     }
     const hyb::SmallBufs bufs{g, pitch, ctx->f.ptr, fp, y, ypitch, reinterpret_cast<unsigned long long*>(ctx->wsum.ptr),
                               reinterpret_cast<unsigned*>(ctx->sbar.ptr)};
-    e = hyb::launch_small(pl, bufs, rows, cols, smax, win, ctx->stream);
+    e = hyb::launch_small(pl, bufs, rows, cols, smax, win, !ctx->exclusive, ctx->stream);
     if (e != cudaSuccess) {
         *status = cuda_fail(ctx, e, "launch_small");
         return true;
@@ -448,6 +450,12 @@ int hyb_set_stream(hyb_ctx* ctx, void* stream) {
     return HYB_OK;
 }
 
+int hyb_set_exclusive(hyb_ctx* ctx, int exclusive) {
+    if (!ctx) return HYB_EINVAL;
+    ctx->exclusive = exclusive != 0;
+    return HYB_OK;
+}
+
 const char* hyb_last_error(const hyb_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
 int64_t hyb_kernel_launches(const hyb_ctx*) { return hyb::g_launches.load(); }
@@ -667,7 +675,10 @@ int hyb_hybrid_u8(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int co
     const bool gok = g && cudaPointerGetAttributes(&ga, g) == cudaSuccess;
     const bool yok = y && cudaPointerGetAttributes(&ya, y) == cudaSuccess;
     cudaGetLastError();
-    const bool graphable = !stats && gok && yok && ga.type != cudaMemoryTypeUnregistered &&
+    // Cooperative launches (the fused small-image kernel without exclusive mode) are cheaper as
+    // direct launches than as graph nodes, so those calls are not captured.
+    const bool coop_small = !ctx->exclusive && parts == 1 && hyb::plan_small(rows, cols, smax, win).ok;
+    const bool graphable = !coop_small && !stats && gok && yok && ga.type != cudaMemoryTypeUnregistered &&
                            ya.type != cudaMemoryTypeUnregistered && ctx->stream != nullptr;
     if (!graphable) return hybrid_u8_impl(ctx, g, pitch, rows, cols, smax, win, parts, y, y_pitch, stats, false);
     const hyb_ctx::GraphKey key{g, y, pitch, y_pitch, rows, cols, smax, win, parts, ctx->stream};

@@ -79,8 +79,10 @@ struct SmallBufs {
     unsigned long long* wsum;      // W (zeroed in the kernel)
     unsigned* sbar;                // 32 bytes, zero when allocated: barrier / exit counters, 3 globaltimer stamps
 };
+// cooperative: launch with cudaLaunchAttributeCooperative (co-residency guaranteed by the driver);
+// otherwise a plain launch whose grid never exceeds the occupancy (caller: exclusive device).
 cudaError_t launch_small(const SmallPlan& pl, const SmallBufs& bufs, int rows, int cols, int smax, int win,
-                         cudaStream_t stream);
+                         bool cooperative, cudaStream_t stream);
 
 // Kernel-launch counter (bench evidence), incremented by every launcher.
 void count_launch();

@@ -33,7 +33,7 @@ namespace hyb {
 namespace {
 
 constexpr int SNT = 256;   // threads per CTA (8 warps)
-constexpr int STPC = 3;    // tiles per CTA (max)
+constexpr int STPC = 2;    // tiles per CTA (max)
 constexpr int SHDR = 1024;  // mbarriers, tile coordinates, level counters
 constexpr int SFH = 8;     // W1 sub-tile rows
 
@@ -93,7 +93,7 @@ __device__ __forceinline__ void cta_replicate_edges(uint8_t* slots, int slot_byt
 }
 
 template <int RW>
-__global__ void __launch_bounds__(SNT, 2) hybrid_small_kernel(const __grid_constant__ CUtensorMap tm_g,
+__global__ void __launch_bounds__(SNT, 3) hybrid_small_kernel(const __grid_constant__ CUtensorMap tm_g,
                                                              const __grid_constant__ CUtensorMap tm_f,
                                                              const __grid_constant__ SArgs a) {
     constexpr int FROWS = TH + 2 * RW;  // f tile rows with the W1 halo
@@ -238,7 +238,7 @@ int g_ssms = 0;
 
 template <int RW>
 cudaError_t launch_small_rw(const SmallPlan& pl, const SmallBufs& bf, int rows, int cols, int smax,
-                            cudaStream_t stream) {
+                            bool cooperative, cudaStream_t stream) {
     SArgs a;
     a.geo = make_ggeo(smax);
     a.slot_bytes = pl.slot_bytes;
@@ -278,7 +278,7 @@ cudaError_t launch_small_rw(const SmallPlan& pl, const SmallBufs& bf, int rows, 
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = cooperative ? 1 : 0;
     e = cudaLaunchKernelEx(&cfg, kern, tm_g, tm_f, a);
     count_launch();
     return e;
@@ -321,12 +321,12 @@ SmallPlan plan_small(int rows, int cols, int smax, int win) {
 }
 
 cudaError_t launch_small(const SmallPlan& pl, const SmallBufs& bf, int rows, int cols, int smax, int win,
-                         cudaStream_t stream) {
+                         bool cooperative, cudaStream_t stream) {
     switch ((win - 1) / 2) {
-        case 0: return launch_small_rw<0>(pl, bf, rows, cols, smax, stream);
-        case 1: return launch_small_rw<1>(pl, bf, rows, cols, smax, stream);
-        case 2: return launch_small_rw<2>(pl, bf, rows, cols, smax, stream);
-        default: return launch_small_rw<3>(pl, bf, rows, cols, smax, stream);
+        case 0: return launch_small_rw<0>(pl, bf, rows, cols, smax, cooperative, stream);
+        case 1: return launch_small_rw<1>(pl, bf, rows, cols, smax, cooperative, stream);
+        case 2: return launch_small_rw<2>(pl, bf, rows, cols, smax, cooperative, stream);
+        default: return launch_small_rw<3>(pl, bf, rows, cols, smax, cooperative, stream);
     }
 }
 

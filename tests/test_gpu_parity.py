@@ -130,6 +130,28 @@ def test_amf_repeated_calls_keep_workspace_consistent(ctx):
         np.testing.assert_array_equal(out.cpu().numpy(), want_small, err_msg=f"rep {rep} small")
 
 
+def test_hybrid_fused_launch_modes_agree(ctx):
+    # config 1 runs the fused single-kernel step: cooperative (default) and exclusive-device launches,
+    # repeated on one context (graph replay in exclusive mode), all equal to the oracle
+    c = CONFIGS[1]
+    img = capi.make_phantom(c["rows"], c["cols"], c["ellipses"], c["sigma"], c["density"], 0)
+    ref_y, ref_w = oracle.hybrid(img, c["smax"], c["win"])
+    g = torch.from_numpy(img).cuda()
+    y = torch.empty_like(g)
+    for exclusive in (False, True, False):
+        ctx.set_exclusive(exclusive)
+        for _ in range(3):
+            y.fill_(0)
+            torch.cuda.synchronize()
+            capi.check(capi.lib.hyb_hybrid_u8(ctx.ptr, g.data_ptr(), c["cols"], c["rows"], c["cols"], c["smax"],
+                                              c["win"], 1, y.data_ptr(), c["cols"], None), ctx.ptr)
+            torch.cuda.synchronize()
+            np.testing.assert_array_equal(y.cpu().numpy(), ref_y, err_msg=f"exclusive={exclusive}")
+    ctx.set_exclusive(False)
+    res = denoise.hybrid_denoise(img, FilterConfig(smax=c["smax"], wiener_window=c["win"]), ctx=ctx)
+    assert res.noise_sum == ref_w and res.t_adaptive > 0 and res.t_wiener > 0
+
+
 def test_amf_worst_case_growth(ctx):
     # config-4 statistics (sigma 20, density 0.5, smax 11) on a 1024^2 crop-sized phantom
     img = capi.make_phantom(1024, 1024, 16, 20.0, 0.5, 0)
