@@ -507,12 +507,12 @@ __device__ __forceinline__ long long rec_off(const unsigned long long* rec, long
 }
 
 // Growth levels k = 5..smax over a pooled queue Q0[0, n) of entries slot << 12 | pixel (pixel =
-// row * 128 + column of a 128 x 32 tile whose window bytes sit in bufs + slot * geo.b_bytes).  CTA-wide
+// row * 128 + column of a 128 x 32 tile whose window bytes start at slot(slot), laid out as geo).  CTA-wide
 // (NTHR threads, every thread calls it; qcount[1..] zero on entry); level k resolves what it can through
 // out(slot, pixel, value, k) and re-queues the rest for k + 2.  Ends with __syncthreads.
-template <bool FIN, int NTHR, class Out>
-__device__ __forceinline__ void grow_levels(const uint8_t* bufs, const GGeo& geo, uint16_t* Q0, uint16_t* Q1,
-                                            int* qcount, int n, int smax, Out out) {
+template <bool FIN, int NTHR, class Slot, class Out>
+__device__ __forceinline__ void grow_levels_at(Slot slot, const GGeo& geo, uint16_t* Q0, uint16_t* Q1, int* qcount,
+                                               int n, int smax, Out out) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int lvl = 0;
     for (int k = 5; k <= smax; k += 2, ++lvl) {
@@ -531,8 +531,8 @@ __device__ __forceinline__ void grow_levels(const uint8_t* bufs, const GGeo& geo
                     eb = hasb ? qin[2 * i + 1] : ea;
                     const int sa = ea >> 12, pa = ea & 4095, sb = eb >> 12, pb = eb & 4095;
                     uint32_t done, outw;
-                    const uint8_t* BA = bufs + (size_t)sa * geo.b_bytes;
-                    const uint8_t* BB = bufs + (size_t)sb * geo.b_bytes;
+                    const uint8_t* BA = slot(sa);
+                    const uint8_t* BB = slot(sb);
                     if (k == 5) level_pair2<5>(BA, BB, geo, pa, pb, done, outw);
                     else level_pair2<7>(BA, BB, geo, pa, pb, done, outw);
                     if (done & 1u) {
@@ -570,7 +570,7 @@ __device__ __forceinline__ void grow_levels(const uint8_t* bufs, const GGeo& geo
                 if (i < n) {
                     e = qin[i];
                     const int sl = e >> 12, pix = e & 4095, ty = pix >> 7, tx = pix & 127;
-                    const uint8_t* B = bufs + (size_t)sl * geo.b_bytes;
+                    const uint8_t* B = slot(sl);
                     uint8_t o = 0;
                     bool done;
                     switch (k) {
@@ -600,6 +600,14 @@ __device__ __forceinline__ void grow_levels(const uint8_t* bufs, const GGeo& geo
         n = qcount[lvl + 1];
         if (n == 0) break;
     }
+}
+
+// Slots at a fixed stride in local shared memory.
+template <bool FIN, int NTHR, class Out>
+__device__ __forceinline__ void grow_levels(const uint8_t* bufs, const GGeo& geo, uint16_t* Q0, uint16_t* Q1,
+                                            int* qcount, int n, int smax, Out out) {
+    grow_levels_at<FIN, NTHR>([&](int sl) { return bufs + (size_t)sl * geo.b_bytes; }, geo, Q0, Q1, qcount, n, smax,
+                              out);
 }
 
 // Growth over the failure range [gbeg, gend) of the weighted record order (records: (offset << 24) |
