@@ -120,6 +120,18 @@ int hyb_hybrid_batch_u8(hyb_ctx* ctx, const uint8_t* g, size_t pitch, size_t sli
                         int n_slices, int rows, int cols, int smax, int win, uint8_t* y,
                         size_t y_pitch, size_t y_slice_stride, int64_t* noise_sums);
 
+/* contrast_stretch -- reference proj/src/pipeline.cpp:10-21: out = (v - lo)
+ * / (hi - lo) over the image min / max, as uint8 = floor((510 (v - lo) + (hi - lo)) / (2 (hi - lo)))
+ * (the exact rational rounded half up; lo -> 0, hi -> 255); unchanged when hi == lo.  src == dst
+ * allowed (in place). */
+int hyb_contrast_stretch_u8(hyb_ctx* ctx, const uint8_t* src, size_t pitch, int rows, int cols,
+                            uint8_t* dst, size_t dst_pitch);
+
+/* hybrid_denoise stages 1-3 (stretch_after_each = false): hyb_hybrid_u8, then the final
+ * contrast_stretch (proj/src/pipeline.cpp:55). */
+int hyb_hybrid_stretch_u8(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int cols, int smax,
+                          int win, int parts, uint8_t* y, size_t y_pitch, hyb_stats* stats);
+
 /* Synthetic phantom of BASELINE.json's configs (host only, deterministic):
  * background 20, n_ellipses ellipses (full axes 20-200 px, rotation U[0,pi), intensity
  * U[40,220]), +-15 linear gradient along columns, Gaussian sigma (rounded, clipped), then salt &

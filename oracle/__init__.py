@@ -31,6 +31,7 @@ def _load_oracle():
                                               P, c_size_t]
     lib.hyb_oracle_hybrid_u8.argtypes = [P, c_size_t, c_int, c_int, c_int, c_int, P, P, c_size_t, POINTER(c_int64)]
     lib.hyb_oracle_validate_smax.argtypes = [c_int]
+    lib.hyb_oracle_contrast_stretch_u8.argtypes = [P, c_size_t, c_int, c_int, P, c_size_t]
     return lib
 
 
@@ -210,3 +211,14 @@ def ref_hybrid_baseline(g, smax, win, threads):
     if st:
         raise ValueError(ref().ref_last_error().decode())
     return y, ta.value, tw.value
+
+
+def contrast_stretch(img):
+    """uint8 contrast stretch (proj/src/pipeline.cpp:10-21 restated, rounded half up to 0..255)."""
+    img, p = _u8(img)
+    rows, cols = img.shape
+    out = np.empty_like(img)
+    if lib().hyb_oracle_contrast_stretch_u8(p, cols, rows, cols, out.ctypes.data, cols):
+        raise ValueError("oracle contrast_stretch rejected its arguments")
+    return out
+

@@ -187,3 +187,28 @@ int hyb_oracle_hybrid_u8(const uint8_t* g, size_t pitch, int rows, int cols, int
     return hyb_oracle_wiener_gain_u8(work, (size_t)cols, rows, cols, 0, rows, win, w,
                                      (int64_t)rows * cols, y, ypitch);
 }
+
+/* contrast_stretch, reference proj/src/pipeline.cpp:10-21: out = (p - lo) / (hi - lo) over the
+ * image's min / max, the image unchanged when hi == lo.  On k/255 inputs the reference's double
+ * result is the exact rational (v - lo) / (hi - lo) up to one rounding; the uint8 form here is that
+ * rational scaled to 0..255 and rounded half up: out = floor((510 (v - lo) + (hi - lo)) / (2 (hi - lo))),
+ * so lo -> 0 and hi -> 255 exactly (the reference's endpoints 0.0 and 1.0, :16-19). */
+int hyb_oracle_contrast_stretch_u8(const uint8_t* src, size_t pitch, int rows, int cols, uint8_t* dst,
+                                   size_t dpitch) {
+    if (rows < 1 || cols < 1) return 1;
+    int lo = 255, hi = 0;
+    for (int r = 0; r < rows; ++r)
+        for (int c = 0; c < cols; ++c) {
+            const int v = src[(size_t)r * pitch + c];
+            if (v < lo) lo = v;
+            if (v > hi) hi = v;
+        }
+    for (int r = 0; r < rows; ++r)
+        for (int c = 0; c < cols; ++c) {
+            const int v = src[(size_t)r * pitch + c];
+            dst[(size_t)r * dpitch + c] =
+                hi == lo ? (uint8_t)v : (uint8_t)((510 * (v - lo) + (hi - lo)) / (2 * (hi - lo)));
+        }
+    return 0;
+}
+

@@ -60,6 +60,7 @@ struct hyb_ctx {
     std::string err;
     DevBuf in, out, fin, f, wsum;      // staging / scratch
     DevBuf sbar;                       // fused small-image kernel: grid-barrier words (zeroed once), stamps
+    DevBuf mm, ys;                     // contrast stretch: min / max scratch, staged hybrid output
     bool small_used = false;           // the last hybrid call ran the fused kernel
     bool exclusive = false;            // hyb_set_exclusive: plain (non-cooperative) fused launches
     DevBuf amf_q[2], amf_cnt;          // AMF growth workspace (failure bitmap)
@@ -425,6 +426,8 @@ int hyb_destroy(hyb_ctx* ctx) {
     ctx->f.release();
     ctx->wsum.release();
     ctx->sbar.release();
+    ctx->mm.release();
+    ctx->ys.release();
     for (auto& b : ctx->amf_q) b.release();
     ctx->amf_cnt.release();
     for (auto& b : ctx->strip_g) b.release();
@@ -804,6 +807,68 @@ static int hybrid_u8_impl(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows
         stats->t_wiener = w * 1e-3;
         stats->t_total = t * 1e-3;
         small_times(ctx, stats);
+    }
+    return HYB_OK;
+}
+
+int hyb_contrast_stretch_u8(hyb_ctx* ctx, const uint8_t* src, size_t pitch, int rows, int cols, uint8_t* dst,
+                            size_t dst_pitch) {
+    if (!ctx) return HYB_EINVAL;
+    int st;
+    if ((st = check_dims(ctx, rows, cols)) || (st = check_pitch(ctx, pitch, cols, "src")) ||
+        (st = check_pitch(ctx, dst_pitch, cols, "dst")))
+        return st;
+    if (!src || !dst) return fail(ctx, HYB_EINVAL, "null image pointer");
+    HYB_CHECK(cudaSetDevice(ctx->device));
+    const bool ds = is_device_ptr(src), dd = is_device_ptr(dst);
+    const size_t pp = round_pitch(cols);
+    const uint8_t* s = src;
+    size_t sp = pitch;
+    if (!ds) {
+        HYB_CHECK(ctx->in.ensure(pp * rows));
+        HYB_CHECK(copy2d(ctx, ctx->in.ptr, pp, src, pitch, cols, rows));
+        s = ctx->in.ptr;
+        sp = pp;
+    }
+    uint8_t* d = dst;
+    size_t dp = dst_pitch;
+    if (!dd) {
+        HYB_CHECK(ctx->out.ensure(pp * rows));
+        d = ctx->out.ptr;
+        dp = pp;
+    }
+    HYB_CHECK(ctx->mm.ensure(2 * sizeof(unsigned)));
+    HYB_CHECK(hyb::launch_contrast_stretch(s, sp, rows, cols, d, dp, reinterpret_cast<unsigned*>(ctx->mm.ptr),
+                                           ctx->stream));
+    if (!dd) HYB_CHECK(copy2d(ctx, dst, dst_pitch, d, dp, cols, rows));
+    if (!ds || !dd) HYB_CHECK(cudaStreamSynchronize(ctx->stream));
+    return HYB_OK;
+}
+
+int hyb_hybrid_stretch_u8(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int cols, int smax, int win,
+                          int parts, uint8_t* y, size_t y_pitch, hyb_stats* stats) {
+    if (!ctx) return HYB_EINVAL;
+    int st;
+    if ((st = check_dims(ctx, rows, cols)) || (st = check_pitch(ctx, y_pitch, cols, "y"))) return st;
+    if (!y) return fail(ctx, HYB_EINVAL, "null image pointer");
+    HYB_CHECK(cudaSetDevice(ctx->device));
+    // stages 1-2 into a device buffer, then the final stretch (in place when y is on the device)
+    const bool dy = is_device_ptr(y);
+    const size_t pp = round_pitch(cols);
+    uint8_t* d = y;
+    size_t dp = y_pitch;
+    if (!dy) {
+        HYB_CHECK(ctx->ys.ensure(pp * rows));
+        d = ctx->ys.ptr;
+        dp = pp;
+    }
+    if ((st = hyb_hybrid_u8(ctx, g, pitch, rows, cols, smax, win, parts, d, dp, stats))) return st;
+    HYB_CHECK(ctx->mm.ensure(2 * sizeof(unsigned)));
+    HYB_CHECK(hyb::launch_contrast_stretch(d, dp, rows, cols, d, dp, reinterpret_cast<unsigned*>(ctx->mm.ptr),
+                                           ctx->stream));
+    if (!dy) {
+        HYB_CHECK(copy2d(ctx, y, y_pitch, d, dp, cols, rows));
+        HYB_CHECK(cudaStreamSynchronize(ctx->stream));
     }
     return HYB_OK;
 }

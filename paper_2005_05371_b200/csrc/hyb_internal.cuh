@@ -1,5 +1,6 @@
 // hyb_internal.cuh -- shared declarations of libhybrid_cuda (kernels + launchers).
 #pragma once
+#include <algorithm>
 #include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -83,6 +84,10 @@ struct SmallBufs {
 // otherwise a plain launch whose grid never exceeds the occupancy (caller: exclusive device).
 cudaError_t launch_small(const SmallPlan& pl, const SmallBufs& bufs, int rows, int cols, int smax, int win,
                          bool cooperative, cudaStream_t stream);
+
+// contrast_stretch (stretch.cu): mm = 2 u32 device scratch; src == dst allowed.
+cudaError_t launch_contrast_stretch(const uint8_t* src, size_t spitch, int rows, int cols, uint8_t* dst,
+                                    size_t dpitch, unsigned* mm, cudaStream_t stream);
 
 // Kernel-launch counter (bench evidence), incremented by every launcher.
 void count_launch();

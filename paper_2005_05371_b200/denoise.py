@@ -183,6 +183,33 @@ def hybrid_denoise(noisy, config: FilterConfig, ctx=None) -> HybridResult:
     return HybridResult(y, st.sigma2, st.t_adaptive, st.t_wiener, 0.0, st.noise_sum, st.t_total)
 
 
+def contrast_stretch(image, ctx=None):
+    """contrast_stretch -- reference proj/src/pipeline.cpp:10-21 on uint8 images: (v - lo) / (hi - lo)
+    scaled to 0..255, rounded half up (lo -> 0, hi -> 255); unchanged when the image is constant."""
+    rows, cols = _shape(image)
+    out = _empty_like(image, rows, cols)
+    sp, spitch = capi.buf(image)
+    dp, dpitch = capi.buf(out)
+    c = _ctx(ctx)
+    check(lib.hyb_contrast_stretch_u8(c, sp, spitch, rows, cols, dp, dpitch), c)
+    return out
+
+
+def hybrid_denoise_stretched(noisy, config: FilterConfig, ctx=None) -> HybridResult:
+    """hybrid_denoise stages 1-3 (reference proj/src/pipeline.cpp:23-57, stretch_after_each = false):
+    AMF, W1, then the final contrast_stretch."""
+    validate_config(config)
+    rows, cols = _shape(noisy)
+    y = _empty_like(noisy, rows, cols)
+    gp, gpitch = capi.buf(noisy)
+    yp, ypitch = capi.buf(y)
+    st = capi.HybStats()
+    c = _ctx(ctx)
+    check(lib.hyb_hybrid_stretch_u8(c, gp, gpitch, rows, cols, config.smax, config.wiener_window, config.parts,
+                                    yp, ypitch, ctypes.byref(st)), c)
+    return HybridResult(y, st.sigma2, st.t_adaptive, st.t_wiener, 0.0, st.noise_sum, st.t_total)
+
+
 def hybrid_denoise_batch(stack, smax: int, win: int, ctx=None):
     """CT-stack hybrid: each slice filtered independently (own noise estimate).  Returns
     (filtered stack, per-slice W)."""

@@ -235,3 +235,36 @@ def test_errors_match_reference_text(ctx):
         denoise.adaptive_median_rows(img, 3, 5, 3)
     with pytest.raises(capi.InvalidArgument, match="exceeds image rows"):
         denoise.hybrid_denoise(img, FilterConfig(smax=3, parts=9))
+
+
+# ---------------------------------------------------------------- contrast_stretch
+
+@pytest.mark.parametrize("shape", [(1, 1), (7, 13), (300, 517), (1600, 1600), (33, 4096 + 3)])
+def test_contrast_stretch_vs_oracle(ctx, shape):
+    rng = np.random.default_rng(shape[0] * 7 + shape[1])
+    img = rng.integers(31, 190, size=shape, dtype=np.uint8)
+    np.testing.assert_array_equal(denoise.contrast_stretch(img), oracle.contrast_stretch(img))
+    g = torch.from_numpy(img).cuda()  # device buffers, in place
+    denoise.contrast_stretch(g)
+    capi.check(capi.lib.hyb_contrast_stretch_u8(ctx.ptr, g.data_ptr(), shape[1], shape[0], shape[1], g.data_ptr(),
+                                                shape[1]), ctx.ptr)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(g.cpu().numpy(), oracle.contrast_stretch(img))
+
+
+def test_contrast_stretch_constant_and_strided(ctx):
+    flat = np.full((40, 70), 99, np.uint8)
+    np.testing.assert_array_equal(denoise.contrast_stretch(flat), flat)
+    base = np.random.default_rng(5).integers(0, 256, size=(50, 100), dtype=np.uint8)
+    view = base[3:45, 7:90]  # non-contiguous host view (pitch 100)
+    np.testing.assert_array_equal(denoise.contrast_stretch(view), oracle.contrast_stretch(np.ascontiguousarray(view)))
+
+
+@pytest.mark.parametrize("cfg", [0, 1])
+def test_hybrid_stretched_vs_oracle(ctx, cfg):
+    c = CONFIGS[cfg]
+    g = capi.make_phantom(c["rows"], c["cols"], c["ellipses"], c["sigma"], c["density"], 0)
+    res = denoise.hybrid_denoise_stretched(g, FilterConfig(smax=c["smax"], wiener_window=c["win"]))
+    ref_y, ref_w = oracle.hybrid(g, c["smax"], c["win"])
+    assert res.noise_sum == ref_w
+    np.testing.assert_array_equal(res.image, oracle.contrast_stretch(ref_y))

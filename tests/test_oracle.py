@@ -136,3 +136,48 @@ def test_oracle_wiener_noise_sum_is_partition_invariant():
         whole = oracle.wiener_stats(f, win)
         cuts = [0, 5, 19, 20, 44, 57]
         assert sum(oracle.wiener_stats(f, win, a, b) for a, b in zip(cuts, cuts[1:])) == whole
+
+
+# ---------------------------------------------------------------- contrast_stretch
+
+def _stretch_ref_double(img):
+    """The reference's double formula (proj/src/pipeline.cpp:10-21) on k/255 values."""
+    p = img.astype(np.float64) / 255.0
+    lo, hi = p.min(), p.max()
+    if hi == lo:
+        return p
+    return (p - lo) / (hi - lo)
+
+
+def test_contrast_stretch_kat_range_onto_0_1():
+    # proj/tests/test_pipeline.cpp:29-36 on the k/255 grid: {0.2, 0.4, 0.6, 0.7}
+    img = np.array([[51, 102], [153, 179]], np.uint8)
+    out = oracle.contrast_stretch(img)
+    assert out[0, 0] == 0 and out[1, 1] == 255
+    np.testing.assert_array_equal(out, np.floor(_stretch_ref_double(img) * 255 + 0.5).astype(np.uint8))
+
+
+def test_contrast_stretch_constants_and_full_range_unchanged():
+    # proj/tests/test_pipeline.cpp:38-43
+    flat = np.full((5, 5), 107, np.uint8)
+    np.testing.assert_array_equal(oracle.contrast_stretch(flat), flat)
+    full = np.array([[0, 64, 255]], np.uint8)
+    np.testing.assert_array_equal(oracle.contrast_stretch(full), full)
+
+
+def test_contrast_stretch_endpoints_order_and_rounding():
+    # proj/tests/test_pipeline.cpp:45-57: both endpoints, order preserved; plus: the uint8 value is the
+    # reference's double result scaled by 255 and rounded to nearest (ties: exact rational, half up)
+    rng = np.random.default_rng(321)
+    for lo, hi in ((76, 128), (0, 17), (200, 255), (3, 250)):
+        img = rng.integers(lo, hi + 1, size=(13, 11), dtype=np.uint8)
+        img[0, 0], img[-1, -1] = lo, hi
+        out = oracle.contrast_stretch(img)
+        assert out.min() == 0 and out.max() == 255
+        flat_in, flat_out = img.ravel().astype(int), out.ravel().astype(int)
+        order = np.argsort(flat_in, kind="stable")
+        assert np.all(np.diff(flat_out[order]) >= 0)
+        ref = _stretch_ref_double(img) * 255.0
+        assert np.max(np.abs(out - ref)) <= 0.5 + 1e-9
+        exact = (510 * (img.astype(int) - lo) + (hi - lo)) // (2 * (hi - lo))
+        np.testing.assert_array_equal(out, exact)
