@@ -10,12 +10,13 @@ LIB := $(PKG)/libhybrid_cuda.so
 HOSTLIB := $(PKG)/libdenoise_cuda.so
 CXX ?= g++
 CPPTEST := tests/cpp/test_host
+PGMTEST := tests/cpp/test_pgm
 
-all: $(LIB) $(HOSTLIB) oracle $(CPPTEST)
+all: $(LIB) $(HOSTLIB) oracle $(CPPTEST) $(PGMTEST)
 
 # C++ host driver with the reference's filter API (paper_2005_05371_b200/host/denoise_cuda.hpp)
-$(HOSTLIB): $(PKG)/host/denoise_cuda.cpp $(PKG)/host/denoise_cuda.hpp include/hybrid_cuda.h $(LIB)
-	$(CXX) -std=c++20 -O2 -fPIC -Wall -Wextra -shared -o $@ $(PKG)/host/denoise_cuda.cpp -L$(PKG) -lhybrid_cuda -Wl,-rpath,'$$ORIGIN'
+$(HOSTLIB): $(PKG)/host/denoise_cuda.cpp $(PKG)/host/pgm_io.cpp $(PKG)/host/denoise_cuda.hpp include/hybrid_cuda.h $(LIB)
+	$(CXX) -std=c++20 -O2 -fPIC -Wall -Wextra -shared -o $@ $(PKG)/host/denoise_cuda.cpp $(PKG)/host/pgm_io.cpp -L$(PKG) -lhybrid_cuda -Wl,-rpath,'$$ORIGIN'
 
 # the reference's unit tests re-expressed against the host driver (run by tests/test_cpp_host.py)
 $(CPPTEST): tests/cpp/test_host.cpp oracle/hyb_oracle.c $(HOSTLIB)
@@ -31,11 +32,16 @@ trace: $(PKG)/libhybrid_cuda_trace.so
 $(PKG)/libhybrid_cuda_trace.so: $(SRCS) $(HDRS)
 	$(NVCC) $(NVFLAGS) -DHYB_TRACE -shared -o $@ $(SRCS) 2> /dev/null
 
+# PGM I/O tests (CPU only)
+$(PGMTEST): tests/cpp/test_pgm.cpp $(HOSTLIB)
+	$(CXX) -std=c++20 -O2 -Wall -Wextra -o $@ tests/cpp/test_pgm.cpp -L$(PKG) -ldenoise_cuda -lhybrid_cuda \
+		-Wl,-rpath,'$$ORIGIN/../../$(PKG)'
+
 oracle:
 	$(MAKE) -C oracle --no-print-directory
 
 clean:
-	rm -f $(LIB) $(PKG)/libhybrid_cuda_trace.so $(HOSTLIB) $(CPPTEST) build_ptxas.log
+	rm -f $(LIB) $(PKG)/libhybrid_cuda_trace.so $(HOSTLIB) $(CPPTEST) $(PGMTEST) build_ptxas.log
 	$(MAKE) -C oracle clean
 
 .PHONY: all oracle clean trace

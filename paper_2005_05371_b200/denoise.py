@@ -247,3 +247,100 @@ def to_u8(img: np.ndarray) -> np.ndarray:
 def to_unit(img_u8) -> np.ndarray:
     """uint8 -> the reference's [0, 1] doubles, k/255 (proj/src/pgm_io.cpp:73,88)."""
     return np.asarray(img_u8, np.float64) / 255.0
+
+
+# ---------------------------------------------------------------- PGM I/O (SURVEY.md 8(f) row 2)
+
+def _pgm_error(path, what):
+    raise RuntimeError(f"pgm {path}: {what}")
+
+
+def load_pgm(path):
+    """load_pgm -- reference proj/src/pgm_io.cpp:49-103: P5 or P2, maxval 1..65535.  maxval 255 files
+    return the uint8 raster (exactly the reference's k/255 doubles, ready for the uint8 path); other
+    maxvals return float64 samples / maxval like the reference.  Errors are RuntimeError("pgm <path>:
+    ...") with the reference's texts."""
+    try:
+        data = open(path, "rb").read()
+    except OSError:
+        _pgm_error(path, "cannot open file")
+    if len(data) < 2 or data[0:1] != b"P" or data[1:2] not in (b"2", b"5"):
+        magic = data[:2].decode("latin-1") if len(data) >= 2 else ""
+        _pgm_error(path, f'unsupported magic "{magic}" (want P2 or P5)')
+    binary = data[1:2] == b"5"
+    i = 2
+
+    def skip(i):
+        while i < len(data):
+            c = data[i:i + 1]
+            if c == b"#":
+                while i < len(data) and data[i:i + 1] != b"\n":
+                    i += 1
+            elif c.isspace():
+                i += 1
+            else:
+                break
+        return i
+
+    def number(i):
+        j = i
+        while j < len(data) and data[j:j + 1].isdigit():
+            j += 1
+        return (int(data[i:j]) if j > i else None), j
+
+    fields = []
+    for name in ("width", "height", "maxval"):
+        i = skip(i)
+        v, i = number(i)
+        if v is None:
+            _pgm_error(path, f"malformed header: missing {name}")
+        if v > 1000000000:
+            _pgm_error(path, f"header field out of range: {name}")
+        fields.append(v)
+    cols, rows, maxval = fields
+    if cols < 1 or rows < 1:
+        _pgm_error(path, "non-positive dimensions in header")
+    if maxval < 1 or maxval > 65535:
+        _pgm_error(path, f"maxval {maxval} out of range [1, 65535]")
+    count = rows * cols
+    if binary:
+        if i >= len(data) or not data[i:i + 1].isspace():
+            _pgm_error(path, "missing separator before pixel data")
+        i += 1
+        bps = 2 if maxval > 255 else 1
+        if len(data) - i < count * bps:
+            _pgm_error(path, "truncated pixel data")
+        raw = np.frombuffer(data, dtype=">u2" if bps == 2 else np.uint8, count=count, offset=i).astype(np.int64)
+    else:
+        vals = []
+        for k in range(count):
+            i = skip(i)
+            v, i = number(i)
+            if v is None:
+                _pgm_error(path, f"truncated pixel data at sample {k}")
+            vals.append(v)
+        raw = np.array(vals, dtype=np.int64)
+    bad = raw > maxval
+    if bad.any():
+        _pgm_error(path, f"sample {int(raw[np.argmax(bad)])} exceeds maxval")
+    raw = raw.reshape(rows, cols)
+    return raw.astype(np.uint8) if maxval == 255 else raw / float(maxval)
+
+
+def save_pgm(image, path):
+    """save_pgm -- reference proj/src/pgm_io.cpp:105-120: P5, maxval 255.  uint8 images are written as
+    is; float images in [0, 1] are quantised round(p * 255) with halves away from zero, clipped."""
+    img = np.asarray(image.cpu() if _is_torch(image) else image)
+    if img.dtype == np.uint8:
+        raw = img
+    else:
+        x = img.astype(np.float64) * 255.0
+        raw = np.clip(np.where(x >= 0, np.floor(x + 0.5), np.ceil(x - 0.5)), 0, 255).astype(np.uint8)
+    rows, cols = raw.shape
+    try:
+        with open(path, "wb") as f:
+            f.write(f"P5\n{cols} {rows}\n255\n".encode())
+            f.write(np.ascontiguousarray(raw).tobytes())
+    except OSError:
+        _pgm_error(path, "cannot open file for writing")
+

@@ -12,6 +12,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <filesystem>
 #include <vector>
 
 namespace denoise_cuda {
@@ -91,5 +92,12 @@ HybridResult hybrid_denoise(const Image& noisy, const FilterConfig& config);
 /// uint8 <-> reference doubles (k/255).  to_u8 throws std::invalid_argument off the grid.
 std::vector<uint8_t> to_u8(const Image& image);
 Image from_u8(const uint8_t* px, int rows, int cols);
+
+/// load_pgm / save_pgm -- proj/src/pgm_io.cpp:49-122: P5 or P2, maxval
+/// 1..65535, samples / maxval; writer P5 maxval 255, round half away from zero.  Same error texts
+/// ("pgm <path>: ...", std::runtime_error).  P5/P2 files with maxval 255 load exactly onto the
+/// k/255 grid, i.e. straight into the uint8 path (to_u8).
+Image load_pgm(const std::filesystem::path& path);
+void save_pgm(const Image& image, const std::filesystem::path& path);
 
 }  // namespace denoise_cuda
