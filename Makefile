@@ -4,7 +4,7 @@ NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 -Xptxas -v -cudart static
 PKG := paper_2005_05371_b200
-SRCS := $(PKG)/csrc/tma_host.cu $(PKG)/csrc/amf.cu $(PKG)/csrc/wiener.cu $(PKG)/csrc/small.cu $(PKG)/csrc/stretch.cu $(PKG)/csrc/capi.cu $(PKG)/csrc/phantom.cpp
+SRCS := $(PKG)/csrc/tma_host.cu $(PKG)/csrc/amf.cu $(PKG)/csrc/wiener.cu $(PKG)/csrc/small.cu $(PKG)/csrc/stretch.cu $(PKG)/csrc/freq.cu $(PKG)/csrc/capi.cu $(PKG)/csrc/phantom.cpp
 HDRS := $(PKG)/csrc/hyb_internal.cuh $(PKG)/csrc/tma.cuh $(PKG)/csrc/networks.cuh $(PKG)/csrc/amf_core.cuh $(PKG)/csrc/w1_core.cuh include/hybrid_cuda.h
 LIB := $(PKG)/libhybrid_cuda.so
 HOSTLIB := $(PKG)/libdenoise_cuda.so
@@ -24,13 +24,13 @@ $(CPPTEST): tests/cpp/test_host.cpp oracle/hyb_oracle.c $(HOSTLIB)
 		-L$(PKG) -ldenoise_cuda -lhybrid_cuda -Wl,-rpath,'$$ORIGIN/../../$(PKG)'
 
 $(LIB): $(SRCS) $(HDRS)
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRCS) 2> build_ptxas.log || (cat build_ptxas.log; exit 1)
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRCS) -lcufft -Xlinker -rpath,/usr/local/cuda/lib64 2> build_ptxas.log || (cat build_ptxas.log; exit 1)
 	@grep -E "registers|spill" build_ptxas.log | sed 's/^ptxas info    : //' | head -40
 
 # phase-timestamp build of the same library (tools/trace_amf.py); not used by tests or bench
 trace: $(PKG)/libhybrid_cuda_trace.so
 $(PKG)/libhybrid_cuda_trace.so: $(SRCS) $(HDRS)
-	$(NVCC) $(NVFLAGS) -DHYB_TRACE -shared -o $@ $(SRCS) 2> /dev/null
+	$(NVCC) $(NVFLAGS) -DHYB_TRACE -shared -o $@ $(SRCS) -lcufft -Xlinker -rpath,/usr/local/cuda/lib64 2> /dev/null
 
 # PGM I/O tests (CPU only)
 $(PGMTEST): tests/cpp/test_pgm.cpp $(HOSTLIB)

@@ -132,6 +132,20 @@ int hyb_contrast_stretch_u8(hyb_ctx* ctx, const uint8_t* src, size_t pitch, int 
 int hyb_hybrid_stretch_u8(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int cols, int smax,
                           int win, int parts, uint8_t* y, size_t y_pitch, hyb_stats* stats);
 
+/* The reference's own Wiener stage, doubles like the reference; pitches
+ * in elements; host or device pointers.
+ * wiener_filter proj/src/wiener.cpp:54-77 (+ dft2 proj/src/dft2.cpp:32-56): per-bin gain
+ * (P - N0) / P, N0 = rows * cols * sigma2, zero where noise dominates; output clamped to [0, 1]
+ * when clamp != 0; sigma2 == 0 returns the input; sigma2 < 0 -> HYB_EINVAL. */
+int hyb_wiener_freq_f64(hyb_ctx* ctx, const double* f, size_t pitch, int rows, int cols, double sigma2,
+                        int clamp, double* out, size_t out_pitch);
+/* estimate_noise_variance without a reference, proj/src/wiener.cpp:44-51:
+ * sigma = median(|p - median3(p)|) / 0.6745 (3x3, replicated borders), sigma2 = sigma^2. */
+int hyb_noise_robust_f64(hyb_ctx* ctx, const double* f, size_t pitch, int rows, int cols, double* sigma2);
+/* estimate_noise_variance with a reference, proj/src/wiener.cpp:31-42: mean squared difference. */
+int hyb_noise_reference_f64(hyb_ctx* ctx, const double* f, size_t pitch, const double* ref, size_t ref_pitch,
+                            int rows, int cols, double* sigma2);
+
 /* Synthetic phantom of BASELINE.json's configs (host only, deterministic):
  * background 20, n_ellipses ellipses (full axes 20-200 px, rotation U[0,pi), intensity
  * U[40,220]), +-15 linear gradient along columns, Gaussian sigma (rounded, clipped), then salt &

@@ -61,6 +61,8 @@ struct hyb_ctx {
     DevBuf in, out, fin, f, wsum;      // staging / scratch
     DevBuf sbar;                       // fused small-image kernel: grid-barrier words (zeroed once), stamps
     DevBuf mm, ys;                     // contrast stretch: min / max scratch, staged hybrid output
+    DevBuf fin64, fout64, fref64, fsc;  // frequency Wiener: staged doubles, scalar results
+    hyb::FreqWork freq;
     bool small_used = false;           // the last hybrid call ran the fused kernel
     bool exclusive = false;            // hyb_set_exclusive: plain (non-cooperative) fused launches
     DevBuf amf_q[2], amf_cnt;          // AMF growth workspace (failure bitmap)
@@ -428,6 +430,11 @@ int hyb_destroy(hyb_ctx* ctx) {
     ctx->sbar.release();
     ctx->mm.release();
     ctx->ys.release();
+    ctx->fin64.release();
+    ctx->fout64.release();
+    ctx->fref64.release();
+    ctx->fsc.release();
+    ctx->freq.release();
     for (auto& b : ctx->amf_q) b.release();
     ctx->amf_cnt.release();
     for (auto& b : ctx->strip_g) b.release();
@@ -870,6 +877,95 @@ int hyb_hybrid_stretch_u8(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows
         HYB_CHECK(copy2d(ctx, y, y_pitch, d, dp, cols, rows));
         HYB_CHECK(cudaStreamSynchronize(ctx->stream));
     }
+    return HYB_OK;
+}
+
+// Stages a double image (host or device, pitch in elements) on the device; returns the device view.
+static int stage_f64(hyb_ctx* ctx, DevBuf& buf, const double* src, size_t pitch, int rows, int cols,
+                     const double** dev, size_t* dpitch) {
+    if (is_device_ptr(src)) {
+        *dev = src;
+        *dpitch = pitch;
+        return HYB_OK;
+    }
+    HYB_CHECK(buf.ensure((size_t)rows * cols * sizeof(double)));
+    HYB_CHECK(cudaMemcpy2DAsync(buf.ptr, (size_t)cols * sizeof(double), src, pitch * sizeof(double),
+                                (size_t)cols * sizeof(double), (size_t)rows, cudaMemcpyDefault, ctx->stream));
+    *dev = reinterpret_cast<const double*>(buf.ptr);
+    *dpitch = (size_t)cols;
+    return HYB_OK;
+}
+
+int hyb_wiener_freq_f64(hyb_ctx* ctx, const double* f, size_t pitch, int rows, int cols, double sigma2, int clamp,
+                        double* out, size_t out_pitch) {
+    if (!ctx) return HYB_EINVAL;
+    int st;
+    if ((st = check_dims(ctx, rows, cols))) return st;
+    if (pitch < (size_t)cols || out_pitch < (size_t)cols) return fail(ctx, HYB_EINVAL, "pitch smaller than cols");
+    if (!f || !out) return fail(ctx, HYB_EINVAL, "null image pointer");
+    if (!(sigma2 >= 0.0)) return fail(ctx, HYB_EINVAL, "noise variance must be nonnegative");
+    HYB_CHECK(cudaSetDevice(ctx->device));
+    const double* s = nullptr;
+    size_t sp = 0;
+    if ((st = stage_f64(ctx, ctx->fin64, f, pitch, rows, cols, &s, &sp))) return st;
+    const bool dout = is_device_ptr(out);
+    double* d = out;
+    size_t dp = out_pitch;
+    if (!dout) {
+        HYB_CHECK(ctx->fout64.ensure((size_t)rows * cols * sizeof(double)));
+        d = reinterpret_cast<double*>(ctx->fout64.ptr);
+        dp = (size_t)cols;
+    }
+    int cst = 0;
+    HYB_CHECK(hyb::launch_wiener_freq(s, sp, rows, cols, sigma2, clamp != 0, d, dp, ctx->freq, ctx->stream, &cst));
+    if (cst) return fail(ctx, HYB_ECUDA, "cuFFT error " + std::to_string(cst));
+    if (!dout)
+        HYB_CHECK(cudaMemcpy2DAsync(out, out_pitch * sizeof(double), d, dp * sizeof(double),
+                                    (size_t)cols * sizeof(double), (size_t)rows, cudaMemcpyDefault, ctx->stream));
+    if (!dout || !is_device_ptr(f)) HYB_CHECK(cudaStreamSynchronize(ctx->stream));
+    return HYB_OK;
+}
+
+int hyb_noise_robust_f64(hyb_ctx* ctx, const double* f, size_t pitch, int rows, int cols, double* sigma2) {
+    if (!ctx) return HYB_EINVAL;
+    int st;
+    if ((st = check_dims(ctx, rows, cols))) return st;
+    if (pitch < (size_t)cols) return fail(ctx, HYB_EINVAL, "pitch smaller than cols");
+    if (!f || !sigma2) return fail(ctx, HYB_EINVAL, "null pointer");
+    HYB_CHECK(cudaSetDevice(ctx->device));
+    const double* s = nullptr;
+    size_t sp = 0;
+    if ((st = stage_f64(ctx, ctx->fin64, f, pitch, rows, cols, &s, &sp))) return st;
+    HYB_CHECK(ctx->fsc.ensure(sizeof(double)));
+    double* dm = reinterpret_cast<double*>(ctx->fsc.ptr);
+    HYB_CHECK(hyb::launch_noise_robust(s, sp, rows, cols, ctx->freq, dm, ctx->stream));
+    double med = 0.0;
+    HYB_CHECK(cudaMemcpyAsync(&med, dm, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    HYB_CHECK(cudaStreamSynchronize(ctx->stream));
+    const double sigma = med / 0.6745;
+    *sigma2 = sigma * sigma;
+    return HYB_OK;
+}
+
+int hyb_noise_reference_f64(hyb_ctx* ctx, const double* f, size_t pitch, const double* ref, size_t ref_pitch,
+                            int rows, int cols, double* sigma2) {
+    if (!ctx) return HYB_EINVAL;
+    int st;
+    if ((st = check_dims(ctx, rows, cols))) return st;
+    if (pitch < (size_t)cols || ref_pitch < (size_t)cols) return fail(ctx, HYB_EINVAL, "pitch smaller than cols");
+    if (!f || !ref || !sigma2) return fail(ctx, HYB_EINVAL, "null pointer");
+    HYB_CHECK(cudaSetDevice(ctx->device));
+    const double *a = nullptr, *b = nullptr;
+    size_t ap = 0, bp = 0;
+    if ((st = stage_f64(ctx, ctx->fin64, f, pitch, rows, cols, &a, &ap))) return st;
+    if ((st = stage_f64(ctx, ctx->fref64, ref, ref_pitch, rows, cols, &b, &bp))) return st;
+    HYB_CHECK(ctx->fsc.ensure(sizeof(double)));
+    double* acc = reinterpret_cast<double*>(ctx->fsc.ptr);
+    HYB_CHECK(hyb::launch_noise_reference(a, ap, b, bp, rows, cols, acc, ctx->stream));
+    double sum = 0.0;
+    HYB_CHECK(cudaMemcpyAsync(&sum, acc, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    HYB_CHECK(cudaStreamSynchronize(ctx->stream));
+    *sigma2 = sum / ((double)rows * cols);
     return HYB_OK;
 }
 

@@ -89,6 +89,28 @@ cudaError_t launch_small(const SmallPlan& pl, const SmallBufs& bufs, int rows, i
 cudaError_t launch_contrast_stretch(const uint8_t* src, size_t spitch, int rows, int cols, uint8_t* dst,
                                     size_t dpitch, unsigned* mm, cudaStream_t stream);
 
+// Frequency-domain Wiener + noise estimates (freq.cu, doubles like the reference).
+struct FreqWork {
+    unsigned long long plan_f = 0, plan_i = 0;  // cufftHandle
+    int rows = 0, cols = 0;
+    double* real = nullptr;
+    void* bins = nullptr;  // double2 (Hermitian half)
+    double* keys = nullptr;
+    void* tmp = nullptr;   // CUB scratch
+    size_t real_n = 0, bins_n = 0, keys_n = 0, tmp_n = 0;
+    ~FreqWork();
+    void release();
+};
+// pitches in elements; cufft_status != 0 reports a cuFFT failure
+cudaError_t launch_wiener_freq(const double* in, size_t ipitch, int rows, int cols, double sigma2, bool clamp,
+                               double* out, size_t opitch, FreqWork& w, cudaStream_t stream, int* cufft_status);
+// d_sigma_med <- median(|p - median3(p)|) (device double)
+cudaError_t launch_noise_robust(const double* in, size_t ipitch, int rows, int cols, FreqWork& w, double* d_sigma_med,
+                                cudaStream_t stream);
+// d_acc <- sum (a - b)^2 (device double)
+cudaError_t launch_noise_reference(const double* a, size_t ap, const double* b, size_t bp, int rows, int cols,
+                                   double* d_acc, cudaStream_t stream);
+
 // Kernel-launch counter (bench evidence), incremented by every launcher.
 void count_launch();
 

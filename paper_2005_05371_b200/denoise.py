@@ -344,3 +344,50 @@ def save_pgm(image, path):
     except OSError:
         _pgm_error(path, "cannot open file for writing")
 
+
+# ---------------------------------------------------------------- the reference's Wiener stage (8(f) row 3)
+
+def _f64(img):
+    """(pointer, pitch in elements, rows, cols) of a float64 numpy array / torch tensor (2-D)."""
+    if _is_torch(img):
+        import torch
+        if img.dtype != torch.float64 or img.dim() != 2 or img.stride(1) != 1:
+            raise InvalidArgument("expected a 2-D float64 tensor with unit column stride")
+        return img.data_ptr(), img.stride(0), int(img.shape[0]), int(img.shape[1])
+    a = np.asarray(img)
+    if a.dtype != np.float64 or a.ndim != 2 or a.strides[1] != 8:
+        raise InvalidArgument("expected a 2-D float64 array with unit column stride")
+    return a.ctypes.data, a.strides[0] // 8, a.shape[0], a.shape[1]
+
+
+def wiener_filter(image, sigma2: float, clamp: bool = True, ctx=None):
+    """wiener_filter -- reference proj/src/wiener.cpp:54-77: frequency-domain Wiener on a float64
+    image (per-bin gain (P - N0) / P, N0 = rows * cols * sigma2), clamped to [0, 1] by default."""
+    p, pitch, rows, cols = _f64(image)
+    if _is_torch(image):
+        import torch
+        out = torch.empty((rows, cols), dtype=torch.float64, device=image.device)
+        op, opitch = out.data_ptr(), cols
+    else:
+        out = np.empty((rows, cols), np.float64)
+        op, opitch = out.ctypes.data, cols
+    c = _ctx(ctx)
+    check(lib.hyb_wiener_freq_f64(c, p, pitch, rows, cols, float(sigma2), int(bool(clamp)), op, opitch), c)
+    return out
+
+
+def estimate_noise_variance(image, reference=None, ctx=None):
+    """estimate_noise_variance -- reference proj/src/wiener.cpp:30-52 on float64 images: with a reference
+    the mean squared difference, else (median |p - median3(p)| / 0.6745)^2.  Returns (sigma2, source)."""
+    p, pitch, rows, cols = _f64(image)
+    c = _ctx(ctx)
+    out = ctypes.c_double(0.0)
+    if reference is not None:
+        rp, rpitch, rr, rc = _f64(reference)
+        if (rr, rc) != (rows, cols):
+            raise InvalidArgument("reference image dimensions do not match")
+        check(lib.hyb_noise_reference_f64(c, p, pitch, rp, rpitch, rows, cols, ctypes.byref(out)), c)
+        return out.value, "reference"
+    check(lib.hyb_noise_robust_f64(c, p, pitch, rows, cols, ctypes.byref(out)), c)
+    return out.value, "robust"
+
