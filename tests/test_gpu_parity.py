@@ -268,3 +268,23 @@ def test_hybrid_stretched_vs_oracle(ctx, cfg):
     ref_y, ref_w = oracle.hybrid(g, c["smax"], c["win"])
     assert res.noise_sum == ref_w
     np.testing.assert_array_equal(res.image, oracle.contrast_stretch(ref_y))
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (1, 300), (300, 1), (2, 2), (33, 129), (127, 255), (64, 64)])
+@pytest.mark.parametrize("smax,win", [(3, 1), (5, 3), (7, 5), (11, 7), (13, 3), (7, 9)])
+def test_hybrid_small_shapes_vs_oracle(ctx, shape, smax, win):
+    # small images take the fused single-kernel path (smax <= 11, win <= 7) or the separate kernels
+    # otherwise; both must equal the oracle, including degenerate 1-pixel-wide images
+    rng = np.random.default_rng(shape[0] * 1000 + shape[1] + smax * 7 + win)
+    g = rng.integers(0, 256, size=shape, dtype=np.uint8)
+    g[rng.random(shape) < 0.25] = 0
+    res = denoise.hybrid_denoise(g, FilterConfig(smax=smax, wiener_window=win))
+    ref_y, ref_w = oracle.hybrid(g, smax, win)
+    assert res.noise_sum == ref_w
+    np.testing.assert_array_equal(res.image, ref_y)
+    gd = torch.from_numpy(g).cuda()
+    yd = torch.empty_like(gd)
+    capi.check(capi.lib.hyb_hybrid_u8(ctx.ptr, gd.data_ptr(), shape[1], shape[0], shape[1], smax, win, 1,
+                                      yd.data_ptr(), shape[1], None), ctx.ptr)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(yd.cpu().numpy(), ref_y)
