@@ -31,14 +31,28 @@ METRIC = "MPix/s for hybrid AMF+Wiener (uint8) at 1/2/4/8 B200; % of roofline"
 L2_BYTES = 126 * 1024 * 1024
 
 
-def load_traffic(cfg):
-    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum from one ncu --set full capture,
-    summed over a stage's kernels) committed under profiles/ -- measured once, reported beside `achieved`."""
+def load_counters(cfg):
+    """Per-launch ncu counters committed under profiles/ (profiles/ncu_counters.json, from one
+    ncu --set full capture per config): DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) and
+    warp instructions (smsp__inst_executed.sum) of each stage -- measured once, reported beside the
+    live timings (`traffic`, and the instruction-issue roofline)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "ncu_counters.json")) as f:
             return json.load(f).get(f"config{cfg}", {})
     except Exception:
         return {}
+
+
+def issue_roofline(kernel, counters, ms, sm_mhz):
+    """Warp-instruction issue rate of a stage vs the B200 peak (148 SMs x 4 schedulers x 1 / clk)."""
+    c = counters.get(kernel)
+    if not c or not ms or not sm_mhz:
+        return None
+    ach = c["warp_instr"] / (ms * 1e-3) / 1e9
+    peak = 148 * 4 * sm_mhz * 1e6 / 1e9
+    return {"bound": "issue", "kernel": kernel, "achieved": round(ach, 1), "peak": round(peak, 1),
+            "unit": "G warp-instr/s", "frac": round(ach / peak, 4),
+            "source": "warp instructions per launch from profiles/ncu_counters.json, duration live"}
 
 
 def peaks():
@@ -346,7 +360,8 @@ def run_gpu(args, cfg, c):
     # ---------------- roofline of the dominant kernel ----------------
     roofline = None
     fused = world == 1 and launches == args.steps  # one kernel per step: the fused small-image kernel
-    traffic = load_traffic(cfg)
+    counters = load_counters(cfg)
+    traffic = {k: v.get("dram_bytes") for k, v in counters.items()}
     if fused:
         # the whole step is one launch; its algorithmic bytes are the hybrid's 4 B/px
         ach = 4 * px_total / (ms_step * 1e-3) / 1e9
@@ -374,6 +389,16 @@ def run_gpu(args, cfg, c):
                     "step_achieved": round(4 * px_total / (ms_step * 1e-3) / 1e9, 1),
                     "step_frac": round(4 * px_total / (ms_step * 1e-3) / 1e9 / hbm, 4),
                     "kernel_ms": kern}
+    # instruction-issue roofline (the north_star's second binding roofline: integer issue rate)
+    issue = None
+    sm_mhz = clk.report().get("sm_mhz")
+    if fused:
+        issue = issue_roofline("hybrid_small_kernel", counters, ms_step, sm_mhz)
+    elif kern:
+        issue = issue_roofline("amf", counters, kern["amf_ms"], sm_mhz)
+        w_issue = issue_roofline("wiener", counters, kern.get("wiener_ms"), sm_mhz)
+        if issue and w_issue:
+            issue["wiener"] = {k: w_issue[k] for k in ("achieved", "frac")}
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -386,7 +411,7 @@ def run_gpu(args, cfg, c):
         "metric": METRIC, "value": round(value, 3), "unit": "MPix/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True,
         "scaling": "weak" if slices > 1 else "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": workload(cfg, c, world, not args.shared_gpu), "clocks": clk.report(), "e2e": e2e, "gpu_launches": int(launches),
+        "config": workload(cfg, c, world, not args.shared_gpu), "clocks": clk.report(), "e2e": e2e, "gpu_launches": int(launches), "issue_roofline": issue,
         "roofline": roofline, "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)
