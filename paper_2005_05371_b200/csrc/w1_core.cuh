@@ -85,6 +85,32 @@ __device__ __forceinline__ int win_count(int r, int lo, int hi, int n, int RW) {
     return cnt;
 }
 
+// Packed f32x2 arithmetic (FFMA2 / FADD2 on sm_100a): two pixels per instruction.
+__device__ __forceinline__ uint64_t f2pack(float a, float b) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ uint64_t f2splat(float a) { return f2pack(a, a); }
+__device__ __forceinline__ void f2unpack(uint64_t v, float& a, float& b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ uint64_t fadd2_rd(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("add.rm.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+
 // Statistics of one tile: this lane's share of n * sum S2 - sum S1^2 over the tile's output pixels
 // (two's complement; the warp / grid sum is W).
 template <int RW, int FH>
@@ -229,35 +255,53 @@ __device__ __forceinline__ void w1_tile_gain(const uint8_t* __restrict__ T, int 
         const uint32_t own = *(base + (y + RW) * (FBS / 4) + 1);  // f of the 4 output pixels
         uint32_t out = 0;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const uint32_t f = (own >> (8 * i)) & 0xFFu;
-            const uint32_t S1 = s1[i];
-            const int V = (int)(NN * s2[i] - S1 * S1);
-            const int d = (int)(NN * f) - (int)S1;  // n (f - mu), |d| <= 49 * 255 < 2^14
-            // y + 1/2 = (S1 + g d) / n + 1/2, g = max(0, 1 - (W/P) / V): one FFMA chain, exponent-trick
-            // conversions; within 2^-11 of a rounding boundary the exact integer test decides.
-            const float s1f = __int_as_float(0x4B000000 | S1) - 8388608.0f;
-            const float df = __int_as_float(0x4B000000 + d + 16384) - 8404992.0f;
-            float rv;
-            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rv) : "f"((float)V));
-            const float gg = fmaxf(0.0f, 1.0f - k.kq * rv);
-            const float hh = fmaf(fmaf(gg, df, s1f), inv_n, 0.5f);
-            const int hb = __float_as_int(__fadd_rd(hh, 12582912.0f));  // floor in the mantissa
-            const float fr = hh - (__int_as_float(hb) - 12582912.0f);
-            int q = hb - 0x4B400000;
-            if (fabsf(fr - 0.5f) > 0.5f - kTieEps) {
-                if (V <= k.wq32) {
-                    q = (int)((2u * S1 + NN) / (2u * NN));  // v <= nu: y = mu, half up
-                } else {
-                    // y >= m - 1/2  <=>  (2 (f - m) + 1) n V P >= 2 D W
-                    const int m = fr < 0.5f ? q : q + 1;
-                    const __int128 Q = (__int128)((long long)NN * V) * k.pixel_count;
-                    const __int128 lhs = (__int128)(2 * ((int)f - m) + 1) * Q;
-                    const __int128 rhs = (__int128)(2 * (long long)d) * k.W;
-                    q = lhs >= rhs ? m : m - 1;
-                }
+        for (int h = 0; h < 2; ++h) {  // pixels (2h, 2h + 1): the float chain runs as packed f32x2 ops
+            int S1[2], V[2], d[2];
+            uint32_t f[2];
+            float rv[2];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int i = 2 * h + j;
+                f[j] = (own >> (8 * i)) & 0xFFu;
+                S1[j] = (int)s1[i];
+                V[j] = (int)(NN * s2[i] - s1[i] * s1[i]);
+                d[j] = (int)(NN * f[j]) - S1[j];  // n (f - mu), |d| <= 49 * 255 < 2^14
+                asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rv[j]) : "f"((float)V[j]));
             }
-            out |= (uint32_t)q << (8 * i);  // y in [min(mu, f), max(mu, f)] -> 0..255
+            // y + 1/2 = (S1 + g d) / n + 1/2, g = max(0, 1 - (W/P) / V): exponent-trick conversions, one
+            // FFMA chain; within 2^-11 of a rounding boundary the exact integer test decides.
+            const uint64_t s1f = fadd2(f2pack(__int_as_float(0x4B000000 | S1[0]), __int_as_float(0x4B000000 | S1[1])),
+                                       f2splat(-8388608.0f));
+            const uint64_t df = fadd2(f2pack(__int_as_float(0x4B000000 + d[0] + 16384),
+                                             __int_as_float(0x4B000000 + d[1] + 16384)),
+                                      f2splat(-8404992.0f));
+            float t0, t1;
+            f2unpack(ffma2(f2splat(-k.kq), f2pack(rv[0], rv[1]), f2splat(1.0f)), t0, t1);
+            const uint64_t gg = f2pack(fmaxf(0.0f, t0), fmaxf(0.0f, t1));
+            const uint64_t hh = ffma2(ffma2(gg, df, s1f), f2splat(inv_n), f2splat(0.5f));
+            const uint64_t hb = fadd2_rd(hh, f2splat(12582912.0f));  // floor in the mantissa
+            const uint64_t fr = ffma2(fadd2(hb, f2splat(-12582912.0f)), f2splat(-1.0f), hh);
+            float frj[2], hbf[2], tie[2];
+            f2unpack(fr, frj[0], frj[1]);
+            f2unpack(hb, hbf[0], hbf[1]);
+            f2unpack(fadd2(fr, f2splat(-0.5f)), tie[0], tie[1]);
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                int q = __float_as_int(hbf[j]) - 0x4B400000;
+                if (fabsf(tie[j]) > 0.5f - kTieEps) {
+                    if (V[j] <= k.wq32) {
+                        q = (int)((2u * (uint32_t)S1[j] + NN) / (2u * NN));  // v <= nu: y = mu, half up
+                    } else {
+                        // y >= m - 1/2  <=>  (2 (f - m) + 1) n V P >= 2 D W
+                        const int m = frj[j] < 0.5f ? q : q + 1;
+                        const __int128 Q = (__int128)((long long)NN * V[j]) * k.pixel_count;
+                        const __int128 lhs = (__int128)(2 * ((int)f[j] - m) + 1) * Q;
+                        const __int128 rhs = (__int128)(2 * (long long)d[j]) * k.W;
+                        q = lhs >= rhs ? m : m - 1;
+                    }
+                }
+                out |= (uint32_t)q << (8 * (2 * h + j));  // y in [min(mu, f), max(mu, f)] -> 0..255
+            }
         }
         if (y < row_lim) {
             if (vec_store) {
