@@ -196,11 +196,17 @@ __global__ void __launch_bounds__(SNT, 3) hybrid_small_kernel(const __grid_const
     cta_replicate_edges(slots, a.slot_bytes, nt, org, FBS, FROWS, a.rows, a.cols, RW);
     TRACE(0, 8);
     unsigned long long vsum = 0;
+    uint32_t* sums = reinterpret_cast<uint32_t*>(Q0);  // [STPC][32][128] packed S1 | S2 << 12 (RW == 1)
     for (int j = warp; j < nt * (TH / SFH); j += NW) {
         const int i = j / (TH / SFH), k = j % (TH / SFH);
         const uint8_t* T = slots + (size_t)i * a.slot_bytes + (size_t)k * SFH * FBS;
         const int y0 = tinfo[2 * i + 1] + k * SFH;
-        if (y0 < a.rows) vsum += (unsigned long long)w1_tile_stats<RW, SFH>(T, tinfo[2 * i], y0, a.rows, a.cols, 0, a.rows);
+        if (y0 >= a.rows) continue;
+        if constexpr (RW == 1)
+            vsum += (unsigned long long)w1_tile_sums3<SFH>(T, a.cols - tinfo[2 * i], a.rows - y0,
+                                                           sums + ((size_t)i * TH + k * SFH) * FW);
+        else
+            vsum += (unsigned long long)w1_tile_stats<RW, SFH>(T, tinfo[2 * i], y0, a.rows, a.cols, 0, a.rows);
     }
     TRACE(0, 9);
 #pragma unroll
@@ -221,7 +227,11 @@ __global__ void __launch_bounds__(SNT, 3) hybrid_small_kernel(const __grid_const
         const int i = j / (TH / SFH), k = j % (TH / SFH);
         const uint8_t* T = slots + (size_t)i * a.slot_bytes + (size_t)k * SFH * FBS;
         const int x0 = tinfo[2 * i], y0 = tinfo[2 * i + 1] + k * SFH;
-        if (y0 < a.rows)
+        if (y0 >= a.rows) continue;
+        if constexpr (RW == 1)
+            w1_tile_gain3<SFH>(T, sums + ((size_t)i * TH + k * SFH) * FW, a.cols - x0, a.rows - y0, kg,
+                               a.y + (size_t)y0 * a.ypitch + x0, a.ypitch);
+        else
             w1_tile_gain<RW, SFH>(T, x0, a.cols - x0, a.rows - y0, kg, a.y + (size_t)y0 * a.ypitch + x0, a.ypitch);
     }
     __syncthreads();

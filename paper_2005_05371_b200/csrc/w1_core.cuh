@@ -217,6 +217,64 @@ __device__ __forceinline__ W1Gain w1_gain_consts(long long W, long long pixel_co
     return k;
 }
 
+// y of the 4 pixels of a lane from their window sums (S1, S2) and f (bytes of own): the float chain
+// as packed f32x2 pairs; exact fix-up near rounding boundaries.
+template <int NN>
+__device__ __forceinline__ uint32_t w1_gain4(const W1Gain& k, uint32_t own, const uint32_t (&s1)[4],
+                                             const uint32_t (&s2)[4], float inv_n) {
+    uint32_t out = 0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {  // pixels (2h, 2h + 1): the float chain runs as packed f32x2 ops
+        int S1[2], V[2], d[2];
+        uint32_t f[2];
+        float rv[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int i = 2 * h + j;
+            f[j] = (own >> (8 * i)) & 0xFFu;
+            S1[j] = (int)s1[i];
+            V[j] = (int)(NN * s2[i] - s1[i] * s1[i]);
+            d[j] = (int)(NN * f[j]) - S1[j];  // n (f - mu), |d| <= 49 * 255 < 2^14
+            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rv[j]) : "f"((float)V[j]));
+        }
+        // y + 1/2 = (S1 + g d) / n + 1/2, g = max(0, 1 - (W/P) / V): exponent-trick conversions, one
+        // FFMA chain; within 2^-11 of a rounding boundary the exact integer test decides.
+        const uint64_t s1f = fadd2(f2pack(__int_as_float(0x4B000000 | S1[0]), __int_as_float(0x4B000000 | S1[1])),
+                                   f2splat(-8388608.0f));
+        const uint64_t df = fadd2(f2pack(__int_as_float(0x4B000000 + d[0] + 16384),
+                                         __int_as_float(0x4B000000 + d[1] + 16384)),
+                                  f2splat(-8404992.0f));
+        float t0, t1;
+        f2unpack(ffma2(f2splat(-k.kq), f2pack(rv[0], rv[1]), f2splat(1.0f)), t0, t1);
+        const uint64_t gg = f2pack(fmaxf(0.0f, t0), fmaxf(0.0f, t1));
+        const uint64_t hh = ffma2(ffma2(gg, df, s1f), f2splat(inv_n), f2splat(0.5f));
+        const uint64_t hb = fadd2_rd(hh, f2splat(12582912.0f));  // floor in the mantissa
+        const uint64_t fr = ffma2(fadd2(hb, f2splat(-12582912.0f)), f2splat(-1.0f), hh);
+        float frj[2], hbf[2], tie[2];
+        f2unpack(fr, frj[0], frj[1]);
+        f2unpack(hb, hbf[0], hbf[1]);
+        f2unpack(fadd2(fr, f2splat(-0.5f)), tie[0], tie[1]);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            int q = __float_as_int(hbf[j]) - 0x4B400000;
+            if (fabsf(tie[j]) > 0.5f - kTieEps) {
+                if (V[j] <= k.wq32) {
+                    q = (int)((2u * (uint32_t)S1[j] + NN) / (2u * NN));  // v <= nu: y = mu, half up
+                } else {
+                    // y >= m - 1/2  <=>  (2 (f - m) + 1) n V P >= 2 D W
+                    const int m = frj[j] < 0.5f ? q : q + 1;
+                    const __int128 Q = (__int128)((long long)NN * V[j]) * k.pixel_count;
+                    const __int128 lhs = (__int128)(2 * ((int)f[j] - m) + 1) * Q;
+                    const __int128 rhs = (__int128)(2 * (long long)d[j]) * k.W;
+                    q = lhs >= rhs ? m : m - 1;
+                }
+            }
+            out |= (uint32_t)q << (8 * (2 * h + j));  // y in [min(mu, f), max(mu, f)] -> 0..255
+        }
+    }
+    return out;
+}
+
 // Gain of one tile: y for the tile's output pixels (rows < row_lim, columns < col_lim) through
 // dst_tile (image row y0, column x0).
 template <int RW, int FH>
@@ -253,56 +311,7 @@ __device__ __forceinline__ void w1_tile_gain(const uint8_t* __restrict__ T, int 
     for (int y = 0; y < FH; ++y) {
         add_row(y + N - 1, false);  // window of output row y = tile rows y .. y + N - 1
         const uint32_t own = *(base + (y + RW) * (FBS / 4) + 1);  // f of the 4 output pixels
-        uint32_t out = 0;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {  // pixels (2h, 2h + 1): the float chain runs as packed f32x2 ops
-            int S1[2], V[2], d[2];
-            uint32_t f[2];
-            float rv[2];
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                const int i = 2 * h + j;
-                f[j] = (own >> (8 * i)) & 0xFFu;
-                S1[j] = (int)s1[i];
-                V[j] = (int)(NN * s2[i] - s1[i] * s1[i]);
-                d[j] = (int)(NN * f[j]) - S1[j];  // n (f - mu), |d| <= 49 * 255 < 2^14
-                asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rv[j]) : "f"((float)V[j]));
-            }
-            // y + 1/2 = (S1 + g d) / n + 1/2, g = max(0, 1 - (W/P) / V): exponent-trick conversions, one
-            // FFMA chain; within 2^-11 of a rounding boundary the exact integer test decides.
-            const uint64_t s1f = fadd2(f2pack(__int_as_float(0x4B000000 | S1[0]), __int_as_float(0x4B000000 | S1[1])),
-                                       f2splat(-8388608.0f));
-            const uint64_t df = fadd2(f2pack(__int_as_float(0x4B000000 + d[0] + 16384),
-                                             __int_as_float(0x4B000000 + d[1] + 16384)),
-                                      f2splat(-8404992.0f));
-            float t0, t1;
-            f2unpack(ffma2(f2splat(-k.kq), f2pack(rv[0], rv[1]), f2splat(1.0f)), t0, t1);
-            const uint64_t gg = f2pack(fmaxf(0.0f, t0), fmaxf(0.0f, t1));
-            const uint64_t hh = ffma2(ffma2(gg, df, s1f), f2splat(inv_n), f2splat(0.5f));
-            const uint64_t hb = fadd2_rd(hh, f2splat(12582912.0f));  // floor in the mantissa
-            const uint64_t fr = ffma2(fadd2(hb, f2splat(-12582912.0f)), f2splat(-1.0f), hh);
-            float frj[2], hbf[2], tie[2];
-            f2unpack(fr, frj[0], frj[1]);
-            f2unpack(hb, hbf[0], hbf[1]);
-            f2unpack(fadd2(fr, f2splat(-0.5f)), tie[0], tie[1]);
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                int q = __float_as_int(hbf[j]) - 0x4B400000;
-                if (fabsf(tie[j]) > 0.5f - kTieEps) {
-                    if (V[j] <= k.wq32) {
-                        q = (int)((2u * (uint32_t)S1[j] + NN) / (2u * NN));  // v <= nu: y = mu, half up
-                    } else {
-                        // y >= m - 1/2  <=>  (2 (f - m) + 1) n V P >= 2 D W
-                        const int m = frj[j] < 0.5f ? q : q + 1;
-                        const __int128 Q = (__int128)((long long)NN * V[j]) * k.pixel_count;
-                        const __int128 lhs = (__int128)(2 * ((int)f[j] - m) + 1) * Q;
-                        const __int128 rhs = (__int128)(2 * (long long)d[j]) * k.W;
-                        q = lhs >= rhs ? m : m - 1;
-                    }
-                }
-                out |= (uint32_t)q << (8 * (2 * h + j));  // y in [min(mu, f), max(mu, f)] -> 0..255
-            }
-        }
+        const uint32_t out = w1_gain4<NN>(k, own, s1, s2, inv_n);
         if (y < row_lim) {
             if (vec_store) {
                 *reinterpret_cast<uint32_t*>(drow) = out;
@@ -314,6 +323,85 @@ __device__ __forceinline__ void w1_tile_gain(const uint8_t* __restrict__ T, int 
         }
         drow += dpitch;
         add_row(y, true);  // drop tile row y
+    }
+}
+
+// 3 x 3 windows, statistics and gain sharing one box-sum pass (fused small-image kernel): the
+// statistics pass stores each pixel's S1 (<= 2295, 12 bits) and S2 (<= 585225, 20 bits) packed in one
+// word, sums[y * 128 + column], and returns this lane's share of sum V over the valid pixels; the gain
+// pass reads them back instead of recomputing the box sums.
+template <int FH>
+__device__ __forceinline__ long long w1_tile_sums3(const uint8_t* __restrict__ T, int col_lim, int row_lim,
+                                                   uint32_t* __restrict__ sums) {
+    constexpr int RW = 1, N = 3, NN = 9;
+    const int lane = threadIdx.x & 31;
+    const int c = 4 * lane;
+    const uint32_t* base = reinterpret_cast<const uint32_t*>(T + FCP + c - 4);
+    uint32_t s1[4] = {0, 0, 0, 0}, s2[4] = {0, 0, 0, 0};
+    auto add_row = [&](int rr, bool sub) {
+        const uint32_t* rp = base + rr * (FBS / 4);
+        const uint32_t w0 = rp[0], w1 = rp[1], w2 = rp[2];
+        uint32_t h1[4], h2[4];
+        hsums<RW, 0>(w0, w1, w2, h1[0], h2[0]);
+        hsums<RW, 1>(w0, w1, w2, h1[1], h2[1]);
+        hsums<RW, 2>(w0, w1, w2, h1[2], h2[2]);
+        hsums<RW, 3>(w0, w1, w2, h1[3], h2[3]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            s1[i] = sub ? s1[i] - h1[i] : s1[i] + h1[i];
+            s2[i] = sub ? s2[i] - h2[i] : s2[i] + h2[i];
+        }
+    };
+#pragma unroll
+    for (int rr = 0; rr < N - 1; ++rr) add_row(rr, false);
+    long long vsum = 0;
+#pragma unroll 1
+    for (int y = 0; y < FH; ++y) {
+        add_row(y + N - 1, false);
+        uint4 pk;
+        pk.x = s1[0] | (s2[0] << 12);
+        pk.y = s1[1] | (s2[1] << 12);
+        pk.z = s1[2] | (s2[2] << 12);
+        pk.w = s1[3] | (s2[3] << 12);
+        *reinterpret_cast<uint4*>(sums + y * FW + c) = pk;
+        if (y < row_lim) {
+            int v = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                if (c + i < col_lim) v += (int)(NN * s2[i] - s1[i] * s1[i]);  // <= 4 * 9 * 585225 < 2^31
+            vsum += v;
+        }
+        add_row(y, true);
+    }
+    return vsum;
+}
+
+template <int FH>
+__device__ __forceinline__ void w1_tile_gain3(const uint8_t* __restrict__ T, const uint32_t* __restrict__ sums,
+                                              int col_lim, int row_lim, const W1Gain& k, uint8_t* dst_tile,
+                                              size_t dpitch) {
+    constexpr int RW = 1;
+    const int lane = threadIdx.x & 31;
+    const int c = 4 * lane;
+    const uint32_t* base = reinterpret_cast<const uint32_t*>(T + FCP + c - 4);
+    uint8_t* drow = dst_tile + c;
+    const bool vec_store = c + 4 <= col_lim && ((reinterpret_cast<uintptr_t>(drow) & 3) == 0) && (dpitch & 3) == 0;
+    const float inv_n = 1.0f / 9.0f;
+#pragma unroll 1
+    for (int y = 0; y < FH && y < row_lim; ++y) {
+        const uint4 pk = *reinterpret_cast<const uint4*>(sums + y * FW + c);
+        const uint32_t s1[4] = {pk.x & 0xFFFu, pk.y & 0xFFFu, pk.z & 0xFFFu, pk.w & 0xFFFu};
+        const uint32_t s2[4] = {pk.x >> 12, pk.y >> 12, pk.z >> 12, pk.w >> 12};
+        const uint32_t own = *(base + (y + RW) * (FBS / 4) + 1);
+        const uint32_t out = w1_gain4<9>(k, own, s1, s2, inv_n);
+        if (vec_store) {
+            *reinterpret_cast<uint32_t*>(drow) = out;
+        } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                if (c + i < col_lim) drow[i] = (uint8_t)(out >> (8 * i));
+        }
+        drow += dpitch;
     }
 }
 
