@@ -139,6 +139,9 @@ int hyb_hybrid_stretch_u8(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows
  * when clamp != 0; sigma2 == 0 returns the input; sigma2 < 0 -> HYB_EINVAL. */
 int hyb_wiener_freq_f64(hyb_ctx* ctx, const double* f, size_t pitch, int rows, int cols, double sigma2,
                         int clamp, double* out, size_t out_pitch);
+/* contrast_stretch on doubles, proj/src/pipeline.cpp:10-21 (the reference's operations: bit-identical). */
+int hyb_contrast_stretch_f64(hyb_ctx* ctx, const double* src, size_t pitch, int rows, int cols, double* dst,
+                             size_t dst_pitch);
 /* estimate_noise_variance without a reference, proj/src/wiener.cpp:44-51:
  * sigma = median(|p - median3(p)|) / 0.6745 (3x3, replicated borders), sigma2 = sigma^2. */
 int hyb_noise_robust_f64(hyb_ctx* ctx, const double* f, size_t pitch, int rows, int cols, double* sigma2);

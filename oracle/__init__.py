@@ -265,3 +265,20 @@ def noise_reference(a, b):
     d = np.asarray(a, np.float64) - np.asarray(b, np.float64)
     return float(np.mean(d * d))
 
+
+def contrast_stretch_f64(img):
+    """proj/src/pipeline.cpp:10-21 verbatim in float64."""
+    x = np.asarray(img, np.float64)
+    lo, hi = x.min(), x.max()
+    return x.copy() if hi == lo else (x - lo) / (hi - lo)
+
+
+def hybrid_reference(g, smax, reference=None, stretch_after_each=False):
+    """The reference's full hybrid_denoise chain restated: AMF (C oracle), [stretch], estimate, frequency
+    Wiener (numpy FFT), final stretch."""
+    f = amf(g, smax).astype(np.float64) / 255.0
+    if stretch_after_each:
+        f = contrast_stretch_f64(f)
+    sigma2 = noise_reference(f, reference) if reference is not None else noise_robust(f)
+    return contrast_stretch_f64(wiener_freq(f, sigma2, True)), sigma2
+

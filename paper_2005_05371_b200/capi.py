@@ -26,7 +26,7 @@ EXPORTED = (
     "hyb_validate_smax", "hyb_validate_config", "hyb_amf_u8", "hyb_amf_batch_u8",
     "hyb_wiener_stats_u8", "hyb_wiener_gain_u8", "hyb_wiener_u8", "hyb_hybrid_u8",
     "hyb_hybrid_batch_u8", "hyb_contrast_stretch_u8", "hyb_hybrid_stretch_u8",
-    "hyb_wiener_freq_f64", "hyb_noise_robust_f64", "hyb_noise_reference_f64", "hyb_make_phantom_u8",
+    "hyb_wiener_freq_f64", "hyb_contrast_stretch_f64", "hyb_noise_robust_f64", "hyb_noise_reference_f64", "hyb_make_phantom_u8",
 )
 
 
@@ -79,6 +79,7 @@ def _load():
         "hyb_hybrid_stretch_u8": (c_int, [P, P, c_size_t, c_int, c_int, c_int, c_int, c_int, P, c_size_t,
                                           POINTER(HybStats)]),
         "hyb_wiener_freq_f64": (c_int, [P, P, c_size_t, c_int, c_int, c_double, c_int, P, c_size_t]),
+        "hyb_contrast_stretch_f64": (c_int, [P, P, c_size_t, c_int, c_int, P, c_size_t]),
         "hyb_noise_robust_f64": (c_int, [P, P, c_size_t, c_int, c_int, POINTER(c_double)]),
         "hyb_noise_reference_f64": (c_int, [P, P, c_size_t, P, c_size_t, c_int, c_int, POINTER(c_double)]),
         "hyb_make_phantom_u8": (c_int, [c_int, c_int, c_int, c_double, c_double, c_uint64, P, c_size_t]),

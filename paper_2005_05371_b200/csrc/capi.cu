@@ -926,6 +926,33 @@ int hyb_wiener_freq_f64(hyb_ctx* ctx, const double* f, size_t pitch, int rows, i
     return HYB_OK;
 }
 
+int hyb_contrast_stretch_f64(hyb_ctx* ctx, const double* src, size_t pitch, int rows, int cols, double* dst,
+                             size_t dst_pitch) {
+    if (!ctx) return HYB_EINVAL;
+    int st;
+    if ((st = check_dims(ctx, rows, cols))) return st;
+    if (pitch < (size_t)cols || dst_pitch < (size_t)cols) return fail(ctx, HYB_EINVAL, "pitch smaller than cols");
+    if (!src || !dst) return fail(ctx, HYB_EINVAL, "null image pointer");
+    HYB_CHECK(cudaSetDevice(ctx->device));
+    const double* s = nullptr;
+    size_t sp = 0;
+    if ((st = stage_f64(ctx, ctx->fin64, src, pitch, rows, cols, &s, &sp))) return st;
+    const bool dd = is_device_ptr(dst);
+    double* d = dst;
+    size_t dp = dst_pitch;
+    if (!dd) {
+        HYB_CHECK(ctx->fout64.ensure((size_t)rows * cols * sizeof(double)));
+        d = reinterpret_cast<double*>(ctx->fout64.ptr);
+        dp = (size_t)cols;
+    }
+    HYB_CHECK(hyb::launch_contrast_stretch_f64(s, sp, rows, cols, d, dp, ctx->freq, ctx->stream));
+    if (!dd)
+        HYB_CHECK(cudaMemcpy2DAsync(dst, dst_pitch * sizeof(double), d, dp * sizeof(double),
+                                    (size_t)cols * sizeof(double), (size_t)rows, cudaMemcpyDefault, ctx->stream));
+    if (!dd || !is_device_ptr(src)) HYB_CHECK(cudaStreamSynchronize(ctx->stream));
+    return HYB_OK;
+}
+
 int hyb_noise_robust_f64(hyb_ctx* ctx, const double* f, size_t pitch, int rows, int cols, double* sigma2) {
     if (!ctx) return HYB_EINVAL;
     int st;

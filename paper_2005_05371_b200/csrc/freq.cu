@@ -122,6 +122,56 @@ __global__ void median_kernel(const double* __restrict__ sorted, long long n, do
     out[0] = (n % 2 == 0) ? (m + sorted[n / 2 - 1]) / 2.0 : m;
 }
 
+// contrast_stretch on doubles (proj/src/pipeline.cpp:10-21): per-CTA min / max partials, one CTA folds
+// them, then (p - lo) / (hi - lo) -- the reference's own operations, so bit-identical results.
+__global__ void __launch_bounds__(FT) minmax_f64_kernel(const double* __restrict__ in, size_t ipitch, int rows,
+                                                       int cols, double* __restrict__ part) {
+    const long long n = (long long)rows * cols;
+    double lo = INFINITY, hi = -INFINITY;
+    for (long long i = (long long)blockIdx.x * FT + threadIdx.x; i < n; i += (long long)gridDim.x * FT) {
+        const int r = (int)(i / cols), c = (int)(i - (long long)r * cols);
+        const double v = in[(size_t)r * ipitch + c];
+        lo = fmin(lo, v);
+        hi = fmax(hi, v);
+    }
+    using BR = cub::BlockReduce<double, FT>;
+    __shared__ typename BR::TempStorage t0, t1;
+    lo = BR(t0).Reduce(lo, cub::Min());
+    hi = BR(t1).Reduce(hi, cub::Max());
+    if (threadIdx.x == 0) {
+        part[2 * blockIdx.x] = lo;
+        part[2 * blockIdx.x + 1] = hi;
+    }
+}
+
+__global__ void __launch_bounds__(FT) fold_kernel(double* __restrict__ part, int nparts) {
+    double lo = INFINITY, hi = -INFINITY;
+    for (int i = threadIdx.x; i < nparts; i += FT) {
+        lo = fmin(lo, part[2 * i]);
+        hi = fmax(hi, part[2 * i + 1]);
+    }
+    using BR = cub::BlockReduce<double, FT>;
+    __shared__ typename BR::TempStorage t0, t1;
+    lo = BR(t0).Reduce(lo, cub::Min());
+    hi = BR(t1).Reduce(hi, cub::Max());
+    if (threadIdx.x == 0) {
+        part[0] = lo;
+        part[1] = hi;
+    }
+}
+
+__global__ void __launch_bounds__(FT) stretch_f64_kernel(const double* __restrict__ in, size_t ipitch, int rows,
+                                                        int cols, const double* __restrict__ mm,
+                                                        double* __restrict__ out, size_t opitch) {
+    const double lo = mm[0], hi = mm[1], range = hi - lo;
+    const long long n = (long long)rows * cols;
+    for (long long i = (long long)blockIdx.x * FT + threadIdx.x; i < n; i += (long long)gridDim.x * FT) {
+        const int r = (int)(i / cols), c = (int)(i - (long long)r * cols);
+        const double p = in[(size_t)r * ipitch + c];
+        out[(size_t)r * opitch + c] = hi == lo ? p : (p - lo) / range;
+    }
+}
+
 int grid_for(long long n) {
     static int sms = 0;
     if (!sms) {
@@ -236,6 +286,21 @@ cudaError_t launch_noise_robust(const double* in, size_t ipitch, int rows, int c
     if ((e = cub::DeviceRadixSort::SortKeys(w.tmp, need, res, sorted, (int)n, 0, 64, stream)) != cudaSuccess) return e;
     count_launch();
     median_kernel<<<1, 1, 0, stream>>>(sorted, n, d_sigma_med);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_contrast_stretch_f64(const double* in, size_t ipitch, int rows, int cols, double* out,
+                                        size_t opitch, FreqWork& w, cudaStream_t stream) {
+    const long long n = (long long)rows * cols;
+    const int grid = grid_for(n);
+    cudaError_t e = grow((void**)&w.keys, &w.keys_n, (size_t)2 * grid * sizeof(double));
+    if (e != cudaSuccess) return e;
+    minmax_f64_kernel<<<grid, FT, 0, stream>>>(in, ipitch, rows, cols, w.keys);
+    fold_kernel<<<1, FT, 0, stream>>>(w.keys, grid);
+    stretch_f64_kernel<<<grid, FT, 0, stream>>>(in, ipitch, rows, cols, w.keys, out, opitch);
+    count_launch();
+    count_launch();
     count_launch();
     return cudaGetLastError();
 }

@@ -107,6 +107,9 @@ cudaError_t launch_wiener_freq(const double* in, size_t ipitch, int rows, int co
 // d_sigma_med <- median(|p - median3(p)|) (device double)
 cudaError_t launch_noise_robust(const double* in, size_t ipitch, int rows, int cols, FreqWork& w, double* d_sigma_med,
                                 cudaStream_t stream);
+// contrast_stretch on doubles (in == out allowed)
+cudaError_t launch_contrast_stretch_f64(const double* in, size_t ipitch, int rows, int cols, double* out,
+                                        size_t opitch, FreqWork& w, cudaStream_t stream);
 // d_acc <- sum (a - b)^2 (device double)
 cudaError_t launch_noise_reference(const double* a, size_t ap, const double* b, size_t bp, int rows, int cols,
                                    double* d_acc, cudaStream_t stream);

@@ -184,8 +184,22 @@ def hybrid_denoise(noisy, config: FilterConfig, ctx=None) -> HybridResult:
 
 
 def contrast_stretch(image, ctx=None):
-    """contrast_stretch -- reference proj/src/pipeline.cpp:10-21 on uint8 images: (v - lo) / (hi - lo)
-    scaled to 0..255, rounded half up (lo -> 0, hi -> 255); unchanged when the image is constant."""
+    """contrast_stretch -- reference proj/src/pipeline.cpp:10-21.  float64 images: the reference's own
+    (p - lo) / (hi - lo) (bit-identical); uint8 images: that quotient scaled to 0..255, rounded half up
+    (lo -> 0, hi -> 255).  Constant images are returned unchanged."""
+    is_f64 = (str(image.dtype) == "torch.float64") if _is_torch(image) else np.asarray(image).dtype == np.float64
+    if is_f64:
+        p, pitch, rows, cols = _f64(image)
+        if _is_torch(image):
+            import torch
+            out = torch.empty((rows, cols), dtype=torch.float64, device=image.device)
+            op = out.data_ptr()
+        else:
+            out = np.empty((rows, cols), np.float64)
+            op = out.ctypes.data
+        c = _ctx(ctx)
+        check(lib.hyb_contrast_stretch_f64(c, p, pitch, rows, cols, op, cols), c)
+        return out
     rows, cols = _shape(image)
     out = _empty_like(image, rows, cols)
     sp, spitch = capi.buf(image)
@@ -390,4 +404,32 @@ def estimate_noise_variance(image, reference=None, ctx=None):
         return out.value, "reference"
     check(lib.hyb_noise_robust_f64(c, p, pitch, rows, cols, ctypes.byref(out)), c)
     return out.value, "robust"
+
+
+def hybrid_denoise_reference(noisy, config: FilterConfig, reference=None, stretch_after_each: bool = False,
+                             ctx=None) -> HybridResult:
+    """The reference's full hybrid_denoise (proj/src/pipeline.cpp:23-57) on the GPU: adaptive median
+    (bands per config), [contrast stretch], noise estimate (robust, or the mean squared difference to
+    `reference`), frequency-domain Wiener (clamped), final contrast stretch.  noisy: uint8 (k/255);
+    reference: float64 in [0, 1] or None.  The image is float64 like the reference's."""
+    import time
+    validate_config(config)
+    rows, cols = _shape(noisy)
+    if reference is not None and _shape(reference) != (rows, cols):
+        raise InvalidArgument("reference image dimensions do not match")
+    t0 = time.perf_counter()
+    f = adaptive_median_parallel(noisy, config, ctx=ctx)
+    f = (f.double() / 255.0) if _is_torch(f) else np.asarray(f, np.float64) / 255.0
+    t1 = time.perf_counter()
+    t_stretch = 0.0
+    if stretch_after_each:
+        f = contrast_stretch(f, ctx=ctx)
+        t_stretch += time.perf_counter() - t1
+    t2 = time.perf_counter()
+    sigma2, _ = estimate_noise_variance(f, reference, ctx=ctx)
+    y = wiener_filter(f, sigma2, clamp=True, ctx=ctx)
+    t3 = time.perf_counter()
+    y = contrast_stretch(y, ctx=ctx)
+    t_stretch += time.perf_counter() - t3
+    return HybridResult(y, sigma2, t1 - t0, t3 - t2, t_stretch, 0, time.perf_counter() - t0)
 

@@ -2,6 +2,7 @@
 #include "denoise_cuda.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <map>
 #include <stdexcept>
@@ -201,6 +202,69 @@ HybridResult hybrid_denoise(const Image& noisy, const FilterConfig& config) {
     r.t_adaptive = st.t_adaptive;
     r.t_wiener = st.t_wiener;
     r.noise_sum = st.noise_sum;
+    return r;
+}
+
+Image contrast_stretch(const Image& image) {
+    Image out(image.rows(), image.cols());
+    hyb_ctx* ctx = context(0);
+    check(hyb_contrast_stretch_f64(ctx, image.pixels().data(), image.cols(), image.rows(), image.cols(),
+                                   out.pixels().data(), out.cols()),
+          ctx);
+    return out;
+}
+
+NoiseEstimate estimate_noise_variance(const Image& image, const Image* reference) {
+    hyb_ctx* ctx = context(0);
+    NoiseEstimate est;
+    if (reference) {
+        if (reference->rows() != image.rows() || reference->cols() != image.cols())
+            throw std::invalid_argument("reference image dimensions do not match");
+        check(hyb_noise_reference_f64(ctx, image.pixels().data(), image.cols(), reference->pixels().data(),
+                                      reference->cols(), image.rows(), image.cols(), &est.sigma2),
+              ctx);
+        est.source = NoiseSource::reference;
+    } else {
+        check(hyb_noise_robust_f64(ctx, image.pixels().data(), image.cols(), image.rows(), image.cols(), &est.sigma2),
+              ctx);
+        est.source = NoiseSource::robust;
+    }
+    return est;
+}
+
+Image wiener_filter(const Image& image, const NoiseEstimate& noise, bool clamp) {
+    Image out(image.rows(), image.cols());
+    hyb_ctx* ctx = context(0);
+    check(hyb_wiener_freq_f64(ctx, image.pixels().data(), image.cols(), image.rows(), image.cols(), noise.sigma2,
+                              clamp ? 1 : 0, out.pixels().data(), out.cols()),
+          ctx);
+    return out;
+}
+
+HybridResult hybrid_denoise_reference(const Image& noisy, const FilterConfig& config, const Image* reference,
+                                      bool stretch_after_each) {
+    validate_config(config);
+    if (reference && (reference->rows() != noisy.rows() || reference->cols() != noisy.cols()))
+        throw std::invalid_argument("reference image dimensions do not match");
+    using clock = std::chrono::steady_clock;
+    auto secs = [](clock::time_point a, clock::time_point b) { return std::chrono::duration<double>(b - a).count(); };
+    HybridResult r;
+    auto t0 = clock::now();
+    Image filtered = adaptive_median_parallel(noisy, config);
+    auto t1 = clock::now();
+    r.t_adaptive = secs(t0, t1);
+    if (stretch_after_each) {
+        filtered = contrast_stretch(filtered);
+        r.t_stretch += secs(t1, clock::now());
+    }
+    auto t2 = clock::now();
+    const NoiseEstimate est = estimate_noise_variance(filtered, reference);
+    r.sigma2 = est.sigma2;
+    Image denoised = wiener_filter(filtered, est);
+    auto t3 = clock::now();
+    r.t_wiener = secs(t2, t3);
+    r.image = contrast_stretch(denoised);
+    r.t_stretch += secs(t3, clock::now());
     return r;
 }
 

@@ -93,6 +93,23 @@ HybridResult hybrid_denoise(const Image& noisy, const FilterConfig& config);
 std::vector<uint8_t> to_u8(const Image& image);
 Image from_u8(const uint8_t* px, int rows, int cols);
 
+/// The reference's own Wiener stage and pipeline tail on the GPU (doubles, like the reference):
+/// contrast_stretch proj/src/pipeline.cpp:10-21 (bit-identical), estimate_noise_variance
+/// proj/src/wiener.cpp:30-52, wiener_filter proj/src/wiener.cpp:54-77 (cuFFT, double).
+enum class NoiseSource { given, reference, robust };
+struct NoiseEstimate {
+    double sigma2 = 0.0;
+    NoiseSource source = NoiseSource::given;
+};
+Image contrast_stretch(const Image& image);
+NoiseEstimate estimate_noise_variance(const Image& image, const Image* reference = nullptr);
+Image wiener_filter(const Image& image, const NoiseEstimate& noise, bool clamp = true);
+
+/// The reference's full hybrid_denoise (proj/src/pipeline.cpp:23-57): adaptive median bands,
+/// [stretch], noise estimate (reference image if given, else robust), frequency Wiener, final stretch.
+HybridResult hybrid_denoise_reference(const Image& noisy, const FilterConfig& config, const Image* reference = nullptr,
+                                      bool stretch_after_each = false);
+
 /// load_pgm / save_pgm -- proj/src/pgm_io.cpp:49-122: P5 or P2, maxval
 /// 1..65535, samples / maxval; writer P5 maxval 255, round half away from zero.  Same error texts
 /// ("pgm <path>: ...", std::runtime_error).  P5/P2 files with maxval 255 load exactly onto the

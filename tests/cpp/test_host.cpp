@@ -158,6 +158,43 @@ int main() {
             CHECK(r.sigma2 > 0);
         }
     }
+    // the reference's pipeline tail (proj/tests/test_pipeline.cpp:29-57, test_wiener.cpp:110-160)
+    {
+        const Image kat = Image::from_pixels(2, 2, {0.2, 0.4, 0.6, 0.7});
+        const Image st = contrast_stretch(kat);
+        CHECK(st.at(0, 0) == 0.0 && st.at(1, 1) == 1.0);
+        CHECK(std::fabs(st.at(0, 1) - 0.4) < 1e-14 && std::fabs(st.at(1, 0) - 0.8) < 1e-14);
+        const Image flat(5, 5, 0.42);
+        CHECK(contrast_stretch(flat) == flat);
+        Image a(8, 8, 0.5), b(8, 8, 0.5);
+        b.at(0, 0) = 0.9;
+        const NoiseEstimate ref = estimate_noise_variance(a, &b);
+        CHECK(ref.source == NoiseSource::reference && std::fabs(ref.sigma2 - 0.16 / 64.0) < 1e-15);
+        CHECK(estimate_noise_variance(Image(32, 32, 0.3)).sigma2 == 0.0);
+        const int n = 8;
+        Image cosine(n, n);
+        for (int r = 0; r < n; ++r)
+            for (int c = 0; c < n; ++c) cosine.at(r, c) = std::cos(2.0 * M_PI * c / n);
+        const Image w = wiener_filter(cosine, {0.01, NoiseSource::given}, false);
+        double worst = 0.0;
+        for (std::size_t i = 0; i < w.size(); ++i)
+            worst = std::max(worst, std::fabs(w.pixels()[i] - 0.999375 * cosine.pixels()[i]));
+        CHECK(worst < 1e-9);
+        bool threw = false;
+        try {
+            wiener_filter(cosine, {-1e-9, NoiseSource::given});
+        } catch (const std::invalid_argument&) {
+            threw = true;
+        }
+        CHECK(threw);
+        // full pipeline: a constant image passes through untouched (test_pipeline.cpp:59-64)
+        FilterConfig cfg;
+        cfg.parts = 2;
+        cfg.workers = 2;
+        const Image flat6(32, 32, 0.6);
+        const HybridResult hr = hybrid_denoise_reference(flat6, cfg);
+        CHECK(hr.image == flat6 && hr.sigma2 == 0.0);
+    }
     std::printf("%d checks, %d failed\n", g_checks, g_fail);
     return g_fail;
 }

@@ -97,3 +97,37 @@ def test_noise_estimate_robust_mode(ctx):
     assert abs(s2 - oracle.noise_robust(noisy)) <= 1e-12 * s2
     odd = np.random.default_rng(5).random((15, 17))  # odd count: the middle element
     assert abs(denoise.estimate_noise_variance(odd)[0] - oracle.noise_robust(odd)) <= 1e-12
+
+
+def test_contrast_stretch_f64_bit_identical(ctx):
+    rng = np.random.default_rng(8)
+    for shape in ((1, 1), (5, 5), (300, 517)):
+        img = rng.random(shape) * 0.2 + 0.3
+        np.testing.assert_array_equal(denoise.contrast_stretch(img), oracle.contrast_stretch_f64(img))
+    np.testing.assert_array_equal(denoise.contrast_stretch(np.full((5, 5), 0.42)), np.full((5, 5), 0.42))
+    kat = np.array([[0.2, 0.4], [0.6, 0.7]])  # proj/tests/test_pipeline.cpp:29-36
+    out = denoise.contrast_stretch(kat)
+    assert out[0, 0] == 0.0 and out[1, 1] == 1.0
+    np.testing.assert_allclose(out, [[0.0, 0.4], [0.8, 1.0]], rtol=1e-14)
+
+
+@pytest.mark.parametrize("stretch_after_each", [False, True])
+def test_full_reference_pipeline_vs_oracle_chain(ctx, stretch_after_each):
+    from paper_2005_05371_b200 import CONFIGS, FilterConfig
+    c = CONFIGS[0]
+    g = capi.make_phantom(c["rows"], c["cols"], c["ellipses"], c["sigma"], c["density"], 0)
+    res = denoise.hybrid_denoise_reference(g, FilterConfig(smax=c["smax"], parts=4), stretch_after_each=stretch_after_each)
+    want, s2 = oracle.hybrid_reference(g, c["smax"], stretch_after_each=stretch_after_each)
+    assert abs(res.sigma2 - s2) <= 1e-12 * max(s2, 1e-30)
+    assert np.max(np.abs(res.image - want)) < 1e-6  # the reference's own Wiener tolerance
+    assert res.image.min() == 0.0 and res.image.max() == 1.0
+
+
+def test_full_reference_pipeline_reference_mode(ctx):
+    from paper_2005_05371_b200 import FilterConfig
+    g = capi.make_phantom(200, 260, 8, 12.0, 0.1, 4)
+    clean = capi.make_phantom(200, 260, 8, 0.0, 0.0, 4).astype(np.float64) / 255.0
+    res = denoise.hybrid_denoise_reference(g, FilterConfig(smax=7), reference=clean)
+    want, s2 = oracle.hybrid_reference(g, 7, reference=clean)
+    assert abs(res.sigma2 - s2) <= 1e-12 * s2
+    assert np.max(np.abs(res.image - want)) < 1e-6
