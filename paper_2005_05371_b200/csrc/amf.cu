@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(GNT, 2) amf_grow_kernel(const __grid_constant_
     uint8_t* bufs = smem + GHDR;
     uint16_t* Q0 = reinterpret_cast<uint16_t*>(bufs + (size_t)GSLOTS * geo.b_bytes);
     uint16_t* Q1 = Q0 + GCAP;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x;
     const int per_slice = args.tiles_x * args.tiles_y;
     if (tid == 0) {
         for (int i = 0; i < GSLOTS; ++i) mbar_init(&bar[i], 1);

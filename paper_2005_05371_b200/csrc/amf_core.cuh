@@ -261,6 +261,10 @@ template <>
 __device__ __forceinline__ void select_net<7>(uint32_t (&v)[49], uint32_t& a, uint32_t& b, uint32_t& c) {
     select_net7(v, a, b, c);
 }
+template <>
+__device__ __forceinline__ void select_net<9>(uint32_t (&v)[81], uint32_t& a, uint32_t& b, uint32_t& c) {
+    select_net9(v, a, b, c);
+}
 
 // k = 5, 7: two queued pixels in the u16x2 lanes of one thread, generated selection network.
 template <int K>
@@ -510,7 +514,13 @@ __device__ __forceinline__ long long rec_off(const unsigned long long* rec, long
 // row * 128 + column of a 128 x 32 tile whose window bytes start at slot(slot), laid out as geo).  CTA-wide
 // (NTHR threads, every thread calls it; qcount[1..] zero on entry); level k resolves what it can through
 // out(slot, pixel, value, k) and re-queues the rest for k + 2.  Ends with __syncthreads.
-template <bool FIN, int NTHR, class Slot, class Out>
+#ifndef HYB_GROW_NETMAX
+#define HYB_GROW_NETMAX 9  // largest window grown with a selection network (k <= 9); radix above
+#endif
+#ifndef HYB_NET9_MIN
+#define HYB_NET9_MIN 1  // the k = 9 network needs >= HYB_NET9_MIN * NTHR queued pixels (else radix, 1 px/thread)
+#endif
+template <bool FIN, int NTHR, class Slot, class Out, int NETMAX = HYB_GROW_NETMAX>
 __device__ __forceinline__ void grow_levels_at(Slot slot, const GGeo& geo, uint16_t* Q0, uint16_t* Q1, int* qcount,
                                                int n, int smax, Out out) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -519,7 +529,7 @@ __device__ __forceinline__ void grow_levels_at(Slot slot, const GGeo& geo, uint1
         const uint16_t* qin = (lvl & 1) ? Q1 : Q0;
         uint16_t* qout = (lvl & 1) ? Q0 : Q1;
         const bool last = k + 2 > smax;
-        if (k <= 7) {
+        if (k <= NETMAX && (k < 9 || n >= HYB_NET9_MIN * NTHR)) {
             const int npairs = (n + 1) >> 1;
             for (int base = warp * 32; base < npairs; base += NTHR) {
                 const int i = base + lane;
@@ -534,7 +544,8 @@ __device__ __forceinline__ void grow_levels_at(Slot slot, const GGeo& geo, uint1
                     const uint8_t* BA = slot(sa);
                     const uint8_t* BB = slot(sb);
                     if (k == 5) level_pair2<5>(BA, BB, geo, pa, pb, done, outw);
-                    else level_pair2<7>(BA, BB, geo, pa, pb, done, outw);
+                    else if (k == 7) level_pair2<7>(BA, BB, geo, pa, pb, done, outw);
+                    else if constexpr (NETMAX >= 9) level_pair2<9>(BA, BB, geo, pa, pb, done, outw);
                     if (done & 1u) {
                         out(sa, pa, (uint8_t)outw, k);
                     } else {
@@ -603,11 +614,11 @@ __device__ __forceinline__ void grow_levels_at(Slot slot, const GGeo& geo, uint1
 }
 
 // Slots at a fixed stride in local shared memory.
-template <bool FIN, int NTHR, class Out>
+template <bool FIN, int NTHR, class Out, int NETMAX = HYB_GROW_NETMAX>
 __device__ __forceinline__ void grow_levels(const uint8_t* bufs, const GGeo& geo, uint16_t* Q0, uint16_t* Q1,
                                             int* qcount, int n, int smax, Out out) {
-    grow_levels_at<FIN, NTHR>([&](int sl) { return bufs + (size_t)sl * geo.b_bytes; }, geo, Q0, Q1, qcount, n, smax,
-                              out);
+    auto slot = [&](int sl) { return bufs + (size_t)sl * geo.b_bytes; };
+    grow_levels_at<FIN, NTHR, decltype(slot), Out, NETMAX>(slot, geo, Q0, Q1, qcount, n, smax, out);
 }
 
 // Growth over the failure range [gbeg, gend) of the weighted record order (records: (offset << 24) |

@@ -168,9 +168,13 @@ __global__ void __launch_bounds__(SNT, 3) hybrid_small_kernel(const __grid_const
         }
 #endif
         if (total > 0)
-            grow_levels<false, SNT>(slots, geo, Q0, Q1, qcount, total, a.smax, [&](int sl, int pix, uint8_t v, int) {
+        {
+            auto out = [&](int sl, int pix, uint8_t v, int) {
                 a.f[(size_t)(tinfo[2 * sl + 1] + (pix >> 7)) * a.fpitch + tinfo[2 * sl] + (pix & 127)] = v;
-            });
+            };
+            // networks up to k = 7 here (the k = 9 one needs more registers than 3 CTAs/SM allow)
+            grow_levels<false, SNT, decltype(out), 7>(slots, geo, Q0, Q1, qcount, total, a.smax, out);
+        }
     }
     TRACE(0, 5);
     if (blockIdx.x == 0 && tid == 0) *a.wsum = 0;

@@ -19,12 +19,12 @@ constexpr int FBS = FW + 2 * FCP;  // staged row bytes (160)
 // 4 bytes starting at byte S of the 12-byte window [w0 w1 w2] (S compile-time, 0..11).
 template <int S>
 __device__ __forceinline__ uint32_t bytes4(uint32_t w0, uint32_t w1, uint32_t w2) {
-    if (S == 0) return w0;
-    if (S == 4) return w1;
-    if (S == 8) return w2;
-    if (S < 4) return __funnelshift_r(w0, w1, 8 * S);
-    if (S < 8) return __funnelshift_r(w1, w2, 8 * (S - 4));
-    return w2 >> (8 * (S - 8));  // only the low 12 - S bytes are meaningful
+    if constexpr (S == 0) return w0;
+    else if constexpr (S == 4) return w1;
+    else if constexpr (S == 8) return w2;
+    else if constexpr (S < 4) return __funnelshift_r(w0, w1, 8 * S);
+    else if constexpr (S < 8) return __funnelshift_r(w1, w2, 8 * (S - 4));
+    else return w2 >> (8 * (S - 8));  // only the low 12 - S bytes are meaningful
 }
 
 // Horizontal window sums (f, f^2) of pixel I (0..3) of the lane's 4 columns.

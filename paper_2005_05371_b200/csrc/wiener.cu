@@ -242,8 +242,6 @@ struct FastArgs {
 template <int RW, bool GAIN, int FH>
 __global__ void __launch_bounds__(FNW * 32, GAIN ? 4 : 3) wiener_fast_kernel(const __grid_constant__ CUtensorMap tm,
                                                                const __grid_constant__ FastArgs a) {
-    constexpr int N = 2 * RW + 1;
-    constexpr int NN = N * N;
     constexpr int SROWS = FH + 2 * RW;
     constexpr int SLOT = kFastSmemSlot(RW, FH);
     extern __shared__ __align__(128) uint8_t smem_raw[];
