@@ -37,6 +37,11 @@ $(PGMTEST): tests/cpp/test_pgm.cpp $(HOSTLIB)
 	$(CXX) -std=c++20 -O2 -Wall -Wextra -o $@ tests/cpp/test_pgm.cpp -L$(PKG) -ldenoise_cuda -lhybrid_cuda \
 		-Wl,-rpath,'$$ORIGIN/../../$(PKG)'
 
+# A/B variant of the same library (tools/ab.sh): make alt ALTDEF=-DHYB_SMALL_NT=256
+ALTDEF ?=
+alt: $(SRCS) $(HDRS)
+	$(NVCC) $(NVFLAGS) $(ALTDEF) -shared -o $(PKG)/libhybrid_cuda_alt.so $(SRCS) -lcufft -Xlinker -rpath,/usr/local/cuda/lib64 2> /dev/null
+
 oracle:
 	$(MAKE) -C oracle --no-print-directory
 
@@ -44,4 +49,4 @@ clean:
 	rm -f $(LIB) $(PKG)/libhybrid_cuda_trace.so $(HOSTLIB) $(CPPTEST) $(PGMTEST) build_ptxas.log
 	$(MAKE) -C oracle clean
 
-.PHONY: all oracle clean trace
+.PHONY: all oracle clean trace alt

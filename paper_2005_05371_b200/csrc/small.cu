@@ -32,8 +32,17 @@
 namespace hyb {
 namespace {
 
-constexpr int SNT = 256;   // threads per CTA (8 warps)
-constexpr int STPC = 2;    // tiles per CTA (max)
+// CTA size: 256 threads, 3 CTAs/SM (2 tiles each).  HYB_SMALL_NT=768 (one CTA per SM, all 24 warps
+// pooling the SM's growth failures) shortened the in-kernel growth tail by 1.8 us at config 1 but
+// measured 1.8 us slower per launch (30.8 vs 29.0 us; 512: 30.8 us) -- kept as a build option.
+#ifndef HYB_SMALL_NT
+#define HYB_SMALL_NT 256
+#endif
+constexpr int SNT = HYB_SMALL_NT;                            // threads per CTA
+constexpr int SNW = SNT / 32;                                // warps per CTA
+constexpr int SMIN = SNT >= 768 ? 1 : (SNT >= 512 ? 2 : 3);  // CTAs per SM (register budget)
+constexpr int STPC = SNT >= 768 ? 6 : (SNT >= 512 ? 3 : 2);  // tiles per CTA (max)
+static_assert(STPC <= 8 && SNW <= 32, "header layout");
 constexpr int SHDR = 1024;  // mbarriers, tile coordinates, level counters
 constexpr int SFH = 8;     // W1 sub-tile rows
 
@@ -93,7 +102,7 @@ __device__ __forceinline__ void cta_replicate_edges(uint8_t* slots, int slot_byt
 }
 
 template <int RW>
-__global__ void __launch_bounds__(SNT, 3) hybrid_small_kernel(const __grid_constant__ CUtensorMap tm_g,
+__global__ void __launch_bounds__(SNT, SMIN) hybrid_small_kernel(const __grid_constant__ CUtensorMap tm_g,
                                                              const __grid_constant__ CUtensorMap tm_f,
                                                              const __grid_constant__ SArgs a) {
     constexpr int FROWS = TH + 2 * RW;  // f tile rows with the W1 halo
@@ -101,14 +110,14 @@ __global__ void __launch_bounds__(SNT, 3) hybrid_small_kernel(const __grid_const
     uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
     const GGeo& geo = a.geo;
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem);           // [STPC] own tiles (g, then f)
-    int* tinfo = reinterpret_cast<int*>(smem + 128);              // [STPC][2]: x0, y0
-    int* org = reinterpret_cast<int*>(smem + 160);                // [STPC][2]: box origin (edge fix-up)
-    unsigned long long* wred = reinterpret_cast<unsigned long long*>(smem + 256);  // [8] warp partial W
-    int* qcount = reinterpret_cast<int*>(smem + 384);             // [MAX_LEVELS]
+    int* tinfo = reinterpret_cast<int*>(smem + 64);               // [STPC][2]: x0, y0
+    int* org = reinterpret_cast<int*>(smem + 128);                // [STPC][2]: box origin (edge fix-up)
+    unsigned long long* wred = reinterpret_cast<unsigned long long*>(smem + 256);  // [SNW] warp partial W
+    int* qcount = reinterpret_cast<int*>(smem + 512);             // [MAX_LEVELS]
     uint8_t* slots = smem + SHDR;                                // [STPC][slot_bytes] g tiles, then f tiles
     uint8_t* bitmaps = slots + (size_t)STPC * a.slot_bytes;     // [STPC][512]
-    uint8_t* stage = bitmaps + STPC * 512;                      // [8 warps][WPIX] k = 3 output staging
-    uint16_t* Q0 = reinterpret_cast<uint16_t*>(stage + NW * WPIX);
+    uint8_t* stage = bitmaps + STPC * 512;                      // [SNW][WPIX] k = 3 output staging
+    uint16_t* Q0 = reinterpret_cast<uint16_t*>(stage + SNW * WPIX);
     uint16_t* Q1 = Q0 + STPC * 4096;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nt = (a.ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;  // my tiles (<= STPC)
@@ -145,10 +154,11 @@ __global__ void __launch_bounds__(SNT, 3) hybrid_small_kernel(const __grid_const
     TRACE(0, 2);
     {
         uint8_t* O = stage + warp * WPIX;
-        for (int i = 0; i < nt; ++i) {
+        for (int j = warp; j < nt * NW; j += SNW) {  // strip j % NW of tile j / NW
+            const int i = j / NW;
             const int x0 = tinfo[2 * i], y0 = tinfo[2 * i + 1];
             const uint8_t* B = slots + (size_t)i * a.slot_bytes + (size_t)(geo.R - 1) * geo.BS;  // row 0 = y0 - 1
-            k3_strip<false>(B, O, O, warp, a.smax >= 5 ? bitmaps + i * 512 : nullptr,
+            k3_strip<false>(B, O, O, j % NW, a.smax >= 5 ? bitmaps + i * 512 : nullptr,
                             a.f + (size_t)y0 * a.fpitch + x0, a.fpitch, nullptr, 0, a.rows - y0, a.cols - x0);
         }
     }
@@ -159,7 +169,7 @@ __global__ void __launch_bounds__(SNT, 3) hybrid_small_kernel(const __grid_const
     if (a.smax >= 5) {
         const int total = cta_bitmap_queue<SNT>(reinterpret_cast<const uint32_t*>(bitmaps), nt * 128, Q0,
                                                 reinterpret_cast<uint16_t*>(stage),
-                                                reinterpret_cast<int*>(stage + 1024));
+                                                reinterpret_cast<int*>(stage + 2048));
         TRACE(0, 4);
 #ifdef HYB_TRACE
         if (tid == 0 && blockIdx.x < 1024) {
@@ -201,7 +211,7 @@ __global__ void __launch_bounds__(SNT, 3) hybrid_small_kernel(const __grid_const
     TRACE(0, 8);
     unsigned long long vsum = 0;
     uint32_t* sums = reinterpret_cast<uint32_t*>(Q0);  // [STPC][32][128] packed S1 | S2 << 12 (RW == 1)
-    for (int j = warp; j < nt * (TH / SFH); j += NW) {
+    for (int j = warp; j < nt * (TH / SFH); j += SNW) {
         const int i = j / (TH / SFH), k = j % (TH / SFH);
         const uint8_t* T = slots + (size_t)i * a.slot_bytes + (size_t)k * SFH * FBS;
         const int y0 = tinfo[2 * i + 1] + k * SFH;
@@ -219,7 +229,7 @@ __global__ void __launch_bounds__(SNT, 3) hybrid_small_kernel(const __grid_const
     __syncthreads();
     if (tid == 0) {
         unsigned long long s = 0;
-        for (int w = 0; w < NW; ++w) s += wred[w];
+        for (int w = 0; w < SNW; ++w) s += wred[w];
         if (s) atomicAdd(a.wsum, s);
     }
     grid_barrier(a.bar_count, 1);  // W complete
@@ -227,7 +237,7 @@ __global__ void __launch_bounds__(SNT, 3) hybrid_small_kernel(const __grid_const
     TRACE(0, 10);
     // ---- D: gain from the resident f tiles ----
     const W1Gain kg = w1_gain_consts((long long)__ldcg(a.wsum), (long long)a.rows * a.cols);
-    for (int j = warp; j < nt * (TH / SFH); j += NW) {
+    for (int j = warp; j < nt * (TH / SFH); j += SNW) {
         const int i = j / (TH / SFH), k = j % (TH / SFH);
         const uint8_t* T = slots + (size_t)i * a.slot_bytes + (size_t)k * SFH * FBS;
         const int x0 = tinfo[2 * i], y0 = tinfo[2 * i + 1] + k * SFH;
@@ -245,7 +255,7 @@ __global__ void __launch_bounds__(SNT, 3) hybrid_small_kernel(const __grid_const
 }
 
 size_t small_smem(int slot_bytes) {
-    return SHDR + (size_t)STPC * slot_bytes + STPC * 512 + NW * WPIX + 2 * STPC * 4096 * 2 + 128;
+    return SHDR + (size_t)STPC * slot_bytes + STPC * 512 + SNW * WPIX + 2 * STPC * 4096 * 2 + 128;
 }
 
 int g_ssms = 0;
@@ -320,6 +330,7 @@ SmallPlan plan_small(int rows, int cols, int smax, int win) {
                         : rw == 1 ? (const void*)hybrid_small_kernel<1>
                         : rw == 2 ? (const void*)hybrid_small_kernel<2>
                                   : (const void*)hybrid_small_kernel<3>;
+        cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[rw], k, SNT, smem) != cudaSuccess)
             per_sm[rw] = 0;

@@ -3,7 +3,7 @@ import ctypes
 import os
 import sys
 
-os.environ["HYB_LIB"] = "libhybrid_cuda_trace.so"
+os.environ.setdefault("HYB_LIB", "libhybrid_cuda_trace.so")
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
