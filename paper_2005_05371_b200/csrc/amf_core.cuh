@@ -7,6 +7,7 @@
 
 #include "networks.cuh"
 #include "tma.cuh"
+#include "trace.cuh"
 
 namespace hyb {
 namespace {
@@ -526,6 +527,10 @@ __device__ __forceinline__ void grow_levels_at(Slot slot, const GGeo& geo, uint1
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int lvl = 0;
     for (int k = 5; k <= smax; k += 2, ++lvl) {
+#ifdef HYB_TRACE
+        unsigned long long t_lvl = 0;
+        if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_lvl));
+#endif
         const uint16_t* qin = (lvl & 1) ? Q1 : Q0;
         uint16_t* qout = (lvl & 1) ? Q0 : Q1;
         const bool last = k + 2 > smax;
@@ -607,6 +612,15 @@ __device__ __forceinline__ void grow_levels_at(Slot slot, const GGeo& geo, uint1
             }
         }
         __syncthreads();
+#ifdef HYB_TRACE
+        // growth-level profile (kernel id 1): slots 5 + lvl += level time, 9 + lvl += level pixels
+        if (threadIdx.x == 0 && blockIdx.x < 1024 && lvl < 4) {
+            unsigned long long t1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            g_trace[(1024 + blockIdx.x) * 16 + 5 + lvl] += t1 - t_lvl;
+            g_trace[(1024 + blockIdx.x) * 16 + 9 + lvl] += (unsigned long long)n;
+        }
+#endif
         if (last) break;
         n = qcount[lvl + 1];
         if (n == 0) break;
@@ -653,6 +667,19 @@ __device__ __forceinline__ void grow_range(const CUtensorMap* tm, const GGeo& ge
     uint8_t* bufs = sm.bufs;
     uint16_t* Q0 = sm.Q0;
     uint16_t* Q1 = sm.Q1;
+#ifdef HYB_TRACE
+    // growth batch profile (kernel id 1): slot 1 += segment choice, 2 += queue build, 3 += tile wait +
+    // edges, 4 += batches, 13 += kernel entry to the first batch
+    unsigned long long tt0 = 0, tt1 = 0;
+    auto tnow = [] { unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; };
+    auto tacc = [&](int slot) {
+        if (tid == 0 && blockIdx.x < 1024) { tt1 = tnow(); g_trace[(1024 + blockIdx.x) * 16 + slot] += tt1 - tt0; tt0 = tt1; }
+    };
+    if (tid == 0) tt0 = tnow();
+#define GTRACE(slot) tacc(slot)
+#else
+#define GTRACE(slot) do {} while (0)
+#endif
     if (warp == 0 && gbeg < gend) {
         // 32-ary search: the last record whose offset is <= gbeg
         long long lo = 0, hi = R;
@@ -670,6 +697,7 @@ __device__ __forceinline__ void grow_range(const CUtensorMap* tm, const GGeo& ge
         }
     }
     __syncthreads();
+    GTRACE(13);
 
     while (gbeg < gend) {
         // ---- 1. warp 0: the next segments (lane l: record cur + l), their TMA loads.  Positions are
@@ -732,6 +760,7 @@ __device__ __forceinline__ void grow_range(const CUtensorMap* tm, const GGeo& ge
             }
         }
         __syncthreads();
+        GTRACE(1);
         const int ns = ctl[0];
         const bool more = ctl[2] != 0;
         if (ns == 0) {  // only tile-load weight in this stretch of the range
@@ -752,6 +781,13 @@ __device__ __forceinline__ void grow_range(const CUtensorMap* tm, const GGeo& ge
                 if (lane >= d) incl += v;
             }
             int rank = incl - nf;
+#ifdef HYB_TRACE
+            unsigned long long tq0 = 0;
+            if (tid == 0 && blockIdx.x < 1024) {
+                tq0 = tnow();
+                g_trace[(1024 + blockIdx.x) * 16 + 0] += tq0 - tt0 + (rank & 0);  // bitmap load + scan (warp 0)
+            }
+#endif
             const int lo = si[4], hi = si[5], qb = si[6] - lo;
             const uint32_t sbase = (uint32_t)warp << 12;
             if (rank < hi && incl > lo) {
@@ -768,8 +804,16 @@ __device__ __forceinline__ void grow_range(const CUtensorMap* tm, const GGeo& ge
                     }
                 }
             }
+#ifdef HYB_TRACE
+            __syncwarp();
+            if (tid == 0 && blockIdx.x < 1024) g_trace[(1024 + blockIdx.x) * 16 + 14] += tnow() - tq0;  // emission (warp 0)
+#endif
         }
         // ---- 3. tiles landed; border tiles get edge replication (whole CTA, columns then rows) ----
+#ifdef HYB_TRACE
+        __syncthreads();
+        GTRACE(2);
+#endif
         for (int sl = 0; sl < ns; ++sl) mbar_wait(&bar[sl], (phases >> sl) & 1u);
         phases ^= (1u << ns) - 1u;
         for (int sl = 0; sl < ns; ++sl) {
@@ -779,13 +823,19 @@ __device__ __forceinline__ void grow_range(const CUtensorMap* tm, const GGeo& ge
                                   max(0, -sy0), min(geo.BH, rows - sy0), 0, geo.BH, geo.R);
         }
         __syncthreads();
+        GTRACE(3);
         // ---- 4. levels, pooled over the batch ----
         int n = ctl[1];
         grow_levels<FIN, NTHR>(bufs, geo, Q0, Q1, qcount, n, smax,
                                [&](int sl, int pix, uint8_t v, int k) { out(sinfo + 8 * sl, pix, v, k); });
         __syncthreads();  // slots, queues and counters are reused by the next batch
+#ifdef HYB_TRACE
+        if (tid == 0 && blockIdx.x < 1024) g_trace[(1024 + blockIdx.x) * 16 + 4] += 1;
+        if (tid == 0) tt0 = tnow();
+#endif
         if (!more) break;
     }
+#undef GTRACE
 }
 
 }  // namespace

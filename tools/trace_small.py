@@ -24,10 +24,13 @@ capi.lib.hyb_trace_read_small(buf)
 t = np.frombuffer(buf, dtype=np.uint64).reshape(2, 1024, 16).astype(np.int64)[0]
 t = t[t[:, 0] > 0]
 t0 = t[:, 0].min()
-names = ["start", "g landed", "edges", "k=3 done", "queue", "growth done", "barrier 1", "f landed", "f edges",
-         "stats done", "barrier 2", "gain done"]
+names = ["start", "g landed", "edges", "k=3 done", "queue", "growth done", "own stats", "barrier 1", "f landed",
+         "f edges", "stats done", "barrier 2", "gain done"]
+slots = [0, 1, 2, 3, 4, 5, 14, 6, 7, 8, 9, 10, 11]
 print(f"config {cfg}: {len(t)} CTAs   quantiles 0/10/50/90/100 (us)")
-for s, nm in enumerate(names):
+for s, nm in zip(slots, names):
+    if not t[:, s].any():
+        continue
     col = (t[:, s] - t0) / 1e3
     print(f"{nm:12s}", " ".join(f"{v:7.2f}" for v in np.percentile(col, [0, 10, 50, 90, 100])))
 
