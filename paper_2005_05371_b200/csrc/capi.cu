@@ -71,6 +71,7 @@ struct hyb_ctx {
     size_t host_w_n = 0;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     cudaStream_t copy = nullptr;       // host<->device staging stream of the pipelined path
+    cudaStream_t copy2 = nullptr;      // device->host stream of the pipelined batch path (PCIe duplex)
     // CUDA-graph cache of hyb_hybrid_u8 calls: a key seen once is captured on its second call and
     // replayed afterwards (one launch per step instead of ~10-30 API calls).
     using GraphKey = std::tuple<const void*, void*, size_t, size_t, int, int, int, int, int, cudaStream_t>;
@@ -80,7 +81,7 @@ struct hyb_ctx {
     };
     std::map<GraphKey, Graph> graphs;
     std::map<GraphKey, int> graph_seen;
-    static constexpr int kMaxChunks = 8;
+    static constexpr int kMaxChunks = 16;
     cudaEvent_t ev_h2d[kMaxChunks] = {}, ev_gain[kMaxChunks] = {};
 };
 
@@ -404,6 +405,7 @@ hyb_ctx* hyb_create(int device, int* status) {
         return nullptr;
     }
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->copy2, cudaStreamNonBlocking);
     for (int i = 0; i < hyb_ctx::kMaxChunks && e == cudaSuccess; ++i) {
         e = cudaEventCreateWithFlags(&ctx->ev_h2d[i], cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_gain[i], cudaEventDisableTiming);
@@ -449,6 +451,7 @@ int hyb_destroy(hyb_ctx* ctx) {
     for (auto& ev : ctx->ev_gain)
         if (ev) cudaEventDestroy(ev);
     if (ctx->copy) cudaStreamDestroy(ctx->copy);
+    if (ctx->copy2) cudaStreamDestroy(ctx->copy2);
     if (ctx->own) cudaStreamDestroy(ctx->own);
     delete ctx;
     return HYB_OK;
@@ -996,6 +999,78 @@ int hyb_noise_reference_f64(hyb_ctx* ctx, const double* f, size_t pitch, const d
     return HYB_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// Host-buffer stacks: slices move in chunks of ~8 MB through three streams so the two PCIe
+// directions and the kernels overlap -- copy stream: H2D of chunk k; compute stream: the hybrid
+// of chunk k (slices are independent, each with its own noise sum); copy2 stream: D2H of chunk k.
+// Returns false (nothing enqueued) when the layout does not fit.
+bool batch_host_pipelined(hyb_ctx* ctx, const uint8_t* g, size_t pitch, size_t slice_stride, int n_slices,
+                          int rows, int cols, int smax, int win, uint8_t* y, size_t y_pitch, size_t y_slice_stride,
+                          unsigned long long* W, int* status) {
+    *status = HYB_OK;
+    const size_t pp = round_pitch(cols), ps = pp * rows;
+    const size_t slice_bytes = (size_t)cols * rows;
+    if (slice_stride != pitch * rows || y_slice_stride != y_pitch * rows) return false;
+    int per = (int)std::max<size_t>(1, ((size_t)8 << 20) / slice_bytes);
+    int K = (n_slices + per - 1) / per;
+    if (K < 2) return false;
+    if (K > hyb_ctx::kMaxChunks) {
+        K = hyb_ctx::kMaxChunks;
+        per = (n_slices + K - 1) / K;
+        K = (n_slices + per - 1) / per;
+    }
+    cudaStream_t cs = ctx->stream, xs = ctx->copy, ys = ctx->copy2;
+    auto run = [&]() -> cudaError_t {
+        cudaError_t e;
+        auto cp = [&](void* dst, size_t dp, const void* src, size_t sp, int nrows, cudaStream_t st) {
+            if (dp == (size_t)cols && sp == (size_t)cols)
+                return cudaMemcpyAsync(dst, src, (size_t)cols * nrows, cudaMemcpyDefault, st);
+            return cudaMemcpy2DAsync(dst, dp, src, sp, (size_t)cols, (size_t)nrows, cudaMemcpyDefault, st);
+        };
+        // both copy streams start after earlier compute-stream work
+        if ((e = cudaEventRecord(ctx->ev_gain[0], cs)) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(xs, ctx->ev_gain[0], 0)) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(ys, ctx->ev_gain[0], 0)) != cudaSuccess) return e;
+        if ((e = cudaMemsetAsync(W, 0, sizeof(long long) * n_slices, cs)) != cudaSuccess) return e;
+        for (int k = 0; k < K; ++k) {
+            const int z0 = k * per, nz = std::min(per, n_slices - z0);
+            if ((e = cp(ctx->in.ptr + ps * z0, pp, g + slice_stride * z0, pitch, rows * nz, xs)) != cudaSuccess)
+                return e;
+            if ((e = cudaEventRecord(ctx->ev_h2d[k], xs)) != cudaSuccess) return e;
+        }
+        for (int k = 0; k < K; ++k) {
+            const int z0 = k * per, nz = std::min(per, n_slices - z0);
+            if ((e = cudaStreamWaitEvent(cs, ctx->ev_h2d[k], 0)) != cudaSuccess) return e;
+            hyb::Plane a{ctx->in.ptr + ps * z0, pp, ps, ctx->f.ptr + ps * z0, pp, ps, rows, cols, 0, rows, nz};
+            if ((e = run_amf(ctx, a, smax, nullptr, 0, 0)) != cudaSuccess) return e;
+            hyb::Plane w{ctx->f.ptr + ps * z0, pp, ps, ctx->out.ptr + ps * z0, pp, ps, rows, cols, 0, rows, nz};
+            if ((e = hyb::launch_wiener_stats(w, win, W + z0, cs)) != cudaSuccess) return e;
+            if ((e = hyb::launch_wiener_gain(w, win, reinterpret_cast<const long long*>(W + z0),
+                                             (long long)rows * cols, cs)) != cudaSuccess)
+                return e;
+            if ((e = cudaEventRecord(ctx->ev_gain[k], cs)) != cudaSuccess) return e;
+            if ((e = cudaStreamWaitEvent(ys, ctx->ev_gain[k], 0)) != cudaSuccess) return e;
+            if ((e = cp(y + y_slice_stride * z0, y_pitch, ctx->out.ptr + ps * z0, pp, rows * nz, ys)) != cudaSuccess)
+                return e;
+        }
+        // the compute stream resumes after the last download and the last upload
+        if ((e = cudaEventRecord(ctx->ev_h2d[0], ys)) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(cs, ctx->ev_h2d[0], 0)) != cudaSuccess) return e;
+        if ((e = cudaEventRecord(ctx->ev_h2d[1], xs)) != cudaSuccess) return e;
+        return cudaStreamWaitEvent(cs, ctx->ev_h2d[1], 0);
+    };
+    const cudaError_t e = run();
+    if (e != cudaSuccess) *status = cuda_fail(ctx, e, "batch pipeline");
+    return true;
+}
+
+}  // namespace
+
+extern "C" {
+
 int hyb_hybrid_batch_u8(hyb_ctx* ctx, const uint8_t* g, size_t pitch, size_t slice_stride,
                         int n_slices, int rows, int cols, int smax, int win, uint8_t* y,
                         size_t y_pitch, size_t y_slice_stride, int64_t* noise_sums) {
@@ -1011,6 +1086,26 @@ int hyb_hybrid_batch_u8(hyb_ctx* ctx, const uint8_t* g, size_t pitch, size_t sli
     HYB_CHECK(cudaSetDevice(ctx->device));
     const bool dg = is_device_ptr(g) && hyb::tma_compatible(g, pitch, slice_stride), dy = is_device_ptr(y);
     const size_t pp = round_pitch(cols), ps = pp * rows;
+    if (!dg && !dy && !is_device_ptr(g)) {
+        HYB_CHECK(ctx->in.ensure(ps * n_slices));
+        HYB_CHECK(ctx->out.ensure(ps * n_slices));
+        HYB_CHECK(ctx->f.ensure(ps * n_slices));
+        HYB_CHECK(ctx->wsum.ensure(sizeof(long long) * n_slices));
+        unsigned long long* W = reinterpret_cast<unsigned long long*>(ctx->wsum.ptr);
+        if (batch_host_pipelined(ctx, g, pitch, slice_stride, n_slices, rows, cols, smax, win, y, y_pitch,
+                                 y_slice_stride, W, &st)) {
+            if (st) return st;
+            if (noise_sums) {
+                if ((st = ensure_host_w(ctx, n_slices))) return st;
+                HYB_CHECK(cudaMemcpyAsync(ctx->host_w, W, sizeof(long long) * n_slices, cudaMemcpyDeviceToHost,
+                                          ctx->stream));
+            }
+            HYB_CHECK(cudaStreamSynchronize(ctx->stream));
+            if (noise_sums)
+                for (int z = 0; z < n_slices; ++z) noise_sums[z] = ctx->host_w[z];
+            return HYB_OK;
+        }
+    }
     const uint8_t* s = g;
     size_t sp = pitch, ss = slice_stride;
     if (!dg) {

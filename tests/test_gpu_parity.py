@@ -4,6 +4,8 @@ AMF: bit-exact (BASELINE.json north_star).  W1 Wiener: the kernel computes the e
 result (fp32 with an exact int128 tie check), so it is held to bit-exactness too -- stricter than
 the north_star tolerance (<= 1 LSB, >= 99.99 % exact), which is asserted as well.
 """
+import ctypes
+
 import numpy as np
 import pytest
 import torch
@@ -223,6 +225,28 @@ def test_hybrid_batch_matches_per_slice(ctx):
         ref_y, ref_w = oracle.hybrid(stack[s], c["smax"], c["win"])
         assert ws[s] == ref_w
         np.testing.assert_array_equal(y[s], ref_y)
+
+
+def test_hybrid_batch_pipelined_host_buffers(ctx):
+    """Host stacks larger than one ~8 MB chunk take the three-stream pipelined path (H2D / hybrid /
+    D2H per chunk): same output and per-slice W as the oracle, pageable and pinned buffers."""
+    import torch
+    c = CONFIGS[3]
+    n = 40  # 512 x 512 slices: chunks of 32 -> 2 chunks
+    stack = np.stack([capi.make_phantom(512, 512, 12, c["sigma"], c["density"], s) for s in range(n)])
+    y, ws = denoise.hybrid_denoise_batch(stack, c["smax"], c["win"])
+    refs = [oracle.hybrid(stack[s], c["smax"], c["win"]) for s in range(n)]
+    for s in range(n):
+        assert ws[s] == refs[s][1]
+        np.testing.assert_array_equal(y[s], refs[s][0])
+    h_in = torch.from_numpy(stack).pin_memory()
+    h_out = torch.empty_like(h_in).pin_memory()
+    w = (ctypes.c_int64 * n)()
+    capi.check(capi.lib.hyb_hybrid_batch_u8(ctx.ptr, h_in.data_ptr(), 512, 512 * 512, n, 512, 512, c["smax"], c["win"],
+                                            h_out.data_ptr(), 512, 512 * 512, w), ctx.ptr)
+    for s in range(n):
+        assert w[s] == refs[s][1]
+        np.testing.assert_array_equal(h_out[s].numpy(), refs[s][0])
 
 
 # ---------------------------------------------------------------- errors
