@@ -215,27 +215,40 @@ struct GArgs {
 // in-tile rank falls in the segment) are pooled into one shared-memory queue (entry = slot << 12 |
 // pixel), and every level round k = 5..smax runs over the whole pool.
 
-inline size_t grow_smem(const GGeo& g) { return GHDR + (size_t)GSLOTS * g.b_bytes + 2 * GCAP * 2 + 128; }
+// Two growth variants, chosen per call by smax: "wide" (k = 9 by selection network, 114 registers,
+// 2 CTAs/SM, batches of 8 tiles / 8192 failures) pays off when the k = 9 level is dense (BASELINE
+// config 4: smax 11, S&P 0.5); "lean" (networks up to k = 7, radix above, <= 80 registers, 3 CTAs/SM,
+// batches of 6 tiles / 4096 failures) when it is sparse or absent (config 2: 3.7 % faster step).
+template <int NETMAX_, int MINB_, int SLOTS_, int CAP_>
+struct GrowCfg {
+    static constexpr int NETMAX = NETMAX_, MINB = MINB_, SLOTS = SLOTS_, CAP = CAP_;
+};
+using GrowWide = GrowCfg<9, 2, 8, 8192>;
+using GrowLean = GrowCfg<7, 3, 6, 4096>;
+static_assert(GrowWide::SLOTS <= 8 && GrowLean::SLOTS <= 8, "header layout");
+
+template <class C>
+inline size_t grow_smem(const GGeo& g) { return GHDR + (size_t)C::SLOTS * g.b_bytes + 2 * C::CAP * 2 + 128; }
 
 
-template <bool FIN>
-__global__ void __launch_bounds__(GNT, 2) amf_grow_kernel(const __grid_constant__ CUtensorMap tm,
+template <bool FIN, class C>
+__global__ void __launch_bounds__(GNT, C::MINB) amf_grow_kernel(const __grid_constant__ CUtensorMap tm,
                                                       const __grid_constant__ GArgs args) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
     const GGeo& geo = args.geo;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);            // [GSLOTS]
-    int* sinfo = reinterpret_cast<int*>(smem + 64);                // [GSLOTS][8]: x0 y0 z tile lo hi qbase border
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);            // [SLOTS]
+    int* sinfo = reinterpret_cast<int*>(smem + 64);                // [SLOTS][8]: x0 y0 z tile lo hi qbase border
     long long* cur = reinterpret_cast<long long*>(smem + 320);     // [0] record, [1] global failure position
     int* ctl = reinterpret_cast<int*>(smem + 336);                 // [0] segments, [1] queue n
     int* qcount = reinterpret_cast<int*>(smem + 384);              // [MAX_LEVELS]
     uint8_t* bufs = smem + GHDR;
-    uint16_t* Q0 = reinterpret_cast<uint16_t*>(bufs + (size_t)GSLOTS * geo.b_bytes);
-    uint16_t* Q1 = Q0 + GCAP;
+    uint16_t* Q0 = reinterpret_cast<uint16_t*>(bufs + (size_t)C::SLOTS * geo.b_bytes);
+    uint16_t* Q1 = Q0 + C::CAP;
     const int tid = threadIdx.x;
     const int per_slice = args.tiles_x * args.tiles_y;
     if (tid == 0) {
-        for (int i = 0; i < GSLOTS; ++i) mbar_init(&bar[i], 1);
+        for (int i = 0; i < C::SLOTS; ++i) mbar_init(&bar[i], 1);
         prefetch_tmap(&tm);
         fence_mbar_init();
     }
@@ -245,15 +258,15 @@ __global__ void __launch_bounds__(GNT, 2) amf_grow_kernel(const __grid_constant_
     const long long gbeg = T * blockIdx.x / gridDim.x, gend = T * (blockIdx.x + 1) / gridDim.x;
     uint32_t phases = 0;
     const GrowSmem sm{bar, sinfo, cur, ctl, qcount, bufs, Q0, Q1};
-    grow_range<FIN, GNT>(&tm, geo, sm, args.bitmap, args.records, R, T, gbeg, gend, per_slice, args.tiles_x,
-                         args.row_begin, args.rows, args.cols, args.smax, phases,
-                         [&](const int* si, int pix, uint8_t v, int k) {
-                             const size_t row = (size_t)(si[1] - args.row_begin + (pix >> 7));
-                             args.dst[(size_t)si[2] * args.dslice + row * args.dpitch + si[0] + (pix & 127)] = v;
-                             if (FIN)
-                                 args.fin[(size_t)si[2] * args.fslice + row * args.fpitch + si[0] + (pix & 127)] =
-                                     (uint8_t)k;
-                         });
+    auto out = [&](const int* si, int pix, uint8_t v, int k) {
+        const size_t row = (size_t)(si[1] - args.row_begin + (pix >> 7));
+        args.dst[(size_t)si[2] * args.dslice + row * args.dpitch + si[0] + (pix & 127)] = v;
+        if (FIN) args.fin[(size_t)si[2] * args.fslice + row * args.fpitch + si[0] + (pix & 127)] = (uint8_t)k;
+    };
+    grow_range<FIN, GNT, decltype(out), C::SLOTS, C::CAP, C::NETMAX>(&tm, geo, sm, args.bitmap, args.records, R, T,
+                                                                     gbeg, gend, per_slice, args.tiles_x,
+                                                                     args.row_begin, args.rows, args.cols, args.smax,
+                                                                     phases, out);
     TRACE(1, 15);
     // the last CTA resets the record counter for the next k = 3 launch
     if (tid == 0) {
@@ -338,13 +351,16 @@ cudaError_t launch_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, si
 
     // ---- growth: one batched launch for every window size k = 5..smax ----
     const GGeo geo = make_ggeo(smax);
-    const size_t gsm = grow_smem(geo);
-    auto kern = fin ? amf_grow_kernel<true> : amf_grow_kernel<false>;
-    static size_t gconfigured[2] = {0, 0};
-    if (gsm > gconfigured[fin ? 1 : 0]) {
+    const bool wide = smax >= 11;
+    const size_t gsm = wide ? grow_smem<GrowWide>(geo) : grow_smem<GrowLean>(geo);
+    auto kern = wide ? (fin ? amf_grow_kernel<true, GrowWide> : amf_grow_kernel<false, GrowWide>)
+                     : (fin ? amf_grow_kernel<true, GrowLean> : amf_grow_kernel<false, GrowLean>);
+    const int vi = (fin ? 1 : 0) + (wide ? 2 : 0);
+    static size_t gconfigured[4] = {0, 0, 0, 0};
+    if (gsm > gconfigured[vi]) {
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm);
         if (e != cudaSuccess) return e;
-        gconfigured[fin ? 1 : 0] = gsm;
+        gconfigured[vi] = gsm;
     }
     CUtensorMap tm_g;
     e = make_tmap_u8(&tm_g, p.src, p.cols, p.rows, p.n_slices, p.spitch, p.sslice, geo.box_w, geo.box_h);
@@ -369,13 +385,13 @@ cudaError_t launch_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, si
     g.rec_ctr = a.rec_ctr;
     g.records = work.records;
     g.done = work.counters + 4;
-    static size_t occ_key[2] = {0, 0};
-    static int occ_val[2] = {1, 1};
-    int& gper_sm = occ_val[fin ? 1 : 0];
-    if (occ_key[fin ? 1 : 0] != gsm) {
+    static size_t occ_key[4] = {0, 0, 0, 0};
+    static int occ_val[4] = {1, 1, 1, 1};
+    int& gper_sm = occ_val[vi];
+    if (occ_key[vi] != gsm) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&gper_sm, kern, GNT, gsm);
         if (gper_sm < 1) gper_sm = 1;
-        occ_key[fin ? 1 : 0] = gsm;
+        occ_key[vi] = gsm;
     }
     // every resident CTA slot busy; each CTA takes a contiguous run of tiles
     const int ggrid = (int)std::min<long long>(ntiles, (long long)g_num_sms * gper_sm);

@@ -503,8 +503,14 @@ __device__ __forceinline__ void grow_tile_load(const CUtensorMap* tm, const GGeo
 constexpr int REC_SHIFT = 40;
 constexpr int REC_W = 128;  // growth balancing weight of one tile load, in failures
 constexpr unsigned long long REC_MASK = (1ull << REC_SHIFT) - 1;
-constexpr int GSLOTS = 8;      // tile segments per growth batch
-constexpr int GCAP = 8192;     // pooled queue capacity
+#ifndef HYB_GSLOTS
+#define HYB_GSLOTS 8
+#endif
+#ifndef HYB_GCAP
+#define HYB_GCAP 8192
+#endif
+constexpr int GSLOTS = HYB_GSLOTS;  // tile segments per growth batch
+constexpr int GCAP = HYB_GCAP;      // pooled queue capacity
 constexpr int MAX_LEVELS = 128;
 
 __device__ __forceinline__ long long rec_off(const unsigned long long* rec, long long i) {
@@ -653,7 +659,7 @@ struct GrowSmem {
     uint16_t* Q1;    // [GCAP]
 };
 
-template <bool FIN, int NTHR, class Out>
+template <bool FIN, int NTHR, class Out, int SLOTS = GSLOTS, int CAP = GCAP, int NETMAX = HYB_GROW_NETMAX>
 __device__ __forceinline__ void grow_range(const CUtensorMap* tm, const GGeo& geo, const GrowSmem& sm,
                                            const uint8_t* bitmap, const unsigned long long* records, long long R,
                                            long long T, long long gbeg, long long gend, int per_slice, int tiles_x,
@@ -708,7 +714,7 @@ __device__ __forceinline__ void grow_range(const CUtensorMap* tm, const GGeo& ge
             long long take = 0, off = 0, nxt = 0, flo = 0, whi = 0;
             int tile = 0;
             bool valid = false;
-            if (rec < R && lane < GSLOTS) {
+            if (rec < R && lane < SLOTS) {
                 const unsigned long long rv = __ldcg(records + rec);
                 off = (long long)(rv >> 24);
                 tile = (int)(rv & 0xFFFFFFu);
@@ -728,8 +734,8 @@ __device__ __forceinline__ void grow_range(const CUtensorMap* tm, const GGeo& ge
                 if (lane >= d) incl += v;
             }
             const long long excl = incl - take;
-            const bool within = valid && excl < GCAP;
-            const long long mine = within ? min(take, (long long)GCAP - excl) : 0;
+            const bool within = valid && excl < CAP;
+            const long long mine = within ? min(take, (long long)CAP - excl) : 0;
             const uint32_t segs = __ballot_sync(0xFFFFFFFFu, mine > 0);
             const uint32_t inside = __ballot_sync(0xFFFFFFFFu, within);  // lanes 0..k (lane 0 always)
             const int ns = __popc(segs);
@@ -826,8 +832,8 @@ __device__ __forceinline__ void grow_range(const CUtensorMap* tm, const GGeo& ge
         GTRACE(3);
         // ---- 4. levels, pooled over the batch ----
         int n = ctl[1];
-        grow_levels<FIN, NTHR>(bufs, geo, Q0, Q1, qcount, n, smax,
-                               [&](int sl, int pix, uint8_t v, int k) { out(sinfo + 8 * sl, pix, v, k); });
+        auto slot_out = [&](int sl, int pix, uint8_t v, int k) { out(sinfo + 8 * sl, pix, v, k); };
+        grow_levels<FIN, NTHR, decltype(slot_out), NETMAX>(bufs, geo, Q0, Q1, qcount, n, smax, slot_out);
         __syncthreads();  // slots, queues and counters are reused by the next batch
 #ifdef HYB_TRACE
         if (tid == 0 && blockIdx.x < 1024) g_trace[(1024 + blockIdx.x) * 16 + 4] += 1;
