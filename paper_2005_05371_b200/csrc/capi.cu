@@ -692,7 +692,8 @@ int hyb_hybrid_u8(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int co
     // direct launches than as graph nodes, so those calls are not captured.
     const bool coop_small = !ctx->exclusive && parts == 1 && hyb::plan_small(rows, cols, smax, win).ok;
     const bool graphable = !coop_small && !stats && gok && yok && ga.type != cudaMemoryTypeUnregistered &&
-                           ya.type != cudaMemoryTypeUnregistered && ctx->stream != nullptr;
+                           ya.type != cudaMemoryTypeUnregistered && ctx->stream != nullptr &&
+                           ctx->stream != cudaStreamLegacy && ctx->stream != cudaStreamPerThread;  // not capturable
     if (!graphable) return hybrid_u8_impl(ctx, g, pitch, rows, cols, smax, win, parts, y, y_pitch, stats, false);
     const hyb_ctx::GraphKey key{g, y, pitch, y_pitch, rows, cols, smax, win, parts, ctx->stream};
     auto it = ctx->graphs.find(key);

@@ -9,6 +9,7 @@ reference's k/255 doubles map onto uint8 exactly for this path (SURVEY.md findin
 from __future__ import annotations
 
 import ctypes
+import sys
 from dataclasses import dataclass
 
 import numpy as np
@@ -18,7 +19,21 @@ from .capi import InvalidArgument, check, lib
 
 
 def _ctx(ctx):
-    return (ctx or capi.default_context()).ptr
+    c = ctx or capi.default_context()
+    _bind_torch_stream(c)
+    return c.ptr
+
+
+def _bind_torch_stream(c) -> None:
+    """Device-pointer calls are stream-ordered on the context stream (include/hybrid_cuda.h), so the
+    torch-facing mirror runs them on torch's current stream: inputs produced and outputs consumed by
+    torch are ordered with the kernels, as the reference's by-value calls are.  torch's default
+    stream is the legacy stream (handle 0), passed as cudaStreamLegacy (1)."""
+    torch = sys.modules.get("torch")
+    if torch is None or not torch.cuda.is_available() or not torch.cuda.is_initialized():
+        return
+    h = torch.cuda.current_stream(c.device).cuda_stream
+    c.set_stream(h if h else 1)
 
 
 def _is_torch(a) -> bool:

@@ -249,6 +249,23 @@ def test_hybrid_batch_pipelined_host_buffers(ctx):
         np.testing.assert_array_equal(h_out[s].numpy(), refs[s][0])
 
 
+def test_mirror_calls_are_ordered_with_torch_streams(ctx):
+    """Device-pointer calls are stream-ordered on the context stream; the Python mirror binds it to
+    torch's current stream, so torch ops before and after a call see its inputs / outputs (found by the
+    config-4 full-size test: an unordered .cpu() read f while the growth kernel still wrote it)."""
+    c = CONFIGS[4]
+    g = capi.make_phantom(2048, 2048, 32, c["sigma"], c["density"], 5)
+    want = oracle.amf(g, c["smax"])
+    h = torch.from_numpy(g).pin_memory()
+    for stream in (torch.cuda.current_stream(), torch.cuda.Stream()):
+        with torch.cuda.stream(stream):
+            for rep in range(3):
+                gd = torch.empty((2048, 2048), dtype=torch.uint8, device="cuda")
+                gd.copy_(h, non_blocking=True)  # input produced on the torch stream
+                out = denoise.adaptive_median_serial(gd, c["smax"], ctx=ctx)
+                np.testing.assert_array_equal(out.cpu().numpy(), want, err_msg=f"rep {rep}")
+
+
 # ---------------------------------------------------------------- errors
 
 def test_errors_match_reference_text(ctx):
