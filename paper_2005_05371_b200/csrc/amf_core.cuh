@@ -66,10 +66,13 @@ __device__ __forceinline__ int zero_bytes(uint32_t x, uint32_t v80) {
 // columns >= col_lim are outside the output), stages them in the warp's O / F areas, and, when
 // bm_tile is set, the level-A failure bits of the strip into the tile's 512-byte bitmap.  Returns the
 // strip's failure count (warp-uniform).
+// With q set, the failures are also appended to the shared-memory queue q (entries qslot | pixel, one
+// shared atomic on *qctr per strip) -- the fused kernel's growth queue, built without a bitmap pass.
 template <bool FIN>
 __device__ __forceinline__ int k3_strip(const uint8_t* __restrict__ B, uint8_t* O, uint8_t* F, int sub,
                                         uint8_t* bm_tile, uint8_t* dst_tile, size_t dpitch, uint8_t* fin_tile,
-                                        size_t fpitch, int tile_row_lim, int col_lim) {
+                                        size_t fpitch, int tile_row_lim, int col_lim, uint16_t* q = nullptr,
+                                        int* qctr = nullptr, uint32_t qslot = 0) {
     const int lane = threadIdx.x & 31;
     // ---- k = 3: lane = rows (r0, r0+1) x columns c0..c0+7, u16x2 lanes = the two rows ----
     const int lr = 2 * (lane >> 4);  // local row within the strip
@@ -158,7 +161,7 @@ __device__ __forceinline__ int k3_strip(const uint8_t* __restrict__ B, uint8_t* 
     // ---- level-A failures (inside the output range) -> the tile's failure bitmap (no atomics:
     //      every bitmap byte of the tile is written by exactly one lane) ----
     int nf = 0;
-    if (bm_tile) {
+    if (bm_tile || q) {
         const uint32_t rv = __brev(failbits);                     // bit 16+j: row lr; bit j: row lr+1
         uint32_t m = ((rv >> 16) & 0xFFu) | ((rv & 0xFFu) << 8);  // bit j: row lr; bit 8+j: row lr+1
         if (lr >= row_lim) m &= 0xFF00u;
@@ -167,10 +170,33 @@ __device__ __forceinline__ int k3_strip(const uint8_t* __restrict__ B, uint8_t* 
             const uint32_t cm = col_lim <= c0 ? 0u : ((1u << (col_lim - c0)) - 1u);
             m &= cm | (cm << 8);
         }
-        uint8_t* bm = bm_tile + (sub * WR + lr) * 16 + (c0 >> 3);
-        bm[0] = (uint8_t)m;
-        bm[16] = (uint8_t)(m >> 8);
-        nf = __reduce_add_sync(0xFFFFFFFFu, __popc(m));
+        if (bm_tile) {
+            uint8_t* bm = bm_tile + (sub * WR + lr) * 16 + (c0 >> 3);
+            bm[0] = (uint8_t)m;
+            bm[16] = (uint8_t)(m >> 8);
+        }
+        const int c = __popc(m);
+        if (q) {
+            int incl = c;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+                if (lane >= d) incl += v;
+            }
+            int base = 0;
+            if (lane == 31 && incl) base = atomicAdd(qctr, incl);
+            base = __shfl_sync(0xFFFFFFFFu, base, 31);
+            int pos = base + incl - c;
+            const uint32_t pbase = qslot | (uint32_t)((sub * WR + lr) * TW + c0);
+            while (m) {
+                const int b = __ffs(m) - 1;
+                m &= m - 1;
+                q[pos++] = (uint16_t)(pbase + (uint32_t)((b >> 3) * TW + (b & 7)));
+            }
+            nf = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        } else {
+            nf = __reduce_add_sync(0xFFFFFFFFu, c);
+        }
     }
     __syncwarp();
 

@@ -5,9 +5,9 @@
 // Per CTA (tiles t = blockIdx.x + i * gridDim.x, i < STPC):
 //   A  TMA-load each tile of g with the growth halo R = (smax-1)/2, replicate edges, run the k = 3
 //      strips (warp w: strip w of every tile; amf_core.cuh k3_strip) writing f to global memory and
-//      the failure bitmaps to shared memory;
-//   B  pool the failures of the CTA's tiles into one queue and run the growth levels k = 5..smax from
-//      the resident tiles (amf_core.cuh grow_levels) -- no second launch, no reload;
+//      appending their level-A failures to one shared-memory queue (one shared atomic per strip);
+//   B  run the growth levels k = 5..smax over that pooled queue from the resident tiles
+//      (amf_core.cuh grow_levels) -- no second launch, no reload, no bitmap pass;
 //   -- grid barrier (f complete; CTA 0 has zeroed W) --
 //   C  TMA-load each tile of f with the W1 halo into the same slots, statistics per 128 x 8
 //      sub-tile (w1_core.cuh), one atomic per CTA into W;
@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(SNT, SMIN) hybrid_small_kernel(const __grid_co
     const int nt = (a.ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;  // my tiles (<= STPC)
 
     TRACE(0, 0);
-    // ---- A: own g tiles (+ growth halo R) by TMA, edges, k = 3 (f, failure bitmaps in shared memory) ----
+    // ---- A: own g tiles (+ growth halo R) by TMA, edges, k = 3 (f; failures queued in Q0) ----
     if (tid == 0) {
         if (blockIdx.x == 0) {
             a.times[0] = gtimer();
@@ -158,8 +158,8 @@ __global__ void __launch_bounds__(SNT, SMIN) hybrid_small_kernel(const __grid_co
             const int i = j / NW;
             const int x0 = tinfo[2 * i], y0 = tinfo[2 * i + 1];
             const uint8_t* B = slots + (size_t)i * a.slot_bytes + (size_t)(geo.R - 1) * geo.BS;  // row 0 = y0 - 1
-            k3_strip<false>(B, O, O, j % NW, a.smax >= 5 ? bitmaps + i * 512 : nullptr,
-                            a.f + (size_t)y0 * a.fpitch + x0, a.fpitch, nullptr, 0, a.rows - y0, a.cols - x0);
+            k3_strip<false>(B, O, O, j % NW, nullptr, a.f + (size_t)y0 * a.fpitch + x0, a.fpitch, nullptr, 0,
+                            a.rows - y0, a.cols - x0, a.smax >= 5 ? Q0 : nullptr, qcount, (uint32_t)i << 12);
         }
     }
     __syncthreads();
@@ -167,9 +167,7 @@ __global__ void __launch_bounds__(SNT, SMIN) hybrid_small_kernel(const __grid_co
 
     // ---- B: growth over the pooled failures of the resident tiles ----
     if (a.smax >= 5) {
-        const int total = cta_bitmap_queue<SNT>(reinterpret_cast<const uint32_t*>(bitmaps), nt * 128, Q0,
-                                                reinterpret_cast<uint16_t*>(stage),
-                                                reinterpret_cast<int*>(stage + 2048));
+        const int total = qcount[0];  // the k = 3 strips appended their failures to Q0
         TRACE(0, 4);
 #ifdef HYB_TRACE
         if (tid == 0 && blockIdx.x < 1024) {
