@@ -218,13 +218,13 @@ struct GArgs {
 // Two growth variants, chosen per call by smax: "wide" (k = 9 by selection network, 114 registers,
 // 2 CTAs/SM, batches of 8 tiles / 8192 failures) pays off when the k = 9 level is dense (BASELINE
 // config 4: smax 11, S&P 0.5); "lean" (networks up to k = 7, radix above, <= 80 registers, 3 CTAs/SM,
-// batches of 6 tiles / 4096 failures) when it is sparse or absent (config 2: 3.7 % faster step).
+// batches of 8 tiles / 4096 failures) when it is sparse or absent (config 2: 6 % faster step).
 template <int NETMAX_, int MINB_, int SLOTS_, int CAP_>
 struct GrowCfg {
     static constexpr int NETMAX = NETMAX_, MINB = MINB_, SLOTS = SLOTS_, CAP = CAP_;
 };
 using GrowWide = GrowCfg<9, 2, 8, 8192>;
-using GrowLean = GrowCfg<7, 3, 6, 4096>;
+using GrowLean = GrowCfg<7, 3, 8, 4096>;
 static_assert(GrowWide::SLOTS <= 8 && GrowLean::SLOTS <= 8, "header layout");
 
 template <class C>
