@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(K3T, 3)
 
 constexpr int GNT = 256;         // threads per growth CTA
 
-constexpr int GHDR = 1024;       // mbarriers, tile coordinates, level counters, scan scratch
+constexpr int GHDR = 1536;       // mbarriers, tile coordinates, level counters, scan scratch
 
 inline size_t grow_smem(const GGeo& g);
 
@@ -228,7 +228,9 @@ using GrowLean = GrowCfg<7, 3, 8, 4096>;
 static_assert(GrowWide::SLOTS <= 8 && GrowLean::SLOTS <= 8, "header layout");
 
 template <class C>
-inline size_t grow_smem(const GGeo& g) { return GHDR + (size_t)C::SLOTS * g.b_bytes + 2 * C::CAP * 2 + 128; }
+inline size_t grow_smem(const GGeo& g) {
+    return GHDR + (size_t)C::SLOTS * g.b_bytes + 2 * C::CAP * 2 + (size_t)C::SLOTS * 512 + 128;
+}
 
 
 template <bool FIN, class C>
@@ -240,15 +242,20 @@ __global__ void __launch_bounds__(GNT, C::MINB) amf_grow_kernel(const __grid_con
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem);            // [SLOTS]
     int* sinfo = reinterpret_cast<int*>(smem + 64);                // [SLOTS][8]: x0 y0 z tile lo hi qbase border
     long long* cur = reinterpret_cast<long long*>(smem + 320);     // [0] record, [1] global failure position
-    int* ctl = reinterpret_cast<int*>(smem + 336);                 // [0] segments, [1] queue n
+    int* ctl = reinterpret_cast<int*>(smem + 336);                 // [4] segments, queue n, more
     int* qcount = reinterpret_cast<int*>(smem + 384);              // [MAX_LEVELS]
     uint8_t* bufs = smem + GHDR;
     uint16_t* Q0 = reinterpret_cast<uint16_t*>(bufs + (size_t)C::SLOTS * geo.b_bytes);
     uint16_t* Q1 = Q0 + C::CAP;
+    int* sinfo_n = reinterpret_cast<int*>(smem + 1024);            // [SLOTS][8] next batch
+    int* ctl_n = reinterpret_cast<int*>(smem + 1280);              // [4]
+    uint64_t* bmbar = reinterpret_cast<uint64_t*>(smem + 1344);    // next batch's bitmap copies
+    uint32_t* bms = reinterpret_cast<uint32_t*>(Q1 + C::CAP);      // [SLOTS][128]
     const int tid = threadIdx.x;
     const int per_slice = args.tiles_x * args.tiles_y;
     if (tid == 0) {
         for (int i = 0; i < C::SLOTS; ++i) mbar_init(&bar[i], 1);
+        mbar_init(bmbar, 1);
         prefetch_tmap(&tm);
         fence_mbar_init();
     }
@@ -257,7 +264,7 @@ __global__ void __launch_bounds__(GNT, C::MINB) amf_grow_kernel(const __grid_con
     const long long R = (long long)(ctr >> REC_SHIFT), T = (long long)(ctr & REC_MASK);
     const long long gbeg = T * blockIdx.x / gridDim.x, gend = T * (blockIdx.x + 1) / gridDim.x;
     uint32_t phases = 0;
-    const GrowSmem sm{bar, sinfo, cur, ctl, qcount, bufs, Q0, Q1};
+    const GrowSmem sm{bar, sinfo, cur, ctl, qcount, bufs, Q0, Q1, sinfo_n, ctl_n, bms, bmbar};
     auto out = [&](const int* si, int pix, uint8_t v, int k) {
         const size_t row = (size_t)(si[1] - args.row_begin + (pix >> 7));
         args.dst[(size_t)si[2] * args.dslice + row * args.dpitch + si[0] + (pix & 127)] = v;

@@ -675,14 +675,18 @@ __device__ __forceinline__ void grow_levels(const uint8_t* bufs, const GGeo& geo
 // stores a result, si = {x0, y0, z, ...} of the pixel's tile.  `phases` carries the slot mbarrier
 // parities across calls.
 struct GrowSmem {
-    uint64_t* bar;   // [GSLOTS] (initialised by the caller)
-    int* sinfo;      // [GSLOTS][8]: x0 y0 z tile lo hi qbase border
-    long long* cur;  // [2]: record, position
-    int* ctl;        // [3]
+    uint64_t* bar;   // [SLOTS] tile slots (initialised by the caller)
+    int* sinfo;      // [SLOTS][8]: x0 y0 z tile lo hi qbase border -- the batch being grown
+    long long* cur;  // [2]: record, position of the next choice
+    int* ctl;        // [4]: segments, queue n, more, bitmaps issued -- the batch being grown
     int* qcount;     // [MAX_LEVELS]
-    uint8_t* bufs;   // [GSLOTS][geo.b_bytes]
-    uint16_t* Q0;    // [GCAP]
-    uint16_t* Q1;    // [GCAP]
+    uint8_t* bufs;   // [SLOTS][geo.b_bytes]
+    uint16_t* Q0;    // [CAP]
+    uint16_t* Q1;    // [CAP]
+    int* sinfo_n;    // [SLOTS][8] the next batch (chosen one batch ahead)
+    int* ctl_n;      // [4]
+    uint32_t* bms;   // [SLOTS][128] the next batch's failure bitmaps (bulk-copied ahead)
+    uint64_t* bmbar; // [1] their mbarrier (initialised by the caller)
 };
 
 template <bool FIN, int NTHR, class Out, int SLOTS = GSLOTS, int CAP = GCAP, int NETMAX = HYB_GROW_NETMAX>
@@ -691,6 +695,7 @@ __device__ __forceinline__ void grow_range(const CUtensorMap* tm, const GGeo& ge
                                            long long T, long long gbeg, long long gend, int per_slice, int tiles_x,
                                            int row_begin, int rows, int cols, int smax, uint32_t& phases, Out out) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NWARP = NTHR / 32;
     uint64_t* bar = sm.bar;
     int* sinfo = sm.sinfo;
     long long* cur = sm.cur;
@@ -699,9 +704,10 @@ __device__ __forceinline__ void grow_range(const CUtensorMap* tm, const GGeo& ge
     uint8_t* bufs = sm.bufs;
     uint16_t* Q0 = sm.Q0;
     uint16_t* Q1 = sm.Q1;
+    uint32_t bmphase = 0;
 #ifdef HYB_TRACE
-    // growth batch profile (kernel id 1): slot 1 += segment choice, 2 += queue build, 3 += tile wait +
-    // edges, 4 += batches, 13 += kernel entry to the first batch
+    // growth batch profile (kernel id 1): slot 1 += promotion + tile loads issued, 2 += queue build,
+    // 3 += tile wait + edges, 4 += batches, 13 += kernel entry to the first batch
     unsigned long long tt0 = 0, tt1 = 0;
     auto tnow = [] { unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; };
     auto tacc = [&](int slot) {
@@ -728,82 +734,103 @@ __device__ __forceinline__ void grow_range(const CUtensorMap* tm, const GGeo& ge
             cur[1] = gbeg;
         }
     }
+    __syncwarp();
+
+    // One warp chooses the next batch (lane l: record cur + l) into sinfo_n / ctl_n and bulk-copies its
+    // tiles' failure bitmaps into bms.  Positions are weighted: record r spans [off, next) = REC_W units
+    // for its tile load, then its failures.
+    auto choose = [&]() {
+        const long long rec = cur[0] + lane, pos = cur[1];
+        long long take = 0, off = 0, nxt = 0, flo = 0, whi = 0;
+        int tile = 0;
+        bool valid = false;
+        if (rec < R && lane < SLOTS) {
+            const unsigned long long rv = __ldcg(records + rec);
+            off = (long long)(rv >> 24);
+            tile = (int)(rv & 0xFFFFFFu);
+            nxt = rec + 1 < R ? rec_off(records, rec + 1) : T;
+            const long long wlo = max(off, pos);
+            whi = min(nxt, gend);
+            valid = wlo < whi;
+            const long long c = nxt - off - REC_W;  // failures of the tile
+            flo = min(max(wlo - off - REC_W, 0ll), c);
+            take = valid ? min(max(whi - off - REC_W, 0ll), c) - flo : 0;
+        }
+        // inclusive prefix of the segment sizes, capped by the queue capacity
+        long long incl = take;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const long long v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+            if (lane >= d) incl += v;
+        }
+        const long long excl = incl - take;
+        const bool within = valid && excl < CAP;
+        const long long mine = within ? min(take, (long long)CAP - excl) : 0;
+        const uint32_t segs = __ballot_sync(0xFFFFFFFFu, mine > 0);
+        const uint32_t inside = __ballot_sync(0xFFFFFFFFu, within);  // lanes 0..k (lane 0 always)
+        const int ns = __popc(segs);
+        if (lane == 0 && ns) mbar_expect_tx(sm.bmbar, (uint32_t)(ns * 512));
+        __syncwarp();
+        if (mine > 0) {
+            const int sl = __popc(segs & ((1u << lane) - 1u));
+            const int z = tile / per_slice, rem = tile - z * per_slice, by = rem / tiles_x;
+            int* si = sm.sinfo_n + 8 * sl;
+            si[0] = (rem - by * tiles_x) * TW;
+            si[1] = row_begin + by * TH;
+            si[2] = z;
+            si[3] = tile;
+            si[4] = (int)flo;  // in-tile failure rank range [lo, hi)
+            si[5] = (int)(flo + mine);
+            si[6] = (int)excl;  // queue base
+            const int sx0 = si[0] - geo.CP, sy0 = si[1] - geo.R;
+            si[7] = sx0 < 0 || sx0 + geo.BS > cols || sy0 < 0 || sy0 + geo.BH > rows;
+            fence_proxy_async_smem();  // the previous batch's generic reads of bms before the async write
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 512, [%2];" ::"r"(
+                    smem_u32(sm.bms + 128 * sl)),
+                "l"(bitmap + (size_t)tile * 512), "r"(smem_u32(sm.bmbar))
+                : "memory");
+        }
+        const int last = 31 - __clz(inside);
+        if (lane == last) {
+            const long long end_pos = mine == take ? whi : off + REC_W + flo + mine;
+            cur[1] = end_pos;
+            cur[0] = rec + (end_pos >= nxt ? 1 : 0);
+            sm.ctl_n[0] = ns;
+            sm.ctl_n[1] = (int)(excl + mine);
+            sm.ctl_n[2] = end_pos < gend;
+        }
+        __syncwarp();
+    };
+    if (warp == 0 && gbeg < gend) choose();
     __syncthreads();
     GTRACE(13);
 
     while (gbeg < gend) {
-        // ---- 1. warp 0: the next segments (lane l: record cur + l), their TMA loads.  Positions are
-        //      weighted: record r spans [off, next) = REC_W units for its tile load, then its failures ----
+        // ---- 1. promote the chosen batch; warp 0 issues its tile loads ----
         if (tid < MAX_LEVELS) qcount[tid] = 0;
-        if (warp == 0) {
-            const long long rec = cur[0] + lane, pos = cur[1];
-            long long take = 0, off = 0, nxt = 0, flo = 0, whi = 0;
-            int tile = 0;
-            bool valid = false;
-            if (rec < R && lane < SLOTS) {
-                const unsigned long long rv = __ldcg(records + rec);
-                off = (long long)(rv >> 24);
-                tile = (int)(rv & 0xFFFFFFu);
-                nxt = rec + 1 < R ? rec_off(records, rec + 1) : T;
-                const long long wlo = max(off, pos);
-                whi = min(nxt, gend);
-                valid = wlo < whi;
-                const long long c = nxt - off - REC_W;  // failures of the tile
-                flo = min(max(wlo - off - REC_W, 0ll), c);
-                take = valid ? min(max(whi - off - REC_W, 0ll), c) - flo : 0;
-            }
-            // inclusive prefix of the segment sizes, capped by the queue capacity
-            long long incl = take;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const long long v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
-                if (lane >= d) incl += v;
-            }
-            const long long excl = incl - take;
-            const bool within = valid && excl < CAP;
-            const long long mine = within ? min(take, (long long)CAP - excl) : 0;
-            const uint32_t segs = __ballot_sync(0xFFFFFFFFu, mine > 0);
-            const uint32_t inside = __ballot_sync(0xFFFFFFFFu, within);  // lanes 0..k (lane 0 always)
-            const int ns = __popc(segs);
-            if (mine > 0) {
-                const int sl = __popc(segs & ((1u << lane) - 1u));
-                const int z = tile / per_slice, rem = tile - z * per_slice, by = rem / tiles_x;
-                int* si = sinfo + 8 * sl;
-                si[0] = (rem - by * tiles_x) * TW;
-                si[1] = row_begin + by * TH;
-                si[2] = z;
-                si[3] = tile;
-                si[4] = (int)flo;  // in-tile failure rank range [lo, hi)
-                si[5] = (int)(flo + mine);
-                si[6] = (int)excl;  // queue base
-                const int sx0 = si[0] - geo.CP, sy0 = si[1] - geo.R;
-                si[7] = sx0 < 0 || sx0 + geo.BS > cols || sy0 < 0 || sy0 + geo.BH > rows;
-                fence_proxy_async_smem();  // the slot's previous generic reads/writes before the async write
-                grow_tile_load(tm, geo, bufs + (size_t)sl * geo.b_bytes, &bar[sl], si[0], si[1], z);
-            }
-            const int last = 31 - __clz(inside);
-            if (lane == last) {
-                const long long end_pos = mine == take ? whi : off + REC_W + flo + mine;
-                cur[1] = end_pos;
-                cur[0] = rec + (end_pos >= nxt ? 1 : 0);
-                ctl[0] = ns;
-                ctl[1] = (int)(excl + mine);
-                ctl[2] = end_pos < gend;
-            }
-        }
+        if (tid < 8 * SLOTS) sinfo[tid] = sm.sinfo_n[tid];
+        if (tid < 3) ctl[tid] = sm.ctl_n[tid];
         __syncthreads();
-        GTRACE(1);
         const int ns = ctl[0];
         const bool more = ctl[2] != 0;
         if (ns == 0) {  // only tile-load weight in this stretch of the range
-            __syncthreads();
             if (!more) break;
+            if (warp == 0) choose();
+            __syncthreads();
             continue;
         }
+        if (warp == 0 && lane < ns) {
+            const int* si = sinfo + 8 * lane;
+            fence_proxy_async_smem();  // the slot's previous generic reads/writes before the async write
+            grow_tile_load(tm, geo, bufs + (size_t)lane * geo.b_bytes, &bar[lane], si[0], si[1], si[2]);
+        }
+        GTRACE(1);
         // ---- 2. queue: warp w collects slot w's failures with in-tile rank in [lo, hi) ----
         if (warp < ns) {
+            mbar_wait_warp(sm.bmbar, bmphase);
             const int* si = sinfo + 8 * warp;
-            const uint4 w4 = __ldcg(reinterpret_cast<const uint4*>(bitmap + (size_t)si[3] * 512) + lane);
+            const uint4 w4 = reinterpret_cast<const uint4*>(sm.bms + 128 * warp)[lane];
             const uint32_t wb[4] = {w4.x, w4.y, w4.z, w4.w};
             const int nf = __popc(w4.x) + __popc(w4.y) + __popc(w4.z) + __popc(w4.w);
             int incl = nf;
@@ -813,13 +840,6 @@ __device__ __forceinline__ void grow_range(const CUtensorMap* tm, const GGeo& ge
                 if (lane >= d) incl += v;
             }
             int rank = incl - nf;
-#ifdef HYB_TRACE
-            unsigned long long tq0 = 0;
-            if (tid == 0 && blockIdx.x < 1024) {
-                tq0 = tnow();
-                g_trace[(1024 + blockIdx.x) * 16 + 0] += tq0 - tt0 + (rank & 0);  // bitmap load + scan (warp 0)
-            }
-#endif
             const int lo = si[4], hi = si[5], qb = si[6] - lo;
             const uint32_t sbase = (uint32_t)warp << 12;
             if (rank < hi && incl > lo) {
@@ -836,16 +856,13 @@ __device__ __forceinline__ void grow_range(const CUtensorMap* tm, const GGeo& ge
                     }
                 }
             }
-#ifdef HYB_TRACE
-            __syncwarp();
-            if (tid == 0 && blockIdx.x < 1024) g_trace[(1024 + blockIdx.x) * 16 + 14] += tnow() - tq0;  // emission (warp 0)
-#endif
         }
-        // ---- 3. tiles landed; border tiles get edge replication (whole CTA, columns then rows) ----
-#ifdef HYB_TRACE
-        __syncthreads();
+        bmphase ^= 1u;
+        __syncthreads();  // bms consumed
         GTRACE(2);
-#endif
+        // ---- 3. the last warp chooses the next batch (its record loads and bitmap copies overlap the
+        //      tile wait and the levels); tiles landed; border tiles get edge replication ----
+        if (more && warp == NWARP - 1) choose();
         for (int sl = 0; sl < ns; ++sl) mbar_wait(&bar[sl], (phases >> sl) & 1u);
         phases ^= (1u << ns) - 1u;
         for (int sl = 0; sl < ns; ++sl) {
