@@ -54,6 +54,8 @@ struct K3Args {
     int* done;               // CTAs finished
     unsigned long long* rec_ctr;  // (records << 40) | weighted failures (+REC_W per tile), once per tile with failures
     unsigned long long* records;  // [record] = (weighted offset << 24) | tile
+    int* chunk_rec;               // [chunk] = record holding weighted position chunk << chunk_shift
+    int chunk_shift;              // log2 of the growth chunk (the growth variant's queue capacity)
 };
 
 
@@ -174,7 +176,12 @@ __global__ void __launch_bounds__(K3T, 3)
                 if (c) {
                     const unsigned long long old =
                         atomicAdd(args.rec_ctr, (1ull << REC_SHIFT) | (unsigned)(c + REC_W));
-                    args.records[old >> REC_SHIFT] = ((old & REC_MASK) << 24) | (unsigned)t;
+                    const long long rec = (long long)(old >> REC_SHIFT), off = (long long)(old & REC_MASK);
+                    args.records[rec] = ((unsigned long long)off << 24) | (unsigned)t;
+                    // chunk boundaries inside this record's weighted span [off, off + c + REC_W)
+                    const int sh = args.chunk_shift;
+                    for (long long ch = (off + (1ll << sh) - 1) >> sh; ch <= (off + c + REC_W - 1) >> sh; ++ch)
+                        args.chunk_rec[ch] = (int)rec;
                 }
             }
             mbar_arrive(&empty[s]);
@@ -204,6 +211,8 @@ struct GArgs {
     int tiles_x, tiles_y;    // k = 3 tiles
     unsigned long long* rec_ctr;        // written by amf_k3_kernel; reset here by the last CTA
     const unsigned long long* records;  // (failure offset << 24) | tile, offsets increasing
+    const int* chunk_rec;               // [chunk] = record holding its first weighted position
+    int* chunk_ctr;                     // growth chunk claims; reset here by the last CTA
     int* done;
 };
 
@@ -219,13 +228,15 @@ struct GArgs {
 // 2 CTAs/SM, batches of 8 tiles / 8192 failures) pays off when the k = 9 level is dense (BASELINE
 // config 4: smax 11, S&P 0.5); "lean" (networks up to k = 7, radix above, <= 80 registers, 3 CTAs/SM,
 // batches of 8 tiles / 4096 failures) when it is sparse or absent (config 2: 6 % faster step).
-template <int NETMAX_, int MINB_, int SLOTS_, int CAP_>
+template <int NETMAX_, int MINB_, int SLOTS_, int CAP_, bool DYN_>
 struct GrowCfg {
     static constexpr int NETMAX = NETMAX_, MINB = MINB_, SLOTS = SLOTS_, CAP = CAP_;
+    static constexpr bool DYN = DYN_;  // dynamic last quarter of the work (amf_core.cuh grow_range)
 };
-using GrowWide = GrowCfg<9, 2, 8, 8192>;
-using GrowLean = GrowCfg<7, 3, 8, 4096>;
+using GrowWide = GrowCfg<9, 2, 8, 8192, true>;
+using GrowLean = GrowCfg<7, 3, 8, 4096, false>;
 static_assert(GrowWide::SLOTS <= 8 && GrowLean::SLOTS <= 8, "header layout");
+static_assert(GrowWide::CAP == 1 << 13 && GrowLean::CAP == 1 << 12, "growth chunk = queue capacity (K3Args::chunk_shift)");
 
 template <class C>
 inline size_t grow_smem(const GGeo& g) {
@@ -241,8 +252,8 @@ __global__ void __launch_bounds__(GNT, C::MINB) amf_grow_kernel(const __grid_con
     const GGeo& geo = args.geo;
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem);            // [SLOTS]
     int* sinfo = reinterpret_cast<int*>(smem + 64);                // [SLOTS][8]: x0 y0 z tile lo hi qbase border
-    long long* cur = reinterpret_cast<long long*>(smem + 320);     // [0] record, [1] global failure position
-    int* ctl = reinterpret_cast<int*>(smem + 336);                 // [4] segments, queue n, more
+    long long* cur = reinterpret_cast<long long*>(smem + 320);     // [4] record, position, range end, static taken
+    int* ctl = reinterpret_cast<int*>(smem + 368);                 // [4] segments, queue n, more
     int* qcount = reinterpret_cast<int*>(smem + 384);              // [MAX_LEVELS]
     uint8_t* bufs = smem + GHDR;
     uint16_t* Q0 = reinterpret_cast<uint16_t*>(bufs + (size_t)C::SLOTS * geo.b_bytes);
@@ -262,7 +273,6 @@ __global__ void __launch_bounds__(GNT, C::MINB) amf_grow_kernel(const __grid_con
     grid_dep_wait();  // records and bitmap come from the k = 3 grid
     const unsigned long long ctr = __ldcg(args.rec_ctr);
     const long long R = (long long)(ctr >> REC_SHIFT), T = (long long)(ctr & REC_MASK);
-    const long long gbeg = T * blockIdx.x / gridDim.x, gend = T * (blockIdx.x + 1) / gridDim.x;
     uint32_t phases = 0;
     const GrowSmem sm{bar, sinfo, cur, ctl, qcount, bufs, Q0, Q1, sinfo_n, ctl_n, bms, bmbar};
     auto out = [&](const int* si, int pix, uint8_t v, int k) {
@@ -270,8 +280,9 @@ __global__ void __launch_bounds__(GNT, C::MINB) amf_grow_kernel(const __grid_con
         args.dst[(size_t)si[2] * args.dslice + row * args.dpitch + si[0] + (pix & 127)] = v;
         if (FIN) args.fin[(size_t)si[2] * args.fslice + row * args.fpitch + si[0] + (pix & 127)] = (uint8_t)k;
     };
-    grow_range<FIN, GNT, decltype(out), C::SLOTS, C::CAP, C::NETMAX>(&tm, geo, sm, args.bitmap, args.records, R, T,
-                                                                     gbeg, gend, per_slice, args.tiles_x,
+    grow_range<FIN, GNT, decltype(out), C::SLOTS, C::CAP, C::NETMAX, C::DYN>(&tm, geo, sm, args.bitmap, args.records, R, T,
+                                                                     args.chunk_rec, args.chunk_ctr, per_slice,
+                                                                     args.tiles_x,
                                                                      args.row_begin, args.rows, args.cols, args.smax,
                                                                      phases, out);
     TRACE(1, 15);
@@ -280,6 +291,7 @@ __global__ void __launch_bounds__(GNT, C::MINB) amf_grow_kernel(const __grid_con
         __threadfence();
         if (atomicAdd(args.done, 1) == (int)gridDim.x - 1) {
             *args.rec_ctr = 0;
+            *args.chunk_ctr = 0;
             *args.done = 0;
         }
     }
@@ -291,7 +303,8 @@ int g_num_sms = 0;
 
 size_t amf_work_bytes(const Plane& p) {
     const size_t tiles = (size_t)((p.cols + TW - 1) / TW) * ((p.row_end - p.row_begin + TH - 1) / TH) * p.n_slices;
-    return 64 + (tiles * 8 + 63) / 64 * 64 + tiles * 512;
+    // chunk table: weighted total <= tiles * (TW * TH + REC_W) over chunks of >= 4096 -> <= 1.04 tiles + 1
+    return 64 + (tiles * 8 + 63) / 64 * 64 + tiles * 512 + (tiles * 2 + 16) * sizeof(int);
 }
 
 AmfWork amf_work(uint8_t* base, const Plane& p) {
@@ -300,6 +313,7 @@ AmfWork amf_work(uint8_t* base, const Plane& p) {
     w.counters = reinterpret_cast<int*>(base);
     w.records = reinterpret_cast<unsigned long long*>(base + 64);
     w.bitmap = base + 64 + (tiles * 8 + 63) / 64 * 64;
+    w.chunk_rec = reinterpret_cast<int*>(w.bitmap + tiles * 512);
     return w;
 }
 
@@ -344,6 +358,8 @@ cudaError_t launch_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, si
     a.done = work.counters + 3;
     a.rec_ctr = reinterpret_cast<unsigned long long*>(work.counters);
     a.records = work.records;
+    a.chunk_rec = work.chunk_rec;
+    a.chunk_shift = smax >= 11 ? 13 : 12;  // GrowWide::CAP = 8192, GrowLean::CAP = 4096 (see below)
     static int per_sm = 0;
     if (!per_sm) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, amf_k3_kernel<false>, K3T, SMEM);
@@ -391,6 +407,8 @@ cudaError_t launch_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, si
     g.tiles_y = a.tiles_y;
     g.rec_ctr = a.rec_ctr;
     g.records = work.records;
+    g.chunk_rec = work.chunk_rec;
+    g.chunk_ctr = work.counters + 5;
     g.done = work.counters + 4;
     static size_t occ_key[4] = {0, 0, 0, 0};
     static int occ_val[4] = {1, 1, 1, 1};

@@ -677,7 +677,7 @@ __device__ __forceinline__ void grow_levels(const uint8_t* bufs, const GGeo& geo
 struct GrowSmem {
     uint64_t* bar;   // [SLOTS] tile slots (initialised by the caller)
     int* sinfo;      // [SLOTS][8]: x0 y0 z tile lo hi qbase border -- the batch being grown
-    long long* cur;  // [2]: record, position of the next choice
+    long long* cur;  // [4]: record, position of the next choice, end of the claimed range, static range taken
     int* ctl;        // [4]: segments, queue n, more, bitmaps issued -- the batch being grown
     int* qcount;     // [MAX_LEVELS]
     uint8_t* bufs;   // [SLOTS][geo.b_bytes]
@@ -689,13 +689,16 @@ struct GrowSmem {
     uint64_t* bmbar; // [1] their mbarrier (initialised by the caller)
 };
 
-template <bool FIN, int NTHR, class Out, int SLOTS = GSLOTS, int CAP = GCAP, int NETMAX = HYB_GROW_NETMAX>
+template <bool FIN, int NTHR, class Out, int SLOTS = GSLOTS, int CAP = GCAP, int NETMAX = HYB_GROW_NETMAX,
+          bool DYN = true>
 __device__ __forceinline__ void grow_range(const CUtensorMap* tm, const GGeo& geo, const GrowSmem& sm,
                                            const uint8_t* bitmap, const unsigned long long* records, long long R,
-                                           long long T, long long gbeg, long long gend, int per_slice, int tiles_x,
-                                           int row_begin, int rows, int cols, int smax, uint32_t& phases, Out out) {
+                                           long long T, const int* chunk_rec, int* chunk_ctr, int per_slice,
+                                           int tiles_x, int row_begin, int rows, int cols, int smax,
+                                           uint32_t& phases, Out out) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int NWARP = NTHR / 32;
+    constexpr long long CHUNK = CAP;  // weighted units per claim (amf.cu: K3Args::chunk_shift)
     uint64_t* bar = sm.bar;
     int* sinfo = sm.sinfo;
     long long* cur = sm.cur;
@@ -718,28 +721,78 @@ __device__ __forceinline__ void grow_range(const CUtensorMap* tm, const GGeo& ge
 #else
 #define GTRACE(slot) do {} while (0)
 #endif
-    if (warp == 0 && gbeg < gend) {
-        // 32-ary search: the last record whose offset is <= gbeg
-        long long lo = 0, hi = R;
-        while (hi - lo > 1) {
-            const long long step = (hi - lo + 31) / 32, idx = lo + lane * step;
-            const bool le = idx < hi && rec_off(records, idx) <= gbeg;
-            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, le);
-            const int last = 31 - __clz(bal);  // lane 0 always qualifies
-            lo += last * step;
-            hi = min(hi, lo + step);
-        }
-        if (lane == 0) {
-            cur[0] = lo;
-            cur[1] = gbeg;
-        }
+    if (tid == 0) {
+        cur[0] = 0;
+        cur[1] = 0;
+        cur[2] = 0;  // nothing claimed yet
+        cur[3] = 0;  // static range not taken yet
     }
-    __syncwarp();
+    // Work split: the first 3/4 of the chunks (CHUNK weighted units each) are split statically, CTA j
+    // taking a contiguous run; with DYN the rest is claimed chunk by chunk from a global counter by
+    // whichever CTA runs out first -- the cost of a failure depends on how deep it grows, which no
+    // static split sees (config 4: static-only CTAs finished 1.70 .. 2.22 ms; with the dynamic quarter
+    // 2.03 .. 2.17 ms and a 3 % shorter step).  Without DYN everything is static (configs 2 / 3, where
+    // the failures are shallow and a claimed chunk's half-filled batches cost more than the tail).
+    const long long nchunks = (T + CHUNK - 1) / CHUNK, nstatic = DYN ? nchunks * 3 / 4 : nchunks;
+    __syncthreads();
 
     // One warp chooses the next batch (lane l: record cur + l) into sinfo_n / ctl_n and bulk-copies its
     // tiles' failure bitmaps into bms.  Positions are weighted: record r spans [off, next) = REC_W units
-    // for its tile load, then its failures.
+    // for its tile load, then its failures.  Work is claimed in chunks of CHUNK weighted units from a
+    // global counter (chunk_rec gives each chunk's first record), so CTAs that meet cheap failures take
+    // more chunks -- the cost of a failure depends on how deep it grows, which no static split sees.
     auto choose = [&]() {
+        if (cur[1] >= cur[2]) {  // range exhausted: the static run, then chunks from the counter
+            bool have = false;
+            if (!cur[3]) {
+                // static run: [Ts j / G, Ts (j + 1) / G) of the first Ts weighted units; its first record by a
+                // 32-ary search (the last record whose offset is <= the start)
+                const long long Ts = min(T, nstatic * CHUNK);
+                const long long b0 = Ts * blockIdx.x / gridDim.x, b1 = Ts * (blockIdx.x + 1) / gridDim.x;
+                have = b0 < b1;
+                long long lo = 0, hi = R;
+                while (have && hi - lo > 1) {
+                    const long long step = (hi - lo + 31) / 32, idx = lo + lane * step;
+                    const bool le = idx < hi && rec_off(records, idx) <= b0;
+                    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, le);
+                    lo += (31 - __clz(bal)) * step;  // lane 0 always qualifies
+                    hi = min(hi, lo + step);
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    cur[3] = 1;
+                    if (have) {
+                        cur[0] = lo;
+                        cur[1] = b0;
+                        cur[2] = b1;
+                    }
+                }
+                __syncwarp();
+            }
+            if (!have) {
+                long long ch = nchunks;  // without DYN: no dynamic chunks
+                if (DYN) {
+                    if (lane == 0) ch = nstatic + atomicAdd(chunk_ctr, 1);
+                    ch = __shfl_sync(0xFFFFFFFFu, ch, 0);
+                }
+                if (ch >= nchunks) {
+                    if (lane == 0) {
+                        sm.ctl_n[0] = 0;
+                        sm.ctl_n[1] = 0;
+                        sm.ctl_n[2] = 0;  // no more work
+                    }
+                    __syncwarp();
+                    return;
+                }
+                if (lane == 0) {
+                    cur[0] = __ldcg(chunk_rec + ch);
+                    cur[1] = ch * CHUNK;
+                    cur[2] = min((ch + 1) * CHUNK, T);
+                }
+                __syncwarp();
+            }
+        }
+        const long long gend = cur[2];
         const long long rec = cur[0] + lane, pos = cur[1];
         long long take = 0, off = 0, nxt = 0, flo = 0, whi = 0;
         int tile = 0;
@@ -798,15 +851,15 @@ __device__ __forceinline__ void grow_range(const CUtensorMap* tm, const GGeo& ge
             cur[0] = rec + (end_pos >= nxt ? 1 : 0);
             sm.ctl_n[0] = ns;
             sm.ctl_n[1] = (int)(excl + mine);
-            sm.ctl_n[2] = end_pos < gend;
+            sm.ctl_n[2] = 1;  // the next choice claims a new chunk or reports the end
         }
         __syncwarp();
     };
-    if (warp == 0 && gbeg < gend) choose();
+    if (warp == 0) choose();
     __syncthreads();
     GTRACE(13);
 
-    while (gbeg < gend) {
+    while (true) {
         // ---- 1. promote the chosen batch; warp 0 issues its tile loads ----
         if (tid < MAX_LEVELS) qcount[tid] = 0;
         if (tid < 8 * SLOTS) sinfo[tid] = sm.sinfo_n[tid];
@@ -862,7 +915,7 @@ __device__ __forceinline__ void grow_range(const CUtensorMap* tm, const GGeo& ge
         GTRACE(2);
         // ---- 3. the last warp chooses the next batch (its record loads and bitmap copies overlap the
         //      tile wait and the levels); tiles landed; border tiles get edge replication ----
-        if (more && warp == NWARP - 1) choose();
+        if (warp == NWARP - 1) choose();
         for (int sl = 0; sl < ns; ++sl) mbar_wait(&bar[sl], (phases >> sl) & 1u);
         phases ^= (1u << ns) - 1u;
         for (int sl = 0; sl < ns; ++sl) {
@@ -882,7 +935,6 @@ __device__ __forceinline__ void grow_range(const CUtensorMap* tm, const GGeo& ge
         if (tid == 0 && blockIdx.x < 1024) g_trace[(1024 + blockIdx.x) * 16 + 4] += 1;
         if (tid == 0) tt0 = tnow();
 #endif
-        if (!more) break;
     }
 #undef GTRACE
 }

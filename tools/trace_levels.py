@@ -39,3 +39,12 @@ tot = sum(t[:, 5 + l] for l in range(4)) / 1e3
 print(f"batches/CTA mean {t[:, 4].mean():.1f}; per CTA mean us: entry {t[:, 13].mean() / 1e3:.1f}  choose {t[:, 1].mean() / 1e3:.1f}"
       f"  queue {t[:, 2].mean() / 1e3:.1f}  wait+edges {t[:, 3].mean() / 1e3:.1f}  levels {tot.mean():.1f}")
 print(f"queue detail (warp 0, per CTA us): bitmap load + scan {t[:, 0].mean() / 1e3:.1f}  emission {t[:, 14].mean() / 1e3:.1f}")
+tt = np.frombuffer(buf, dtype=np.uint64).reshape(2, 1024, 16).astype(np.int64)
+k3s = tt[0][:, 0][tt[0][:, 0] > 0]
+k3e = tt[0][:, 15][tt[0][:, 15] > 0]
+ge = tt[1][:, 15][tt[1][:, 15] > 0]
+t0 = k3s.min()
+q = lambda v: " ".join(f"{x:8.1f}" for x in np.percentile((v - t0) / 1e3, [0, 10, 50, 90, 100]))
+print("us from the k3 start, quantiles 0/10/50/90/100 over CTAs")
+print("k3 end     ", q(k3e))
+print("growth end ", q(ge))
