@@ -163,6 +163,24 @@ def test_amf_worst_case_growth(ctx):
     np.testing.assert_array_equal(fin, ref_fin)
 
 
+def test_amf_wide_growth_row_ranges_and_stacks(ctx):
+    """smax 11 on dense impulses takes the wide growth variant with its dynamically claimed last quarter
+    of the work (amf.cu GrowWide): row ranges of a source (tiles offset by row_begin) and stacks (tiles
+    across slices) against the oracle, finalized_at included."""
+    img = capi.make_phantom(700, 900, 16, 20.0, 0.5, 3)
+    for rb, re in [(0, 700), (123, 611), (650, 700)]:
+        out, fin = denoise.adaptive_median_rows(img, 11, rb, re, finalized_at=True)
+        ref_out, ref_fin = oracle.amf(img, 11, rb, re, finalized_at=True)
+        np.testing.assert_array_equal(out, ref_out, err_msg=f"rows [{rb},{re})")
+        np.testing.assert_array_equal(fin, ref_fin, err_msg=f"rows [{rb},{re})")
+    stack = np.stack([capi.make_phantom(384, 512, 10, 20.0, 0.5, s) for s in range(4)])
+    y, ws = denoise.hybrid_denoise_batch(stack, 11, 7)
+    for s in range(4):
+        ref_y, ref_w = oracle.hybrid(stack[s], 11, 7)
+        assert ws[s] == ref_w
+        np.testing.assert_array_equal(y[s], ref_y, err_msg=f"slice {s}")
+
+
 # ---------------------------------------------------------------- W1 Wiener
 
 @pytest.mark.parametrize("win", [1, 3, 5, 7, 9])
