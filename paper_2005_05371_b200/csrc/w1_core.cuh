@@ -112,10 +112,14 @@ __device__ __forceinline__ uint64_t fadd2_rd(uint64_t a, uint64_t b) {
 }
 
 // Statistics of one tile: this lane's share of n * sum S2 - sum S1^2 over the tile's output pixels
-// (two's complement; the warp / grid sum is W).
-template <int RW, int FH>
-__device__ __forceinline__ long long w1_tile_stats(const uint8_t* __restrict__ T, int x0, int y0, int rows, int cols,
-                                                   int row_begin, int row_end) {
+// (two's complement; the warp / grid sum is W).  FAST: the tile's rows and the lane's columns are all
+// interior (every f^2 of the tile's output rows is covered by n windows, no image or range border
+// within reach), so the coverage-weighted sum is n^2 times a plain 32-bit sum of f^2 over the output
+// rows -- no per-row window counts (they were a quarter of this pass's instructions).
+template <int RW, int FH, bool FAST>
+__device__ __forceinline__ long long w1_tile_stats_body(const uint8_t* __restrict__ T, int x0, int y0, int rows,
+                                                        int cols, int row_begin, int row_end, const uint32_t (&wc)[4],
+                                                        bool wc_full) {
     constexpr int N = 2 * RW + 1;
     constexpr int NN = N * N;
     constexpr int SROWS = FH + 2 * RW;
@@ -123,22 +127,11 @@ __device__ __forceinline__ long long w1_tile_stats(const uint8_t* __restrict__ T
     const int c = 4 * lane;
     const int col_lim = cols - x0, row_lim = row_end - y0;
     const uint32_t* base = reinterpret_cast<const uint32_t*>(T + FCP + c - 4);
-    // ---- statistics: W = n * sum_p S2(p) - sum_p S1(p)^2 with sum_p S2(p) = sum_q f(q)^2 WR(q_r) WC(q_c)
-    // (WR / WC = how many output windows cover a row / column, clamping included), so only S1
-    // needs a per-pixel box sum.  Each image pixel's f^2 is owned by exactly one tile: its output
-    // rows, plus the RW halo rows outside the output range for the first / last tile.
-    uint32_t wc[4];
-    bool wc_full = true;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int cc = x0 + c + i;
-        wc[i] = cc < cols ? (uint32_t)win_count(cc, 0, cols, cols, RW) : 0u;
-        wc_full &= wc[i] == (uint32_t)N;
-    }
     const int own_lo = (y0 == row_begin) ? max(0, row_begin - RW) : y0;
     const int own_hi = (y0 + FH >= row_end) ? min(rows, row_end + RW) : y0 + FH;
     uint32_t r1[N][4], s1[4] = {0, 0, 0, 0};
     long long tile_sq = 0, tile_s1sq = 0;
+    uint32_t sq32 = 0;  // FAST: sum of f^2 over the output rows (<= 16 * 4 * 255^2)
     auto take_row = [&](int rr, uint32_t (&h)[4]) {
         const uint32_t* rp = base + rr * (FBS / 4);
         const uint32_t w0 = rp[0], w1 = rp[1], w2 = rp[2];
@@ -146,22 +139,26 @@ __device__ __forceinline__ long long w1_tile_stats(const uint8_t* __restrict__ T
         h[1] = hsum1<RW, 1>(w0, w1, w2);
         h[2] = hsum1<RW, 2>(w0, w1, w2);
         h[3] = hsum1<RW, 3>(w0, w1, w2);
-        const int r = y0 - RW + rr;  // image row of this tile row
-        if (r >= own_lo && r < own_hi) {
-            const bool interior = r - RW >= max(row_begin, 0) && r + RW < min(row_end, rows);
-            const uint32_t wr = interior ? (uint32_t)N : (uint32_t)win_count(r, row_begin, row_end, rows, RW);
-            uint32_t q;
-            if (wc_full) {
-                q = (uint32_t)N * __dp4a(w1, w1, 0u);
-            } else {
-                q = 0;
+        if constexpr (FAST) {
+            if (rr >= RW && rr < RW + FH) sq32 = __dp4a(w1, w1, sq32);
+        } else {
+            const int r = y0 - RW + rr;  // image row of this tile row
+            if (r >= own_lo && r < own_hi) {
+                const bool interior = r - RW >= max(row_begin, 0) && r + RW < min(row_end, rows);
+                const uint32_t wr = interior ? (uint32_t)N : (uint32_t)win_count(r, row_begin, row_end, rows, RW);
+                uint32_t q;
+                if (wc_full) {
+                    q = (uint32_t)N * __dp4a(w1, w1, 0u);
+                } else {
+                    q = 0;
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const uint32_t f = (w1 >> (8 * i)) & 0xFFu;
-                    q += wc[i] * f * f;
+                    for (int i = 0; i < 4; ++i) {
+                        const uint32_t f = (w1 >> (8 * i)) & 0xFFu;
+                        q += wc[i] * f * f;
+                    }
                 }
+                tile_sq += (long long)wr * q;
             }
-            tile_sq += (long long)wr * q;
         }
     };
 #pragma unroll
@@ -183,13 +180,14 @@ __device__ __forceinline__ long long w1_tile_stats(const uint8_t* __restrict__ T
             for (int i = 0; i < 4; ++i) {
                 s1[i] += h[i];
                 r1[(u + N - 1) % N][i] = h[i];
-                if (c + i < col_lim) sq4 += s1[i] * s1[i];  // <= 4 * 12495^2 < 2^32
+                if (FAST || c + i < col_lim) sq4 += s1[i] * s1[i];  // <= 4 * 12495^2 < 2^32
             }
-            if (y < row_lim) tile_s1sq += sq4;
+            if (FAST || y < row_lim) tile_s1sq += sq4;
 #pragma unroll
             for (int i = 0; i < 4; ++i) s1[i] -= r1[u][i];
         }
     }
+    if constexpr (FAST) return (long long)NN * NN * sq32 - tile_s1sq;
     // the last rows of the tile box (below the window of the last output row) hold halo f^2
 #pragma unroll
     for (int rr = FH + N - 1; rr < SROWS; ++rr) {
@@ -197,6 +195,31 @@ __device__ __forceinline__ long long w1_tile_stats(const uint8_t* __restrict__ T
         take_row(rr, h);
     }
     return (long long)NN * tile_sq - tile_s1sq;
+}
+
+template <int RW, int FH>
+__device__ __forceinline__ long long w1_tile_stats(const uint8_t* __restrict__ T, int x0, int y0, int rows, int cols,
+                                                   int row_begin, int row_end) {
+    constexpr int N = 2 * RW + 1;
+    // ---- statistics: W = n * sum_p S2(p) - sum_p S1(p)^2 with sum_p S2(p) = sum_q f(q)^2 WR(q_r) WC(q_c)
+    // (WR / WC = how many output windows cover a row / column, clamping included), so only S1
+    // needs a per-pixel box sum.  Each image pixel's f^2 is owned by exactly one tile: its output
+    // rows, plus the RW halo rows outside the output range for the first / last tile.
+    const int c = 4 * (threadIdx.x & 31);
+    uint32_t wc[4];
+    bool wc_full = true;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int cc = x0 + c + i;
+        wc[i] = cc < cols ? (uint32_t)win_count(cc, 0, cols, cols, RW) : 0u;
+        wc_full &= wc[i] == (uint32_t)N;
+    }
+    // rows: output rows y0 .. y0 + FH - 1 all in range and all RW away from the image and range borders
+    const bool rows_interior = y0 - RW >= max(row_begin, 0) && y0 + FH - 1 + RW < min(row_end, rows) &&
+                               y0 != row_begin && y0 + FH < row_end;
+    if (__all_sync(0xFFFFFFFFu, wc_full) && rows_interior)
+        return w1_tile_stats_body<RW, FH, true>(T, x0, y0, rows, cols, row_begin, row_end, wc, true);
+    return w1_tile_stats_body<RW, FH, false>(T, x0, y0, rows, cols, row_begin, row_end, wc, wc_full);
 }
 
 // Gain constants of one image: W = sum of V, wq32 = min(floor(W / P), 2^31 - 1), kq = W / P.
