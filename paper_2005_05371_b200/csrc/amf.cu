@@ -228,15 +228,19 @@ struct GArgs {
 // 2 CTAs/SM, batches of 8 tiles / 8192 failures) pays off when the k = 9 level is dense (BASELINE
 // config 4: smax 11, S&P 0.5); "lean" (networks up to k = 7, radix above, <= 80 registers, 3 CTAs/SM,
 // batches of 8 tiles / 4096 failures) when it is sparse or absent (config 2: 6 % faster step).
-template <int NETMAX_, int MINB_, int SLOTS_, int CAP_, bool DYN_>
+template <int NETMAX_, int MINB_, int SLOTS_, int CAP_, bool DYN_, int CHUNK_SHIFT_>
 struct GrowCfg {
     static constexpr int NETMAX = NETMAX_, MINB = MINB_, SLOTS = SLOTS_, CAP = CAP_;
     static constexpr bool DYN = DYN_;  // dynamic last quarter of the work (amf_core.cuh grow_range)
+    static constexpr int CHUNK_SHIFT = CHUNK_SHIFT_;  // log2 of a claim, in weighted units
 };
-using GrowWide = GrowCfg<9, 2, 8, 8192, true>;
-using GrowLean = GrowCfg<7, 3, 8, 4096, false>;
+#ifndef HYB_LEAN_DYN
+#define HYB_LEAN_DYN 0
+#endif
+using GrowWide = GrowCfg<9, 2, 8, 8192, true, 13>;
+using GrowLean = GrowCfg<7, 3, 8, 4096, HYB_LEAN_DYN != 0, 11>;
 static_assert(GrowWide::SLOTS <= 8 && GrowLean::SLOTS <= 8, "header layout");
-static_assert(GrowWide::CAP == 1 << 13 && GrowLean::CAP == 1 << 12, "growth chunk = queue capacity (K3Args::chunk_shift)");
+static_assert(GrowWide::CHUNK_SHIFT >= 11 && GrowLean::CHUNK_SHIFT >= 11, "chunk table sized for chunks >= 2048");
 
 template <class C>
 inline size_t grow_smem(const GGeo& g) {
@@ -280,7 +284,7 @@ __global__ void __launch_bounds__(GNT, C::MINB) amf_grow_kernel(const __grid_con
         args.dst[(size_t)si[2] * args.dslice + row * args.dpitch + si[0] + (pix & 127)] = v;
         if (FIN) args.fin[(size_t)si[2] * args.fslice + row * args.fpitch + si[0] + (pix & 127)] = (uint8_t)k;
     };
-    grow_range<FIN, GNT, decltype(out), C::SLOTS, C::CAP, C::NETMAX, C::DYN>(&tm, geo, sm, args.bitmap, args.records, R, T,
+    grow_range<FIN, GNT, decltype(out), C::SLOTS, C::CAP, C::NETMAX, C::DYN, 1ll << C::CHUNK_SHIFT>(&tm, geo, sm, args.bitmap, args.records, R, T,
                                                                      args.chunk_rec, args.chunk_ctr, per_slice,
                                                                      args.tiles_x,
                                                                      args.row_begin, args.rows, args.cols, args.smax,
@@ -303,8 +307,8 @@ int g_num_sms = 0;
 
 size_t amf_work_bytes(const Plane& p) {
     const size_t tiles = (size_t)((p.cols + TW - 1) / TW) * ((p.row_end - p.row_begin + TH - 1) / TH) * p.n_slices;
-    // chunk table: weighted total <= tiles * (TW * TH + REC_W) over chunks of >= 4096 -> <= 1.04 tiles + 1
-    return 64 + (tiles * 8 + 63) / 64 * 64 + tiles * 512 + (tiles * 2 + 16) * sizeof(int);
+    // chunk table: weighted total <= tiles * (TW * TH + REC_W) over chunks of >= 2048 -> <= 2.07 tiles + 1
+    return 64 + (tiles * 8 + 63) / 64 * 64 + tiles * 512 + (tiles * 3 + 16) * sizeof(int);
 }
 
 AmfWork amf_work(uint8_t* base, const Plane& p) {
@@ -359,7 +363,7 @@ cudaError_t launch_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, si
     a.rec_ctr = reinterpret_cast<unsigned long long*>(work.counters);
     a.records = work.records;
     a.chunk_rec = work.chunk_rec;
-    a.chunk_shift = smax >= 11 ? 13 : 12;  // GrowWide::CAP = 8192, GrowLean::CAP = 4096 (see below)
+    a.chunk_shift = smax >= 11 ? GrowWide::CHUNK_SHIFT : GrowLean::CHUNK_SHIFT;  // the growth variant below
     static int per_sm = 0;
     if (!per_sm) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, amf_k3_kernel<false>, K3T, SMEM);

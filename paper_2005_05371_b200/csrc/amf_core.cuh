@@ -690,7 +690,7 @@ struct GrowSmem {
 };
 
 template <bool FIN, int NTHR, class Out, int SLOTS = GSLOTS, int CAP = GCAP, int NETMAX = HYB_GROW_NETMAX,
-          bool DYN = true>
+          bool DYN = true, long long CHUNK = CAP>
 __device__ __forceinline__ void grow_range(const CUtensorMap* tm, const GGeo& geo, const GrowSmem& sm,
                                            const uint8_t* bitmap, const unsigned long long* records, long long R,
                                            long long T, const int* chunk_rec, int* chunk_ctr, int per_slice,
@@ -698,7 +698,6 @@ __device__ __forceinline__ void grow_range(const CUtensorMap* tm, const GGeo& ge
                                            uint32_t& phases, Out out) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int NWARP = NTHR / 32;
-    constexpr long long CHUNK = CAP;  // weighted units per claim (amf.cu: K3Args::chunk_shift)
     uint64_t* bar = sm.bar;
     int* sinfo = sm.sinfo;
     long long* cur = sm.cur;
