@@ -132,9 +132,12 @@ __global__ void __launch_bounds__(SNT, SMIN) hybrid_small_kernel(const __grid_co
         for (int i = 0; i < STPC; ++i) mbar_init(&bar[i], 1);
         fence_mbar_init();
         for (int i = 0; i < nt; ++i) {
-            // second tile: the point mirror of the first (tile ntiles - 1 - b), so a CTA pairs tiles from
-            // opposite corners -- failure density follows the image content and its column gradient
-            const int t = (STPC == 2 && i == 1) ? a.ntiles - 1 - (int)blockIdx.x : (int)blockIdx.x + i * (int)gridDim.x;
+            // snake order: block i of G consecutive tiles is dealt forwards for even i, backwards for odd i
+            // (for two tiles per CTA: the second is the point mirror of the first), so a CTA's tiles come
+            // from opposite parts of the image -- failure density follows the image content and its
+            // column gradient
+            const int G = (int)gridDim.x, b = (int)blockIdx.x;
+            const int t = (i & 1) ? min((i + 1) * G, a.ntiles) - 1 - b : i * G + b;
             const int by = t / a.tiles_x;
             tinfo[2 * i] = (t - by * a.tiles_x) * TW;
             tinfo[2 * i + 1] = by * TH;
