@@ -218,6 +218,11 @@ bool try_small(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int cols,
     const hyb::SmallBufs bufs{g, pitch, ctx->f.ptr, fp, y, ypitch, reinterpret_cast<unsigned long long*>(ctx->wsum.ptr),
                               reinterpret_cast<unsigned*>(ctx->sbar.ptr)};
     e = hyb::launch_small(pl, bufs, rows, cols, smax, win, !ctx->exclusive, ctx->stream);
+    if (e == cudaErrorCooperativeLaunchTooLarge) {
+        // the grid no longer fits co-resident (another context holds SMs): the separate kernels
+        cudaGetLastError();
+        return false;
+    }
     if (e != cudaSuccess) {
         *status = cuda_fail(ctx, e, "launch_small");
         return true;
@@ -330,7 +335,8 @@ int hybrid_host_pipelined(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows
         if (timed) HYB_CHECK(cudaEventRecord(ctx->ev[3], ctx->stream));
         HYB_CHECK(copy2d(ctx, ctx->in.ptr, pp, g, pitch, cols, rows));
         int st;
-        try_small(ctx, ctx->in.ptr, pp, rows, cols, smax, win, ctx->out.ptr, pp, timed, &st);
+        if (!try_small(ctx, ctx->in.ptr, pp, rows, cols, smax, win, ctx->out.ptr, pp, timed, &st))
+            st = hybrid_device(ctx, ctx->in.ptr, pp, rows, cols, smax, win, 1, ctx->out.ptr, pp, timed);
         if (st) return st;
         HYB_CHECK(copy2d(ctx, y, y_pitch, ctx->out.ptr, pp, cols, rows));
         return HYB_OK;
