@@ -20,8 +20,12 @@ LPAD, RPAD, GUARD = 16, 45, 3
 
 
 def guarded(rows, cols, dev="cuda", init=None):
-    """(full buffer, view): view = rows x cols at (GUARD, LPAD) of a canary-filled buffer."""
-    full = torch.full((rows + 2 * GUARD, LPAD + cols + RPAD), CANARY, dtype=torch.uint8, device=dev)
+    """(full buffer, view): view = rows x cols at (GUARD, LPAD) of a canary-filled buffer on the device,
+    in pinned host memory (dev="pinned") or in pageable host memory (dev="cpu")."""
+    full = torch.full((rows + 2 * GUARD, LPAD + cols + RPAD), CANARY, dtype=torch.uint8,
+                      device="cpu" if dev == "pinned" else dev)
+    if dev == "pinned":
+        full = full.pin_memory()
     view = full[GUARD:GUARD + rows, LPAD:LPAD + cols]
     if init is not None:
         view.copy_(torch.from_numpy(init))
@@ -49,12 +53,15 @@ def run(st, ctx, what):
 @pytest.mark.parametrize("rows,cols,smax,win", [(300, 333, 7, 3), (1600, 1600, 11, 7), (2048, 2112, 9, 5),
                                                  (5, 3, 15, 7), (1, 200, 7, 3)])
 @pytest.mark.parametrize("parts", [1, 2])
-def test_hybrid_writes_stay_in_view(ctx, rows, cols, smax, win, parts):
+@pytest.mark.parametrize("mem", ["cuda", "pinned", "cpu"])
+def test_hybrid_writes_stay_in_view(ctx, rows, cols, smax, win, parts, mem):
+    """mem: where g and y live -- device, pinned host (the fused kernel stores y straight into it) or
+    pageable host memory."""
     if parts > rows:
         pytest.skip("parts > rows is rejected")
     g = capi.make_phantom(rows, cols, 8, 20.0, 0.5, rows + cols)
-    gfull, gv = guarded(rows, cols, init=g)
-    yfull, yv = guarded(rows, cols)
+    gfull, gv = guarded(rows, cols, dev=mem, init=g)
+    yfull, yv = guarded(rows, cols, dev=mem)
     st = capi.lib.hyb_hybrid_u8(ctx.ptr, gv.data_ptr(), gv.stride(0), rows, cols, smax, win, parts,
                                 yv.data_ptr(), yv.stride(0), None)
     run(st, ctx, "hybrid")
