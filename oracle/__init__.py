@@ -32,6 +32,7 @@ def _load_oracle():
     lib.hyb_oracle_hybrid_u8.argtypes = [P, c_size_t, c_int, c_int, c_int, c_int, P, P, c_size_t, POINTER(c_int64)]
     lib.hyb_oracle_validate_smax.argtypes = [c_int]
     lib.hyb_oracle_contrast_stretch_u8.argtypes = [P, c_size_t, c_int, c_int, P, c_size_t]
+    lib.oracle_make_phantom_u8.argtypes = [c_int, c_int, c_int, c_double, c_double, c_uint64, P, c_size_t]
     return lib
 
 
@@ -137,6 +138,59 @@ def hybrid(g, smax, win):
     if st:
         raise ValueError("oracle hybrid rejected its arguments")
     return y, w.value
+
+
+def make_phantom(rows, cols, n_ellipses, sigma, density, seed):
+    """The BASELINE.json phantom (the product's phantom.cpp compiled into liboracle.so): identical bytes
+    to paper_2005_05371_b200.capi.make_phantom, for the CPU reference arm (which must not load the
+    product library)."""
+    out = np.empty((rows, cols), np.uint8)
+    if lib().oracle_make_phantom_u8(rows, cols, n_ellipses, float(sigma), float(density), seed, out.ctypes.data,
+                                    cols):
+        raise ValueError("bad phantom parameters")
+    return out
+
+
+def _bands(rows, threads):
+    threads = max(1, min(threads, rows))
+    return [(rows * i // threads, rows * (i + 1) // threads) for i in range(threads)]
+
+
+def _pool_map(fn, items, threads):
+    # ctypes releases the GIL for the foreign call, so row bands run in parallel
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=max(1, threads)) as ex:
+        return list(ex.map(fn, items))
+
+
+def amf_threaded(img, smax, threads=None):
+    """amf() of the whole image, row bands in parallel (each band's windows read the whole source)."""
+    img, _ = _u8(img)
+    threads = threads or os.cpu_count() or 1
+    parts = _pool_map(lambda ab: amf(img, smax, ab[0], ab[1]), _bands(img.shape[0], threads), threads)
+    return np.concatenate(parts, axis=0)
+
+
+def wiener_threaded(f, win, threads=None):
+    """wiener() with the statistics and the gain over row bands in parallel (W is an exact int64 sum)."""
+    f, _ = _u8(f)
+    threads = threads or os.cpu_count() or 1
+    bands = _bands(f.shape[0], threads)
+    w = sum(_pool_map(lambda ab: wiener_stats(f, win, ab[0], ab[1]), bands, threads))
+    P = f.shape[0] * f.shape[1]
+    y = np.concatenate(_pool_map(lambda ab: wiener_gain(f, win, w, P, ab[0], ab[1]), bands, threads), axis=0)
+    return y, w
+
+
+def hybrid_threaded(g, smax, win, threads=None):
+    f = amf_threaded(g, smax, threads)
+    return wiener_threaded(f, win, threads)
+
+
+def hybrid_many(images, smax, win, threads=None):
+    """oracle hybrid() of independent images (a CT stack), one image per worker thread."""
+    threads = threads or os.cpu_count() or 1
+    return _pool_map(lambda g: hybrid(g, smax, win), list(images), threads)
 
 
 # ---------------- the reference itself (oracle/_ref) ----------------

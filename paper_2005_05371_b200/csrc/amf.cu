@@ -301,8 +301,6 @@ __global__ void __launch_bounds__(GNT, C::MINB) amf_grow_kernel(const __grid_con
     }
 }
 
-int g_num_sms = 0;
-
 }  // namespace
 
 size_t amf_work_bytes(const Plane& p) {
@@ -323,24 +321,15 @@ AmfWork amf_work(uint8_t* base, const Plane& p) {
 
 cudaError_t launch_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, size_t fslice, const AmfWork& work,
                        cudaStream_t stream) {
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e =
-            cudaFuncSetAttribute(amf_k3_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(amf_k3_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
-    if (!g_num_sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    static PerDevice attr_k3[2], occ_k3;
+    cudaError_t e = ensure_smem_attr(attr_k3[0], (const void*)amf_k3_kernel<false>, SMEM);
+    if (e == cudaSuccess) e = ensure_smem_attr(attr_k3[1], (const void*)amf_k3_kernel<true>, SMEM);
+    if (e != cudaSuccess) return e;
+    const int num_sms = device_sms();
     const int out_rows = p.row_end - p.row_begin;
     const bool grow = smax >= 5;
     CUtensorMap tm_src;
-    cudaError_t e = make_tmap_u8(&tm_src, p.src, p.cols, p.rows, p.n_slices, p.spitch, p.sslice, BS, BH);
+    e = make_tmap_u8(&tm_src, p.src, p.cols, p.rows, p.n_slices, p.spitch, p.sslice, BS, BH);
     if (e != cudaSuccess) return e;
     K3Args a;
     a.dst = p.dst;
@@ -364,13 +353,9 @@ cudaError_t launch_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, si
     a.records = work.records;
     a.chunk_rec = work.chunk_rec;
     a.chunk_shift = smax >= 11 ? GrowWide::CHUNK_SHIFT : GrowLean::CHUNK_SHIFT;  // the growth variant below
-    static int per_sm = 0;
-    if (!per_sm) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, amf_k3_kernel<false>, K3T, SMEM);
-        if (per_sm < 1) per_sm = 1;
-    }
+    const int per_sm = occupancy(occ_k3, (const void*)amf_k3_kernel<false>, K3T, SMEM);
     const long long ntiles = (long long)a.tiles_x * a.tiles_y * a.n_slices;
-    const int grid = (int)std::min<long long>(ntiles, (long long)g_num_sms * per_sm);
+    const int grid = (int)std::min<long long>(ntiles, (long long)num_sms * per_sm);
     a.dynamic = ntiles > 8ll * grid;
     e = launch_pdl(fin ? amf_k3_kernel<true> : amf_k3_kernel<false>, dim3(grid), dim3(K3T), SMEM, stream, tm_src, a);
     count_launch();
@@ -383,12 +368,9 @@ cudaError_t launch_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, si
     auto kern = wide ? (fin ? amf_grow_kernel<true, GrowWide> : amf_grow_kernel<false, GrowWide>)
                      : (fin ? amf_grow_kernel<true, GrowLean> : amf_grow_kernel<false, GrowLean>);
     const int vi = (fin ? 1 : 0) + (wide ? 2 : 0);
-    static size_t gconfigured[4] = {0, 0, 0, 0};
-    if (gsm > gconfigured[vi]) {
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm);
-        if (e != cudaSuccess) return e;
-        gconfigured[vi] = gsm;
-    }
+    static PerDevice gattr[4], gocc[4];
+    e = ensure_smem_attr(gattr[vi], (const void*)kern, gsm);
+    if (e != cudaSuccess) return e;
     CUtensorMap tm_g;
     e = make_tmap_u8(&tm_g, p.src, p.cols, p.rows, p.n_slices, p.spitch, p.sslice, geo.box_w, geo.box_h);
     if (e != cudaSuccess) return e;
@@ -414,16 +396,9 @@ cudaError_t launch_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, si
     g.chunk_rec = work.chunk_rec;
     g.chunk_ctr = work.counters + 5;
     g.done = work.counters + 4;
-    static size_t occ_key[4] = {0, 0, 0, 0};
-    static int occ_val[4] = {1, 1, 1, 1};
-    int& gper_sm = occ_val[vi];
-    if (occ_key[vi] != gsm) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&gper_sm, kern, GNT, gsm);
-        if (gper_sm < 1) gper_sm = 1;
-        occ_key[vi] = gsm;
-    }
+    const int gper_sm = occupancy(gocc[vi], (const void*)kern, GNT, gsm);
     // every resident CTA slot busy; each CTA takes a contiguous run of tiles
-    const int ggrid = (int)std::min<long long>(ntiles, (long long)g_num_sms * gper_sm);
+    const int ggrid = (int)std::min<long long>(ntiles, (long long)num_sms * gper_sm);
     e = launch_pdl(kern, dim3(ggrid), dim3(GNT), gsm, stream, tm_g, g);
     count_launch();
     return e;

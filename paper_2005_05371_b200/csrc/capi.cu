@@ -19,8 +19,13 @@
 #include "tma.cuh"
 
 namespace hyb {
-static std::atomic<long long> g_launches{0};
-void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+// Kernel-launch evidence: every launcher calls count_launch(), which adds to the counter of the
+// context whose entry point is running on this thread (CtxScope below) -- per context, so several
+// contexts (devices, host threads) do not mix their counts.
+static thread_local long long* t_launch_counter = nullptr;
+void count_launch() {
+    if (t_launch_counter) ++*t_launch_counter;
+}
 }  // namespace hyb
 
 namespace {
@@ -78,14 +83,44 @@ struct hyb_ctx {
     struct Graph {
         cudaGraphExec_t exec = nullptr;
         long long kernels = 0;
+        std::vector<const void*> bufs;  // the scratch buffers the graph was captured over (buf_signature)
     };
     std::map<GraphKey, Graph> graphs;
     std::map<GraphKey, int> graph_seen;
+    long long launches = 0;            // kernels this context launched (hyb_kernel_launches)
     static constexpr int kMaxChunks = 16;
     cudaEvent_t ev_h2d[kMaxChunks] = {}, ev_gain[kMaxChunks] = {};
 };
 
 namespace {
+
+// Routes count_launch() to ctx->launches for the duration of one entry point.
+struct CtxScope {
+    long long* prev;
+    explicit CtxScope(hyb_ctx* ctx) : prev(hyb::t_launch_counter) { hyb::t_launch_counter = &ctx->launches; }
+    ~CtxScope() { hyb::t_launch_counter = prev; }
+};
+
+// Every context-owned device buffer a captured CUDA graph may reference (pointer and size of each):
+// DevBuf::ensure reallocates when a later call needs more room, so a graph captured before that
+// would replay over freed memory.  A cached graph is replayed only while this signature is unchanged.
+std::vector<const void*> buf_signature(const hyb_ctx* ctx) {
+    std::vector<const void*> v;
+    auto add = [&](const DevBuf& b) {
+        v.push_back(b.ptr);
+        v.push_back(reinterpret_cast<const void*>(b.bytes));
+    };
+    add(ctx->in);
+    add(ctx->out);
+    add(ctx->fin);
+    add(ctx->f);
+    add(ctx->wsum);
+    add(ctx->sbar);
+    add(ctx->amf_q[0]);
+    for (const auto& b : ctx->strip_g) add(b);
+    for (const auto& b : ctx->strip_f) add(b);
+    return v;
+}
 
 int fail(hyb_ctx* ctx, int code, const std::string& msg) {
     if (ctx) ctx->err = msg;
@@ -263,8 +298,9 @@ int hybrid_device(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int co
     } else {
         // split_bands geometry (reference proj/src/tiling.cpp:23-32) with halo rA + rW
         const int h = rA + rW;
-        ctx->strip_g.resize(parts);
-        ctx->strip_f.resize(parts);
+        // grow only: dropping DevBufs would leak their device memory (DevBuf frees in release())
+        if ((int)ctx->strip_g.size() < parts) ctx->strip_g.resize(parts);
+        if ((int)ctx->strip_f.size() < parts) ctx->strip_f.resize(parts);
         struct S { int start, core, hA, hB, fa, fb; };
         std::vector<S> s(parts);
         const int base = rows / parts, extra = rows % parts;
@@ -465,19 +501,21 @@ int hyb_destroy(hyb_ctx* ctx) {
 
 int hyb_set_stream(hyb_ctx* ctx, void* stream) {
     if (!ctx) return HYB_EINVAL;
+    CtxScope scope_(ctx);
     ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own;
     return HYB_OK;
 }
 
 int hyb_set_exclusive(hyb_ctx* ctx, int exclusive) {
     if (!ctx) return HYB_EINVAL;
+    CtxScope scope_(ctx);
     ctx->exclusive = exclusive != 0;
     return HYB_OK;
 }
 
 const char* hyb_last_error(const hyb_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
-int64_t hyb_kernel_launches(const hyb_ctx*) { return hyb::g_launches.load(); }
+int64_t hyb_kernel_launches(const hyb_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 int hyb_validate_smax(int smax) { return (smax <= 1 || smax % 2 == 0) ? HYB_EINVAL : HYB_OK; }
 
@@ -491,6 +529,7 @@ int hyb_amf_u8(hyb_ctx* ctx, const uint8_t* src, size_t src_pitch, int rows, int
                int row_begin, int row_end, int smax, uint8_t* dst, size_t dst_pitch,
                uint8_t* finalized_at, size_t fin_pitch) {
     if (!ctx) return HYB_EINVAL;
+    CtxScope scope_(ctx);
     int st;
     if ((st = check_smax(ctx, smax)) || (st = check_dims(ctx, rows, cols)) ||
         (st = check_range(ctx, rows, row_begin, row_end)) ||
@@ -539,6 +578,7 @@ int hyb_amf_batch_u8(hyb_ctx* ctx, const uint8_t* src, size_t src_pitch, size_t 
                      int n_slices, int rows, int cols, int smax, uint8_t* dst, size_t dst_pitch,
                      size_t dst_slice_stride) {
     if (!ctx) return HYB_EINVAL;
+    CtxScope scope_(ctx);
     int st;
     if ((st = check_smax(ctx, smax)) || (st = check_dims(ctx, rows, cols)) ||
         (st = check_pitch(ctx, src_pitch, cols, "src")) || (st = check_pitch(ctx, dst_pitch, cols, "dst")))
@@ -558,6 +598,7 @@ int hyb_amf_batch_u8(hyb_ctx* ctx, const uint8_t* src, size_t src_pitch, size_t 
 int hyb_wiener_stats_u8(hyb_ctx* ctx, const uint8_t* f, size_t pitch, int rows, int cols,
                         int row_begin, int row_end, int win, int64_t* noise_sum) {
     if (!ctx) return HYB_EINVAL;
+    CtxScope scope_(ctx);
     int st;
     if ((st = check_win(ctx, win)) || (st = check_dims(ctx, rows, cols)) ||
         (st = check_range(ctx, rows, row_begin, row_end)) || (st = check_pitch(ctx, pitch, cols, "f")))
@@ -596,6 +637,7 @@ int hyb_wiener_gain_u8(hyb_ctx* ctx, const uint8_t* f, size_t pitch, int rows, i
                        int row_begin, int row_end, int win, const int64_t* noise_sum,
                        int64_t pixel_count, uint8_t* y, size_t y_pitch) {
     if (!ctx) return HYB_EINVAL;
+    CtxScope scope_(ctx);
     int st;
     if ((st = check_win(ctx, win)) || (st = check_dims(ctx, rows, cols)) ||
         (st = check_range(ctx, rows, row_begin, row_end)) || (st = check_pitch(ctx, pitch, cols, "f")) ||
@@ -643,6 +685,7 @@ int hyb_wiener_gain_u8(hyb_ctx* ctx, const uint8_t* f, size_t pitch, int rows, i
 int hyb_wiener_u8(hyb_ctx* ctx, const uint8_t* f, size_t pitch, int rows, int cols, int win,
                   uint8_t* y, size_t y_pitch, int64_t* noise_sum_out) {
     if (!ctx) return HYB_EINVAL;
+    CtxScope scope_(ctx);
     int st;
     if ((st = check_win(ctx, win)) || (st = check_dims(ctx, rows, cols)) ||
         (st = check_pitch(ctx, pitch, cols, "f")) || (st = check_pitch(ctx, y_pitch, cols, "y")))
@@ -689,6 +732,7 @@ static int hybrid_u8_impl(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows
 int hyb_hybrid_u8(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int cols, int smax,
                   int win, int parts, uint8_t* y, size_t y_pitch, hyb_stats* stats) {
     if (!ctx) return HYB_EINVAL;
+    CtxScope scope_(ctx);
     // Untimed calls on device buffers or pinned host buffers replay a cached CUDA graph.
     cudaPointerAttributes ga{}, ya{};
     const bool gok = g && cudaPointerGetAttributes(&ga, g) == cudaSuccess;
@@ -703,13 +747,23 @@ int hyb_hybrid_u8(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int co
     if (!graphable) return hybrid_u8_impl(ctx, g, pitch, rows, cols, smax, win, parts, y, y_pitch, stats, false);
     const hyb_ctx::GraphKey key{g, y, pitch, y_pitch, rows, cols, smax, win, parts, ctx->stream};
     auto it = ctx->graphs.find(key);
+    if (it != ctx->graphs.end() && it->second.bufs != buf_signature(ctx)) {
+        // scratch reallocated since the capture (a larger image, a batch, more strips): drop the graph,
+        // run plainly now (re-allocating what this call needs) and re-capture on the next call
+        HYB_CHECK(cudaSetDevice(ctx->device));
+        cudaGraphExecDestroy(it->second.exec);
+        ctx->graphs.erase(it);
+        ctx->graph_seen[key] = 1;
+        return hybrid_u8_impl(ctx, g, pitch, rows, cols, smax, win, parts, y, y_pitch, nullptr, false);
+    }
     if (it == ctx->graphs.end()) {
         int& seen = ctx->graph_seen[key];
         if (seen++ == 0)  // first use: plain run (allocates every buffer the sequence needs)
             return hybrid_u8_impl(ctx, g, pitch, rows, cols, smax, win, parts, y, y_pitch, nullptr, false);
         HYB_CHECK(cudaSetDevice(ctx->device));
         HYB_CHECK(cudaStreamSynchronize(ctx->stream));
-        const long long k0 = hyb::g_launches.load();
+        const long long k0 = ctx->launches;
+        const std::vector<const void*> sig = buf_signature(ctx);
         HYB_CHECK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
         int st = hybrid_u8_impl(ctx, g, pitch, rows, cols, smax, win, parts, y, y_pitch, nullptr, true);
         cudaGraph_t graph = nullptr;
@@ -719,12 +773,18 @@ int hyb_hybrid_u8(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int co
             return st;
         }
         if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaStreamEndCapture");
+        if (buf_signature(ctx) != sig) {
+            // the captured call allocated (it cannot: the plain run before it did) -- do not keep it
+            cudaGraphDestroy(graph);
+            return fail(ctx, HYB_ECUDA, "scratch reallocated during graph capture");
+        }
         hyb_ctx::Graph gr;
         e = cudaGraphInstantiate(&gr.exec, graph, 0);
         cudaGraphDestroy(graph);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaGraphInstantiate");
-        gr.kernels = hyb::g_launches.load() - k0;
-        hyb::g_launches.fetch_sub(gr.kernels);  // counted again at each replay
+        gr.kernels = ctx->launches - k0;
+        gr.bufs = sig;
+        ctx->launches = k0;  // counted at each replay instead
         if (ctx->graphs.size() >= 4096) {
             for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second.exec);
             ctx->graphs.clear();
@@ -732,7 +792,7 @@ int hyb_hybrid_u8(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int co
         it = ctx->graphs.emplace(key, gr).first;
     }
     HYB_CHECK(cudaGraphLaunch(it->second.exec, ctx->stream));
-    hyb::g_launches.fetch_add(it->second.kernels);
+    ctx->launches += it->second.kernels;
     if (ga.type != cudaMemoryTypeDevice || ya.type != cudaMemoryTypeDevice)
         HYB_CHECK(cudaStreamSynchronize(ctx->stream));
     return HYB_OK;
@@ -749,6 +809,7 @@ static void small_times(hyb_ctx* ctx, hyb_stats* stats) {
 static int hybrid_u8_impl(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int cols, int smax,
                           int win, int parts, uint8_t* y, size_t y_pitch, hyb_stats* stats, bool capturing) {
     if (!ctx) return HYB_EINVAL;
+    CtxScope scope_(ctx);
     ctx->small_used = false;
     int st;
     if ((st = check_smax(ctx, smax)) || (st = check_win(ctx, win)) || (st = check_dims(ctx, rows, cols)) ||
@@ -831,6 +892,7 @@ static int hybrid_u8_impl(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows
 int hyb_contrast_stretch_u8(hyb_ctx* ctx, const uint8_t* src, size_t pitch, int rows, int cols, uint8_t* dst,
                             size_t dst_pitch) {
     if (!ctx) return HYB_EINVAL;
+    CtxScope scope_(ctx);
     int st;
     if ((st = check_dims(ctx, rows, cols)) || (st = check_pitch(ctx, pitch, cols, "src")) ||
         (st = check_pitch(ctx, dst_pitch, cols, "dst")))
@@ -865,6 +927,7 @@ int hyb_contrast_stretch_u8(hyb_ctx* ctx, const uint8_t* src, size_t pitch, int 
 int hyb_hybrid_stretch_u8(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int cols, int smax, int win,
                           int parts, uint8_t* y, size_t y_pitch, hyb_stats* stats) {
     if (!ctx) return HYB_EINVAL;
+    CtxScope scope_(ctx);
     int st;
     if ((st = check_dims(ctx, rows, cols)) || (st = check_pitch(ctx, y_pitch, cols, "y"))) return st;
     if (!y) return fail(ctx, HYB_EINVAL, "null image pointer");
@@ -909,6 +972,7 @@ static int stage_f64(hyb_ctx* ctx, DevBuf& buf, const double* src, size_t pitch,
 int hyb_wiener_freq_f64(hyb_ctx* ctx, const double* f, size_t pitch, int rows, int cols, double sigma2, int clamp,
                         double* out, size_t out_pitch) {
     if (!ctx) return HYB_EINVAL;
+    CtxScope scope_(ctx);
     int st;
     if ((st = check_dims(ctx, rows, cols))) return st;
     if (pitch < (size_t)cols || out_pitch < (size_t)cols) return fail(ctx, HYB_EINVAL, "pitch smaller than cols");
@@ -939,6 +1003,7 @@ int hyb_wiener_freq_f64(hyb_ctx* ctx, const double* f, size_t pitch, int rows, i
 int hyb_contrast_stretch_f64(hyb_ctx* ctx, const double* src, size_t pitch, int rows, int cols, double* dst,
                              size_t dst_pitch) {
     if (!ctx) return HYB_EINVAL;
+    CtxScope scope_(ctx);
     int st;
     if ((st = check_dims(ctx, rows, cols))) return st;
     if (pitch < (size_t)cols || dst_pitch < (size_t)cols) return fail(ctx, HYB_EINVAL, "pitch smaller than cols");
@@ -965,6 +1030,7 @@ int hyb_contrast_stretch_f64(hyb_ctx* ctx, const double* src, size_t pitch, int 
 
 int hyb_noise_robust_f64(hyb_ctx* ctx, const double* f, size_t pitch, int rows, int cols, double* sigma2) {
     if (!ctx) return HYB_EINVAL;
+    CtxScope scope_(ctx);
     int st;
     if ((st = check_dims(ctx, rows, cols))) return st;
     if (pitch < (size_t)cols) return fail(ctx, HYB_EINVAL, "pitch smaller than cols");
@@ -987,6 +1053,7 @@ int hyb_noise_robust_f64(hyb_ctx* ctx, const double* f, size_t pitch, int rows, 
 int hyb_noise_reference_f64(hyb_ctx* ctx, const double* f, size_t pitch, const double* ref, size_t ref_pitch,
                             int rows, int cols, double* sigma2) {
     if (!ctx) return HYB_EINVAL;
+    CtxScope scope_(ctx);
     int st;
     if ((st = check_dims(ctx, rows, cols))) return st;
     if (pitch < (size_t)cols || ref_pitch < (size_t)cols) return fail(ctx, HYB_EINVAL, "pitch smaller than cols");
@@ -1082,6 +1149,7 @@ int hyb_hybrid_batch_u8(hyb_ctx* ctx, const uint8_t* g, size_t pitch, size_t sli
                         int n_slices, int rows, int cols, int smax, int win, uint8_t* y,
                         size_t y_pitch, size_t y_slice_stride, int64_t* noise_sums) {
     if (!ctx) return HYB_EINVAL;
+    CtxScope scope_(ctx);
     int st;
     if ((st = check_smax(ctx, smax)) || (st = check_win(ctx, win)) || (st = check_dims(ctx, rows, cols)) ||
         (st = check_pitch(ctx, pitch, cols, "g")) || (st = check_pitch(ctx, y_pitch, cols, "y")))

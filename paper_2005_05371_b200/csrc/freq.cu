@@ -173,12 +173,7 @@ __global__ void __launch_bounds__(FT) stretch_f64_kernel(const double* __restric
 }
 
 int grid_for(long long n) {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int sms = device_sms();
     return (int)std::max(1ll, std::min((long long)sms * 8, (n + FT - 1) / FT));
 }
 

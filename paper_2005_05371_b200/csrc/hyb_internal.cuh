@@ -1,11 +1,70 @@
 // hyb_internal.cuh -- shared declarations of libhybrid_cuda (kernels + launchers).
 #pragma once
 #include <algorithm>
+#include <atomic>
 #include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
 
 namespace hyb {
+
+// ---- per-device launch setup ----
+// Function attributes (the >48 KB dynamic shared-memory opt-in), occupancies and SM counts belong to
+// one device; a process may drive several devices (one context each, or a multi-device context) from
+// several host threads.  Each call site keeps one PerDevice cache (static storage: zero-initialised);
+// racing threads may compute the same value twice, which is harmless.
+constexpr int kMaxDevices = 64;
+struct PerDevice {
+    std::atomic<long long> v[kMaxDevices];
+};
+inline int current_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d;
+}
+inline int device_sms() {
+    static PerDevice cache;
+    const int d = current_device();
+    if (d < kMaxDevices) {
+        const long long c = cache.v[d].load(std::memory_order_acquire);
+        if (c) return (int)c;
+    }
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
+    if (n < 1) n = 1;
+    if (d < kMaxDevices) cache.v[d].store(n, std::memory_order_release);
+    return n;
+}
+// Dynamic shared-memory opt-in of `kern` on the current device, raised to at least `smem` bytes.
+inline cudaError_t ensure_smem_attr(PerDevice& pd, const void* kern, size_t smem) {
+    const int d = current_device();
+    if (d < kMaxDevices && (size_t)pd.v[d].load(std::memory_order_acquire) >= smem) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess && d < kMaxDevices) {
+        long long cur = pd.v[d].load(std::memory_order_relaxed);
+        while (cur < (long long)smem && !pd.v[d].compare_exchange_weak(cur, (long long)smem)) {
+        }
+    }
+    return e;
+}
+// Resident blocks per SM of `kern` on the current device at (threads, smem), cached per device (the
+// cache entry is keyed by smem; at least 1).
+inline int occupancy(PerDevice& pd, const void* kern, int threads, size_t smem) {
+    const int d = current_device();
+    const long long key = (long long)smem << 16;
+    if (d < kMaxDevices) {
+        const long long c = pd.v[d].load(std::memory_order_acquire);
+        if (c && (c & ~0xFFFFll) == key) return (int)(c & 0xFFFF);
+    }
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, threads, smem) != cudaSuccess) {
+        cudaGetLastError();
+        n = 0;
+    }
+    if (n < 1) n = 1;
+    if (d < kMaxDevices) pd.v[d].store(key | n, std::memory_order_release);
+    return n;
+}
 
 // Geometry of one filtering launch: `n_slices` images of rows x cols with byte
 // pitches and slice strides.  Output row i corresponds to input row row_begin + i.

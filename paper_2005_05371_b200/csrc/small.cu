@@ -261,8 +261,6 @@ size_t small_smem(int slot_bytes) {
     return SHDR + (size_t)STPC * slot_bytes + STPC * 512 + SNW * WPIX + 2 * STPC * 4096 * 2 + 128;
 }
 
-int g_ssms = 0;
-
 template <int RW>
 cudaError_t launch_small_rw(const SmallPlan& pl, const SmallBufs& bf, int rows, int cols, int smax,
                             bool cooperative, cudaStream_t stream) {
@@ -290,12 +288,9 @@ cudaError_t launch_small_rw(const SmallPlan& pl, const SmallBufs& bf, int rows, 
     if (e != cudaSuccess) return e;
     auto kern = hybrid_small_kernel<RW>;
     const size_t smem = small_smem(pl.slot_bytes);
-    static size_t configured = 0;
-    if (smem > configured) {
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        configured = smem;
-    }
+    static PerDevice smem_attr;
+    e = ensure_smem_attr(smem_attr, (const void*)kern, smem);
+    if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(pl.grid);
     cfg.blockDim = dim3(SNT);
@@ -320,28 +315,25 @@ SmallPlan plan_small(int rows, int cols, int smax, int win) {
     const GGeo geo = make_ggeo(smax);
     const int rw = (win - 1) / 2;
     pl.slot_bytes = std::max(geo.b_bytes, (FBS * (TH + 2 * rw) + 127) / 128 * 128);
-    if (!g_ssms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_ssms, cudaDevAttrMultiProcessorCount, dev);
-    }
-    static int per_sm[4] = {-1, -1, -1, -1};
-    static size_t per_sm_smem[4] = {0, 0, 0, 0};
+    static PerDevice attr[4], occ[4];
     const size_t smem = small_smem(pl.slot_bytes);
-    if (per_sm[rw] < 0 || per_sm_smem[rw] != smem) {
-        const void* k = rw == 0   ? (const void*)hybrid_small_kernel<0>
-                        : rw == 1 ? (const void*)hybrid_small_kernel<1>
-                        : rw == 2 ? (const void*)hybrid_small_kernel<2>
-                                  : (const void*)hybrid_small_kernel<3>;
-        cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[rw], k, SNT, smem) != cudaSuccess)
-            per_sm[rw] = 0;
-        per_sm_smem[rw] = smem;
-        cudaGetLastError();
+    const void* k = rw == 0   ? (const void*)hybrid_small_kernel<0>
+                    : rw == 1 ? (const void*)hybrid_small_kernel<1>
+                    : rw == 2 ? (const void*)hybrid_small_kernel<2>
+                              : (const void*)hybrid_small_kernel<3>;
+    static PerDevice carve[4];
+    const int dev = current_device();
+    if (dev >= kMaxDevices || !carve[rw].v[dev].load(std::memory_order_acquire)) {
+        cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);  // a hint; before occupancy
+        if (dev < kMaxDevices) carve[rw].v[dev].store(1, std::memory_order_release);
     }
+    if (ensure_smem_attr(attr[rw], k, smem) != cudaSuccess) {
+        cudaGetLastError();
+        return pl;
+    }
+    const int per_sm = occupancy(occ[rw], k, SNT, smem);
     const long long ntiles = (long long)((cols + TW - 1) / TW) * ((rows + TH - 1) / TH);
-    const long long capacity = (long long)g_ssms * per_sm[rw];
+    const long long capacity = (long long)device_sms() * per_sm;
     if (capacity <= 0 || ntiles > capacity * STPC) return pl;
     pl.grid = (int)std::min<long long>(capacity, ntiles);
     pl.ok = true;

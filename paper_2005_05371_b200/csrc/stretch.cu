@@ -89,25 +89,19 @@ __global__ void __launch_bounds__(XT) map_kernel(const uint8_t* __restrict__ src
     }
 }
 
-int g_xsms = 0;
-
 }  // namespace
 
 cudaError_t launch_contrast_stretch(const uint8_t* src, size_t spitch, int rows, int cols, uint8_t* dst,
                                     size_t dpitch, unsigned* mm, cudaStream_t stream) {
-    if (!g_xsms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_xsms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int sms = device_sms();
     cudaError_t e = cudaMemsetAsync(mm, 0xFF, 2 * sizeof(unsigned), stream);  // lo = 255+, 255 - hi = 255+
     if (e != cudaSuccess) return e;
     const long long px = (long long)rows * cols;
-    const int grid = (int)std::max(1ll, std::min((long long)g_xsms * 8, (px + XT * 16 - 1) / (XT * 16)));
+    const int grid = (int)std::max(1ll, std::min((long long)sms * 8, (px + XT * 16 - 1) / (XT * 16)));
     e = launch_pdl(minmax_kernel, dim3(grid), dim3(XT), 0, stream, src, spitch, rows, cols, mm);
     count_launch();
     if (e != cudaSuccess) return e;
-    const int mgrid = (int)std::max(1ll, std::min((long long)g_xsms * 8, (px + XT * 4 - 1) / (XT * 4)));
+    const int mgrid = (int)std::max(1ll, std::min((long long)sms * 8, (px + XT * 4 - 1) / (XT * 4)));
     e = launch_pdl(map_kernel, dim3(mgrid), dim3(XT), 0, stream, src, spitch, rows, cols, dst, dpitch,
                    (const unsigned*)mm);
     count_launch();

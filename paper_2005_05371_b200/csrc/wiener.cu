@@ -202,12 +202,10 @@ cudaError_t launch(const Plane& p, int win, unsigned long long* wsum, const long
                    long long pixel_count, cudaStream_t stream) {
     const WGeo geo = make_wgeo(win);
     const size_t smem = wsmem_bytes(geo);
-    static size_t configured = 0;
-    if (smem > configured) {
-        cudaError_t e = cudaFuncSetAttribute(wiener_kernel<GAIN>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    static PerDevice attr;
+    {
+        const cudaError_t e = ensure_smem_attr(attr, (const void*)wiener_kernel<GAIN>, smem);
         if (e != cudaSuccess) return e;
-        configured = smem;
     }
     const dim3 grid((p.cols + TW - 1) / TW, (p.row_end - p.row_begin + TH - 1) / TH, p.n_slices);
     cudaError_t e = launch_pdl(wiener_kernel<GAIN>, dim3(grid), dim3(NT), smem, stream, p, win, wsum, wread,
@@ -327,24 +325,15 @@ __global__ void __launch_bounds__(FNW * 32, GAIN ? 4 : 3) wiener_fast_kernel(con
     }
 }
 
-int g_wsms = 0;
-
 template <int RW, bool GAIN, int FH>
 cudaError_t launch_fast(const Plane& p, unsigned long long* wsum, const long long* wread, long long pixel_count,
                         cudaStream_t stream) {
     constexpr int SLOT = kFastSmemSlot(RW, FH);
     constexpr size_t smem = 128 + (size_t)FNW * 2 * SLOT + 128;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(wiener_fast_kernel<RW, GAIN, FH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
+    static PerDevice attr, occ;
+    {
+        const cudaError_t e = ensure_smem_attr(attr, (const void*)wiener_fast_kernel<RW, GAIN, FH>, smem);
         if (e != cudaSuccess) return e;
-        configured = true;
-    }
-    if (!g_wsms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_wsms, cudaDevAttrMultiProcessorCount, dev);
     }
     CUtensorMap tm;
     cudaError_t e = make_tmap_u8(&tm, p.src, p.cols, p.rows, p.n_slices, p.spitch, p.sslice, FBS, FH + 2 * RW);
@@ -363,13 +352,9 @@ cudaError_t launch_fast(const Plane& p, unsigned long long* wsum, const long lon
     a.wsum = wsum;
     a.wread = wread;
     a.pixel_count = pixel_count;
-    static int per_sm = 0;
-    if (!per_sm) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, wiener_fast_kernel<RW, GAIN, FH>, FNW * 32, smem);
-        if (per_sm < 1) per_sm = 1;
-    }
+    const int per_sm = occupancy(occ, (const void*)wiener_fast_kernel<RW, GAIN, FH>, FNW * 32, smem);
     const long long ntiles = (long long)a.tiles_x * a.tiles_y * a.n_slices;
-    const long long warps = std::min<long long>(ntiles, (long long)g_wsms * per_sm * FNW);
+    const long long warps = std::min<long long>(ntiles, (long long)device_sms() * per_sm * FNW);
     const int grid = (int)((warps + FNW - 1) / FNW);
     const cudaError_t le =
         launch_pdl(wiener_fast_kernel<RW, GAIN, FH>, dim3(grid), dim3(FNW * 32), smem, stream, tm, a);

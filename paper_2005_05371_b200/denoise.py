@@ -18,8 +18,21 @@ from . import capi
 from .capi import InvalidArgument, check, lib
 
 
-def _ctx(ctx):
-    c = ctx or capi.default_context()
+def _ctx(ctx, *arrays):
+    """The context for a call on `arrays`: the caller's, else the default context of the device the
+    CUDA tensors live on (device 0 for host arrays).  Inputs on different devices, or on a device
+    other than the given context's, are rejected."""
+    devs = {a.device.index for a in arrays
+            if a is not None and _is_torch(a) and getattr(a, "is_cuda", False)}
+    if len(devs) > 1:
+        raise InvalidArgument(f"inputs on different CUDA devices: {sorted(devs)}")
+    dev = devs.pop() if devs else None
+    if ctx is None:
+        c = capi.default_context(dev if dev is not None else 0)
+    else:
+        c = ctx
+        if dev is not None and dev != c.device:
+            raise InvalidArgument(f"tensor on cuda:{dev} but the context drives device {c.device}")
     _bind_torch_stream(c)
     return c.ptr
 
@@ -119,7 +132,7 @@ def adaptive_median_rows(src, smax: int, row_begin: int, row_end: int, finalized
     sp, spitch = capi.buf(src)
     dp, dpitch = capi.buf(out) if out.shape[0] else (0, cols)
     fp, fpitch = capi.buf(fin) if fin is not None and fin.shape[0] else (None, cols)
-    c = _ctx(ctx)
+    c = _ctx(ctx, src, out, fin)
     check(lib.hyb_amf_u8(c, sp, spitch, rows, cols, row_begin, row_end, smax, dp, dpitch, fp, fpitch), c)
     return (out, fin) if finalized_at else out
 
@@ -158,7 +171,7 @@ def wiener_local(f, win: int = 3, ctx=None):
     fp, fpitch = capi.buf(f)
     yp, ypitch = capi.buf(y)
     w = ctypes.c_int64(0)
-    c = _ctx(ctx)
+    c = _ctx(ctx, f, y)
     check(lib.hyb_wiener_u8(c, fp, fpitch, rows, cols, win, yp, ypitch, ctypes.byref(w)), c)
     return y, w.value
 
@@ -192,7 +205,7 @@ def hybrid_denoise(noisy, config: FilterConfig, ctx=None) -> HybridResult:
     gp, gpitch = capi.buf(noisy)
     yp, ypitch = capi.buf(y)
     st = capi.HybStats()
-    c = _ctx(ctx)
+    c = _ctx(ctx, noisy, y)
     check(lib.hyb_hybrid_u8(c, gp, gpitch, rows, cols, config.smax, config.wiener_window, config.parts,
                             yp, ypitch, ctypes.byref(st)), c)
     return HybridResult(y, st.sigma2, st.t_adaptive, st.t_wiener, 0.0, st.noise_sum, st.t_total)
@@ -212,14 +225,14 @@ def contrast_stretch(image, ctx=None):
         else:
             out = np.empty((rows, cols), np.float64)
             op = out.ctypes.data
-        c = _ctx(ctx)
+        c = _ctx(ctx, image, out)
         check(lib.hyb_contrast_stretch_f64(c, p, pitch, rows, cols, op, cols), c)
         return out
     rows, cols = _shape(image)
     out = _empty_like(image, rows, cols)
     sp, spitch = capi.buf(image)
     dp, dpitch = capi.buf(out)
-    c = _ctx(ctx)
+    c = _ctx(ctx, image, out)
     check(lib.hyb_contrast_stretch_u8(c, sp, spitch, rows, cols, dp, dpitch), c)
     return out
 
@@ -233,7 +246,7 @@ def hybrid_denoise_stretched(noisy, config: FilterConfig, ctx=None) -> HybridRes
     gp, gpitch = capi.buf(noisy)
     yp, ypitch = capi.buf(y)
     st = capi.HybStats()
-    c = _ctx(ctx)
+    c = _ctx(ctx, noisy, y)
     check(lib.hyb_hybrid_stretch_u8(c, gp, gpitch, rows, cols, config.smax, config.wiener_window, config.parts,
                                     yp, ypitch, ctypes.byref(st)), c)
     return HybridResult(y, st.sigma2, st.t_adaptive, st.t_wiener, 0.0, st.noise_sum, st.t_total)
@@ -257,7 +270,7 @@ def hybrid_denoise_batch(stack, smax: int, win: int, ctx=None):
     gp, gpitch = capi.buf(stack)
     yp, ypitch = capi.buf(y)
     w = (ctypes.c_int64 * n)()
-    c = _ctx(ctx)
+    c = _ctx(ctx, stack, y)
     check(lib.hyb_hybrid_batch_u8(c, gp, gpitch, sstride, n, rows, cols, smax, win, yp, ypitch, ystride, w), c)
     return y, list(w)
 
@@ -400,7 +413,7 @@ def wiener_filter(image, sigma2: float, clamp: bool = True, ctx=None):
     else:
         out = np.empty((rows, cols), np.float64)
         op, opitch = out.ctypes.data, cols
-    c = _ctx(ctx)
+    c = _ctx(ctx, image, out)
     check(lib.hyb_wiener_freq_f64(c, p, pitch, rows, cols, float(sigma2), int(bool(clamp)), op, opitch), c)
     return out
 
@@ -409,7 +422,7 @@ def estimate_noise_variance(image, reference=None, ctx=None):
     """estimate_noise_variance -- reference proj/src/wiener.cpp:30-52 on float64 images: with a reference
     the mean squared difference, else (median |p - median3(p)| / 0.6745)^2.  Returns (sigma2, source)."""
     p, pitch, rows, cols = _f64(image)
-    c = _ctx(ctx)
+    c = _ctx(ctx, image, reference)
     out = ctypes.c_double(0.0)
     if reference is not None:
         rp, rpitch, rr, rc = _f64(reference)

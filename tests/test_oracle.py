@@ -138,6 +138,47 @@ def test_oracle_wiener_noise_sum_is_partition_invariant():
         assert sum(oracle.wiener_stats(f, win, a, b) for a, b in zip(cuts, cuts[1:])) == whole
 
 
+# W1 pinned to a published third-party implementation: scipy.signal.wiener (scipy 1.x, the MATLAB
+# wiener2 estimator: local mean / variance over an N x N box, noise = the mean local variance, output
+# lMean where lVar < noise, else lMean + (1 - noise / lVar) (im - lMean)).  Edge replication is supplied
+# by padding the image (scipy pads with zeros, which the crop removes); the noise is passed as the
+# oracle's exact nu = W / (n^2 P).  scipy computes in float64; the result is rounded half up.
+def _scipy_w1(f, win, nu):
+    from scipy.signal import wiener as sp_wiener
+    r = win // 2
+    pad = np.pad(f.astype(np.float64), r, mode="edge")
+    with np.errstate(divide="ignore", invalid="ignore"):
+        out = sp_wiener(pad, (win, win), noise=nu)
+    out = out[r:r + f.shape[0], r:r + f.shape[1]] if r else out
+    return np.clip(np.floor(out + 0.5), 0, 255).astype(np.uint8)
+
+
+@pytest.mark.parametrize("win", [3, 5, 7])
+@pytest.mark.parametrize("seed,shape,sp", [(0, (97, 131), 0.0), (1, (64, 200), 0.1), (2, (150, 77), 0.3)])
+def test_oracle_wiener_matches_scipy_signal_wiener(win, seed, shape, sp):
+    pytest.importorskip("scipy")
+    from numpy.lib.stride_tricks import sliding_window_view
+    rng = np.random.default_rng(seed)
+    base = np.clip(rng.normal(120, 40, shape), 0, 255)
+    u = rng.random(shape)
+    base[u < sp / 2] = 0
+    base[(u >= sp / 2) & (u < sp)] = 255
+    f = np.floor(base + 0.5).astype(np.uint8)
+    y, w = oracle.wiener(f, win)
+    n, P = win * win, f.size
+    nu = w / (n * n * P)
+    # nu equals numpy's mean local variance (edge-replicated windows)
+    r = win // 2
+    wins = sliding_window_view(np.pad(f.astype(np.float64), r, mode="edge"), (win, win))
+    lvar = wins.var(axis=(2, 3))
+    assert abs(nu - lvar.mean()) <= 1e-9 * max(1.0, nu)
+    ys = _scipy_w1(f, win, nu)
+    d = np.abs(y.astype(np.int16) - ys.astype(np.int16))
+    # north_star tolerance (<= 1 LSB, >= 99.99 % exact); the exact-rational oracle agrees bit for bit
+    assert d.max() <= 1 and (d == 0).mean() >= 0.9999
+    np.testing.assert_array_equal(y, ys)
+
+
 # ---------------------------------------------------------------- contrast_stretch
 
 def _stretch_ref_double(img):
