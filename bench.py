@@ -116,6 +116,17 @@ class ClockSampler:
         except Exception:
             self.nv = None
 
+    def poll_until(self, event):
+        """Sample synchronously until `event` (recorded after the timed launches) completes: the GPU is
+        busy with the timed region the whole time, whatever the Python thread scheduling."""
+        while not event.query():
+            if self.nv:
+                try:
+                    self._sample()
+                except Exception:
+                    pass
+            time.sleep(0.0005)
+
     def _sample(self):
         clk = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
         mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
@@ -355,9 +366,9 @@ def run_gpu(args, cfg, c):
         else:
             hybrid_strip_step(backend, plan, g, f_strip, y, w_dev)
 
-    def timed(fn, k):
+    def timed(fn, k, sampler=None):
         """k calls of fn between a barrier + synchronize on both sides; CUDA events on the launch
-        stream; the max over ranks."""
+        stream; the max over ranks.  `sampler` polls the clocks until the last launch completes."""
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -366,6 +377,8 @@ def run_gpu(args, cfg, c):
         for i in range(k):
             fn(i)
         e1.record(stream)
+        if sampler is not None:
+            sampler.poll_until(e1)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
         if world > 1:
@@ -382,7 +395,7 @@ def run_gpu(args, cfg, c):
     torch.cuda.synchronize()
     l0 = ctx.launches()
     with ClockSampler(local) as clk:
-        ms = timed(step, args.steps)
+        ms = timed(step, args.steps, clk)
     launches = ctx.launches() - l0
     px_total = rows * cols * slices
     ms_step = ms / args.steps

@@ -53,6 +53,20 @@ typedef struct hyb_stats {
  * reference's per-call pool (proj/src/parallel.cpp:62-65). */
 hyb_ctx* hyb_create(int device, int* status);
 int hyb_destroy(hyb_ctx* ctx);
+/* Multi-device context: the paper's 2/4/8-partition scheme on one box, behind the same entry points
+ * (reference FilterConfig.parts / workers, proj/include/denoise/parallel.hpp:13-19, executed by
+ * adaptive_median_parallel proj/src/parallel.cpp:27-70; SURVEY.md 8(b) sketched hyb_create(n_gpus,
+ * device_ids)).  Strip i of an image runs on device_ids[i] (ids may repeat: several strips on one
+ * GPU); peer access is enabled between all pairs of distinct devices that support it (NVLink).
+ * hyb_hybrid_u8 on this context splits the image into n_devices horizontal strips (split_bands
+ * geometry, halo (smax-1)/2 + (win-1)/2 rows read straight from the caller's buffer), filters them
+ * concurrently, reduces the exact int64 noise sum over NVLink (each device reads its peers'
+ * partials) and applies the gain -- bit-identical to one device for every n.  hyb_hybrid_batch_u8
+ * shards the slices of a stack by contiguous chunks, one per device.  Every other entry point runs on
+ * device_ids[0].  hyb_destroy releases all devices' resources. */
+hyb_ctx* hyb_create_multi(int n_devices, const int* device_ids, int* status);
+/* Number of devices a context drives (1 for hyb_create); device_ids (nullable) receives them. */
+int hyb_context_devices(const hyb_ctx* ctx, int* device_ids);
 /* Use a caller-owned cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream); NULL restores the context stream. */
 int hyb_set_stream(hyb_ctx* ctx, void* stream);
 /* exclusive != 0: the caller guarantees that no other kernels run on this device while this

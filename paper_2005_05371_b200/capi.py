@@ -22,7 +22,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)),
 
 # Every symbol include/hybrid_cuda.h declares (checked by tests/test_capi_symbols.py).
 EXPORTED = (
-    "hyb_create", "hyb_destroy", "hyb_set_stream", "hyb_set_exclusive", "hyb_last_error", "hyb_kernel_launches",
+    "hyb_create", "hyb_create_multi", "hyb_context_devices", "hyb_destroy", "hyb_set_stream", "hyb_set_exclusive", "hyb_last_error", "hyb_kernel_launches",
     "hyb_validate_smax", "hyb_validate_config", "hyb_amf_u8", "hyb_amf_batch_u8",
     "hyb_wiener_stats_u8", "hyb_wiener_gain_u8", "hyb_wiener_u8", "hyb_hybrid_u8",
     "hyb_hybrid_batch_u8", "hyb_contrast_stretch_u8", "hyb_hybrid_stretch_u8",
@@ -58,6 +58,8 @@ def _load():
     P, Pi64 = c_void_p, POINTER(c_int64)
     sig = {
         "hyb_create": (c_void_p, [c_int, POINTER(c_int)]),
+        "hyb_create_multi": (c_void_p, [c_int, POINTER(c_int), POINTER(c_int)]),
+        "hyb_context_devices": (c_int, [P, POINTER(c_int)]),
         "hyb_destroy": (c_int, [P]),
         "hyb_set_stream": (c_int, [P, c_void_p]),
         "hyb_set_exclusive": (c_int, [P, c_int]),
@@ -104,15 +106,27 @@ def check(status: int, ctx=None) -> None:
 
 
 class Context:
-    """Owns one hyb_ctx (one CUDA device, one stream, pooled device scratch)."""
+    """Owns one hyb_ctx (one CUDA device, one stream, pooled device scratch), or with `devices` a
+    multi-device context (hyb_create_multi: one strip / slice chunk per listed device)."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, devices=None):
         st = c_int(0)
-        self.ptr = lib.hyb_create(device, ctypes.byref(st))
+        if devices is not None:
+            ids = (c_int * len(devices))(*devices)
+            self.ptr = lib.hyb_create_multi(len(devices), ids, ctypes.byref(st))
+            device = devices[0] if devices else device
+        else:
+            self.ptr = lib.hyb_create(device, ctypes.byref(st))
         if not self.ptr:
-            raise CudaError(f"hyb_create(device={device}) failed with status {st.value} "
+            raise CudaError(f"hyb_create(device={device}, devices={devices}) failed with status {st.value} "
                             "(no CUDA device?)")
         self.device = device
+
+    def devices(self) -> list:
+        n = lib.hyb_context_devices(self.ptr, None)
+        ids = (c_int * n)()
+        lib.hyb_context_devices(self.ptr, ids)
+        return list(ids)
 
     def close(self) -> None:
         if self.ptr:

@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/hybrid_cuda.h"
@@ -88,6 +89,13 @@ struct hyb_ctx {
     std::map<GraphKey, Graph> graphs;
     std::map<GraphKey, int> graph_seen;
     long long launches = 0;            // kernels this context launched (hyb_kernel_launches)
+    // Multi-device context (hyb_create_multi): this context drives strip 0 on `device`; peers[i - 1]
+    // drives strip i on its own device (ids may repeat).  peer_ok[i * n + j]: strip i's kernels can read
+    // strip j's device memory (same device, or peer access enabled).
+    std::vector<hyb_ctx*> peers;
+    std::vector<char> peer_ok;
+    DevBuf wparts, wtot, mg_in, mg_out;  // gathered partial W, total W, staged batch chunk
+    cudaEvent_t ev_stats = nullptr, ev_done = nullptr, ev_start = nullptr;
     static constexpr int kMaxChunks = 16;
     cudaEvent_t ev_h2d[kMaxChunks] = {}, ev_gain[kMaxChunks] = {};
 };
@@ -136,6 +144,11 @@ int cuda_fail(hyb_ctx* ctx, cudaError_t e, const char* where) {
     do {                                                        \
         cudaError_t e_ = (expr);                                \
         if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #expr); \
+    } while (0)
+#define HYB_CHECK_C(c, expr)                                    \
+    do {                                                        \
+        cudaError_t e_ = (expr);                                \
+        if (e_ != cudaSuccess) return cuda_fail((c), e_, #expr); \
     } while (0)
 
 bool is_device_ptr(const void* p) {
@@ -424,6 +437,173 @@ int hybrid_host_pipelined(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows
     return HYB_OK;
 }
 
+// Device holding p (-1: host memory, pinned or pageable).
+int ptr_device(const void* p) {
+    cudaPointerAttributes a;
+    if (!p || cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+    }
+    return (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) ? a.device : -1;
+}
+
+// Multi-device hybrid (hyb_create_multi): one strip per device in one process -- the paper's
+// parts = workers partition (reference proj/src/parallel.cpp:27-70, split_bands geometry
+// proj/src/tiling.cpp:23-32) with one GPU per band.  Per strip i on its device (own stream, all strips
+// concurrent):
+//   1. its rows of g plus a halo of rA + rW rows, straight from the caller's buffer (H2D from host
+//      memory, a peer copy over NVLink from another device, or a local copy);
+//   2. the AMF on its core rows +- rW (so the W1 statistics of its core rows need no second exchange),
+//      then the statistics of its core rows into its partial W;
+//   3. after every strip's statistics (cross-device events), the exact total W by one reduction kernel
+//      per device reading the other devices' partials over NVLink (peer access) -- every device gets the
+//      identical int64 W, so the output is bit-identical to one GPU;
+//   4. the gain of its core rows, written straight into y when y is device memory this device can
+//      store to (its own, or a peer's over NVLink), else staged and copied out.
+// The caller's stream (ctx->stream, strip 0) orders the call: every strip starts after the work already
+// on it, and it waits for every strip's end.
+int hybrid_multi(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int cols, int smax, int win, int parts,
+                 uint8_t* y, size_t ypitch, hyb_stats* stats) {
+    int st;
+    if ((st = check_smax(ctx, smax)) || (st = check_win(ctx, win)) || (st = check_dims(ctx, rows, cols)) ||
+        (st = check_pitch(ctx, pitch, cols, "g")) || (st = check_pitch(ctx, ypitch, cols, "y")))
+        return st;
+    if (parts < 1) return fail(ctx, HYB_EINVAL, "parts must be >= 1, got " + std::to_string(parts));
+    const int n = 1 + (int)ctx->peers.size();
+    if (std::max(parts, n) > rows)
+        return fail(ctx, HYB_EINVAL, "parts " + std::to_string(std::max(parts, n)) + " exceeds image rows " +
+                                         std::to_string(rows));
+    if (!g || !y) return fail(ctx, HYB_EINVAL, "null image pointer");
+    std::vector<hyb_ctx*> sub(n);
+    sub[0] = ctx;
+    for (int i = 1; i < n; ++i) sub[i] = ctx->peers[i - 1];
+    const int rA = (smax - 1) / 2, rW = (win - 1) / 2, h = rA + rW;
+    const int ydev = ptr_device(y);
+    const bool timed = stats != nullptr;
+    struct S { int start, core, hA, hB, fa, fb; };
+    std::vector<S> s(n);
+    {
+        const int base = rows / n, extra = rows % n;
+        int start = 0;
+        for (int i = 0; i < n; ++i) {
+            S& t = s[i];
+            t.start = start;
+            t.core = base + (i < extra ? 1 : 0);
+            t.hA = std::min(h, start);
+            t.hB = std::min(h, rows - start - t.core);
+            t.fa = std::min(rW, start);
+            t.fb = std::min(rW, rows - start - t.core);
+            start += t.core;
+        }
+    }
+    const size_t sp = round_pitch(cols);
+    const long long P = (long long)rows * cols;
+    HYB_CHECK(cudaSetDevice(ctx->device));
+    if (timed) HYB_CHECK(cudaEventRecord(ctx->ev[3], ctx->stream));
+    HYB_CHECK(cudaEventRecord(ctx->ev_start, ctx->stream));
+    // 1-2: halo rows + AMF + statistics per strip
+    for (int i = 0; i < n; ++i) {
+        hyb_ctx* c = sub[i];
+        const S& t = s[i];
+        CtxScope scope(c);
+        if (cudaSetDevice(c->device) != cudaSuccess) return cuda_fail(ctx, cudaGetLastError(), "cudaSetDevice");
+        auto chk = [&](cudaError_t e, const char* what) { return e == cudaSuccess ? HYB_OK : cuda_fail(ctx, e, what); };
+        if (i && (st = chk(cudaStreamWaitEvent(c->stream, ctx->ev_start, 0), "wait start"))) return st;
+        if (c->strip_g.empty()) c->strip_g.resize(1);
+        if (c->strip_f.empty()) c->strip_f.resize(1);
+        const int grows = t.hA + t.core + t.hB, frows = t.fa + t.core + t.fb;
+        if ((st = chk(c->strip_g[0].ensure(sp * grows), "strip alloc")) ||
+            (st = chk(c->strip_f[0].ensure(sp * frows), "strip alloc")) ||
+            (st = chk(c->wsum.ensure(sizeof(long long)), "alloc")) ||
+            (st = chk(c->wtot.ensure(sizeof(long long)), "alloc")) ||
+            (st = chk(c->wparts.ensure(sizeof(long long) * n), "alloc")))
+            return st;
+        if ((st = chk(copy2d(c, c->strip_g[0].ptr, sp, g + (size_t)(t.start - t.hA) * pitch, pitch, cols, grows),
+                      "strip halo copy")))
+            return st;
+        if ((st = chk(cudaMemsetAsync(c->wsum.ptr, 0, sizeof(long long), c->stream), "memset")))
+            return st;
+        hyb::Plane a{c->strip_g[0].ptr, sp, 0, c->strip_f[0].ptr, sp, 0, grows, cols, t.hA - t.fa,
+                     t.hA + t.core + t.fb, 1};
+        if ((st = chk(run_amf(c, a, smax, nullptr, 0, 0), "strip AMF"))) return st;
+        hyb::Plane w{c->strip_f[0].ptr, sp, 0, nullptr, 0, 0, frows, cols, t.fa, t.fa + t.core, 1};
+        if ((st = chk(hyb::launch_wiener_stats(w, win, reinterpret_cast<unsigned long long*>(c->wsum.ptr), c->stream),
+                      "strip statistics")))
+            return st;
+        if ((st = chk(cudaEventRecord(c->ev_stats, c->stream), "event"))) return st;
+    }
+    if (timed) {
+        HYB_CHECK(cudaSetDevice(ctx->device));
+        HYB_CHECK(cudaEventRecord(ctx->ev[1], ctx->stream));
+    }
+    // 3-4: exact total W on every device, then the gain of its core rows
+    for (int i = 0; i < n; ++i) {
+        hyb_ctx* c = sub[i];
+        const S& t = s[i];
+        CtxScope scope(c);
+        if (cudaSetDevice(c->device) != cudaSuccess) return cuda_fail(ctx, cudaGetLastError(), "cudaSetDevice");
+        auto chk = [&](cudaError_t e, const char* what) { return e == cudaSuccess ? HYB_OK : cuda_fail(ctx, e, what); };
+        hyb::Partials parts_w{};
+        parts_w.n = n;
+        for (int j = 0; j < n; ++j) {
+            if (j != i && (st = chk(cudaStreamWaitEvent(c->stream, sub[j]->ev_stats, 0), "wait statistics")))
+                return st;
+            if (ctx->peer_ok[(size_t)i * n + j]) {
+                parts_w.p[j] = reinterpret_cast<const long long*>(sub[j]->wsum.ptr);
+            } else {
+                long long* dst = reinterpret_cast<long long*>(c->wparts.ptr) + j;
+                if ((st = chk(cudaMemcpyPeerAsync(dst, c->device, sub[j]->wsum.ptr, sub[j]->device, sizeof(long long),
+                                                  c->stream),
+                              "partial W copy")))
+                    return st;
+                parts_w.p[j] = dst;
+            }
+        }
+        long long* Wt = reinterpret_cast<long long*>(c->wtot.ptr);
+        if ((st = chk(hyb::launch_sum_partials(parts_w, Wt, c->stream), "W reduction"))) return st;
+        // output rows: straight into y when this device can store there (y on this device, or on a strip's
+        // device with peer access enabled), else staged + copied out
+        bool direct = ydev >= 0 && ydev == c->device;
+        for (int j = 0; j < n && ydev >= 0 && !direct; ++j)
+            direct = sub[j]->device == ydev && ctx->peer_ok[(size_t)i * n + j];
+        uint8_t* yd = y + (size_t)t.start * ypitch;
+        size_t yp = ypitch;
+        if (!direct) {
+            if ((st = chk(c->out.ensure(sp * t.core), "alloc"))) return st;
+            yd = c->out.ptr;
+            yp = sp;
+        }
+        hyb::Plane w{c->strip_f[0].ptr, sp, 0, yd, yp, 0, t.fa + t.core + t.fb, cols, t.fa, t.fa + t.core, 1};
+        if ((st = chk(hyb::launch_wiener_gain(w, win, Wt, P, c->stream), "strip gain"))) return st;
+        if (!direct &&
+            (st = chk(copy2d(c, y + (size_t)t.start * ypitch, ypitch, yd, yp, cols, t.core), "strip output copy")))
+            return st;
+        if ((st = chk(cudaEventRecord(c->ev_done, c->stream), "event"))) return st;
+    }
+    HYB_CHECK(cudaSetDevice(ctx->device));
+    for (int i = 1; i < n; ++i) HYB_CHECK(cudaStreamWaitEvent(ctx->stream, sub[i]->ev_done, 0));
+    if (timed) {
+        HYB_CHECK(cudaEventRecord(ctx->ev[2], ctx->stream));
+        if ((st = ensure_host_w(ctx, 1))) return st;
+        HYB_CHECK(cudaMemcpyAsync(ctx->host_w, ctx->wtot.ptr, sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    if (timed || ydev < 0 || ptr_device(g) < 0) HYB_CHECK(cudaStreamSynchronize(ctx->stream));
+    if (timed) {
+        float a = 0, w = 0, t = 0;
+        HYB_CHECK(cudaEventElapsedTime(&a, ctx->ev[3], ctx->ev[1]));
+        HYB_CHECK(cudaEventElapsedTime(&w, ctx->ev[1], ctx->ev[2]));
+        HYB_CHECK(cudaEventElapsedTime(&t, ctx->ev[3], ctx->ev[2]));
+        const double nn = (double)win * win;
+        stats->noise_sum = ctx->host_w[0];
+        stats->pixel_count = P;
+        stats->sigma2 = (double)stats->noise_sum / (nn * nn * (double)P) / (255.0 * 255.0);
+        stats->t_adaptive = a * 1e-3;  // strip 0's stream: halo copies, AMF and statistics enqueued for every strip
+        stats->t_wiener = w * 1e-3;
+        stats->t_total = t * 1e-3;
+    }
+    return HYB_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -448,6 +628,9 @@ hyb_ctx* hyb_create(int device, int* status) {
     }
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->copy2, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_stats, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_done, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_start, cudaEventDisableTiming);
     for (int i = 0; i < hyb_ctx::kMaxChunks && e == cudaSuccess; ++i) {
         e = cudaEventCreateWithFlags(&ctx->ev_h2d[i], cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_gain[i], cudaEventDisableTiming);
@@ -464,6 +647,8 @@ hyb_ctx* hyb_create(int device, int* status) {
 
 int hyb_destroy(hyb_ctx* ctx) {
     if (!ctx) return HYB_OK;
+    for (hyb_ctx* p : ctx->peers) hyb_destroy(p);
+    ctx->peers.clear();
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     ctx->in.release();
@@ -483,7 +668,13 @@ int hyb_destroy(hyb_ctx* ctx) {
     ctx->amf_cnt.release();
     for (auto& b : ctx->strip_g) b.release();
     for (auto& b : ctx->strip_f) b.release();
+    ctx->wparts.release();
+    ctx->wtot.release();
+    ctx->mg_in.release();
+    ctx->mg_out.release();
     if (ctx->host_w) cudaFreeHost(ctx->host_w);
+    for (cudaEvent_t ev : {ctx->ev_stats, ctx->ev_done, ctx->ev_start})
+        if (ev) cudaEventDestroy(ev);
     for (auto& ev : ctx->ev)
         if (ev) cudaEventDestroy(ev);
     for (auto& kv : ctx->graphs)
@@ -515,7 +706,55 @@ int hyb_set_exclusive(hyb_ctx* ctx, int exclusive) {
 
 const char* hyb_last_error(const hyb_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
-int64_t hyb_kernel_launches(const hyb_ctx* ctx) { return ctx ? ctx->launches : 0; }
+int64_t hyb_kernel_launches(const hyb_ctx* ctx) {
+    if (!ctx) return 0;
+    long long n = ctx->launches;
+    for (const hyb_ctx* p : ctx->peers) n += p->launches;
+    return n;
+}
+
+hyb_ctx* hyb_create_multi(int n_devices, const int* device_ids, int* status) {
+    if (n_devices < 1 || n_devices > hyb::kMaxDevices || !device_ids) {
+        if (status) *status = HYB_EINVAL;
+        return nullptr;
+    }
+    hyb_ctx* ctx = hyb_create(device_ids[0], status);
+    if (!ctx) return nullptr;
+    for (int i = 1; i < n_devices; ++i) {
+        hyb_ctx* p = hyb_create(device_ids[i], status);
+        if (!p) {
+            hyb_destroy(ctx);
+            return nullptr;
+        }
+        ctx->peers.push_back(p);
+    }
+    // all-pairs peer access (NVLink on B200 boxes); pairs without it exchange through copies
+    ctx->peer_ok.assign((size_t)n_devices * n_devices, 0);
+    for (int i = 0; i < n_devices; ++i)
+        for (int j = 0; j < n_devices; ++j) {
+            const int di = device_ids[i], dj = device_ids[j];
+            int can = di == dj;
+            if (!can && cudaDeviceCanAccessPeer(&can, di, dj) == cudaSuccess && can) {
+                cudaSetDevice(di);
+                const cudaError_t e = cudaDeviceEnablePeerAccess(dj, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) can = 0;
+                cudaGetLastError();
+            }
+            ctx->peer_ok[(size_t)i * n_devices + j] = (char)(can != 0);
+        }
+    cudaSetDevice(device_ids[0]);
+    if (status) *status = HYB_OK;
+    return ctx;
+}
+
+int hyb_context_devices(const hyb_ctx* ctx, int* device_ids) {
+    if (!ctx) return 0;
+    if (device_ids) {
+        device_ids[0] = ctx->device;
+        for (size_t i = 0; i < ctx->peers.size(); ++i) device_ids[i + 1] = ctx->peers[i]->device;
+    }
+    return 1 + (int)ctx->peers.size();
+}
 
 int hyb_validate_smax(int smax) { return (smax <= 1 || smax % 2 == 0) ? HYB_EINVAL : HYB_OK; }
 
@@ -733,6 +972,7 @@ int hyb_hybrid_u8(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int co
                   int win, int parts, uint8_t* y, size_t y_pitch, hyb_stats* stats) {
     if (!ctx) return HYB_EINVAL;
     CtxScope scope_(ctx);
+    if (!ctx->peers.empty()) return hybrid_multi(ctx, g, pitch, rows, cols, smax, win, parts, y, y_pitch, stats);
     // Untimed calls on device buffers or pinned host buffers replay a cached CUDA graph.
     cudaPointerAttributes ga{}, ya{};
     const bool gok = g && cudaPointerGetAttributes(&ga, g) == cudaSuccess;
@@ -1141,23 +1381,10 @@ bool batch_host_pipelined(hyb_ctx* ctx, const uint8_t* g, size_t pitch, size_t s
     return true;
 }
 
-}  // namespace
-
-extern "C" {
-
-int hyb_hybrid_batch_u8(hyb_ctx* ctx, const uint8_t* g, size_t pitch, size_t slice_stride,
-                        int n_slices, int rows, int cols, int smax, int win, uint8_t* y,
-                        size_t y_pitch, size_t y_slice_stride, int64_t* noise_sums) {
-    if (!ctx) return HYB_EINVAL;
-    CtxScope scope_(ctx);
+// Core of hyb_hybrid_batch_u8 on one device (arguments validated).
+int batch_single(hyb_ctx* ctx, const uint8_t* g, size_t pitch, size_t slice_stride, int n_slices, int rows, int cols,
+                 int smax, int win, uint8_t* y, size_t y_pitch, size_t y_slice_stride, int64_t* noise_sums) {
     int st;
-    if ((st = check_smax(ctx, smax)) || (st = check_win(ctx, win)) || (st = check_dims(ctx, rows, cols)) ||
-        (st = check_pitch(ctx, pitch, cols, "g")) || (st = check_pitch(ctx, y_pitch, cols, "y")))
-        return st;
-    if (n_slices < 1) return fail(ctx, HYB_EINVAL, "n_slices must be >= 1, got " + std::to_string(n_slices));
-    if (!g || !y) return fail(ctx, HYB_EINVAL, "null image pointer");
-    if (slice_stride < pitch * rows || y_slice_stride < y_pitch * rows)
-        return fail(ctx, HYB_EINVAL, "slice stride smaller than one slice");
     HYB_CHECK(cudaSetDevice(ctx->device));
     const bool dg = is_device_ptr(g) && hyb::tma_compatible(g, pitch, slice_stride), dy = is_device_ptr(y);
     const size_t pp = round_pitch(cols), ps = pp * rows;
@@ -1230,6 +1457,101 @@ int hyb_hybrid_batch_u8(hyb_ctx* ctx, const uint8_t* g, size_t pitch, size_t sli
     if (noise_sums)
         for (int z = 0; z < n_slices; ++z) noise_sums[z] = ctx->host_w[z];
     return HYB_OK;
+}
+
+// Multi-device CT stack (hyb_create_multi): slices sharded by contiguous chunks, one chunk per device,
+// each an independent batch on its own device (no cross-slice reduction: every slice has its own noise
+// sum).  One host thread per device enqueues (and, for host buffers, pipelines) its
+// chunk; chunks whose input / output live on another device move through NVLink peer copies.
+int batch_multi(hyb_ctx* ctx, const uint8_t* g, size_t pitch, size_t slice_stride, int n_slices, int rows, int cols,
+                int smax, int win, uint8_t* y, size_t y_pitch, size_t y_slice_stride, int64_t* noise_sums) {
+    const int n = 1 + (int)ctx->peers.size();
+    std::vector<hyb_ctx*> sub(n);
+    sub[0] = ctx;
+    for (int i = 1; i < n; ++i) sub[i] = ctx->peers[i - 1];
+    const int gdev = ptr_device(g), ydev = ptr_device(y);
+    HYB_CHECK(cudaSetDevice(ctx->device));
+    HYB_CHECK(cudaEventRecord(ctx->ev_start, ctx->stream));
+    std::vector<int64_t> ws(noise_sums ? n_slices : 0);
+    std::vector<int> status(n, HYB_OK);
+    std::vector<std::string> errs(n);
+    const size_t pp = round_pitch(cols), ps = pp * rows;
+    auto work = [&](int i) {
+        hyb_ctx* c = sub[i];
+        const int z0 = (int)((long long)n_slices * i / n), z1 = (int)((long long)n_slices * (i + 1) / n), nz = z1 - z0;
+        CtxScope scope(c);
+        auto run = [&]() -> int {
+            if (cudaSetDevice(c->device) != cudaSuccess) return cuda_fail(c, cudaGetLastError(), "cudaSetDevice");
+            if (i) HYB_CHECK_C(c, cudaStreamWaitEvent(c->stream, ctx->ev_start, 0));
+            if (nz > 0) {
+                const uint8_t* gi = g + slice_stride * z0;
+                size_t gp = pitch, gs = slice_stride;
+                uint8_t* yi = y + y_slice_stride * z0;
+                size_t yp = y_pitch, ys = y_slice_stride;
+                const bool remote_g = gdev >= 0 && gdev != c->device, remote_y = ydev >= 0 && ydev != c->device;
+                if (remote_g) {  // peer copy of the chunk into this device
+                    HYB_CHECK_C(c, c->mg_in.ensure(ps * nz));
+                    for (int z = 0; z < nz; ++z)
+                        HYB_CHECK_C(c, copy2d(c, c->mg_in.ptr + ps * z, pp, gi + slice_stride * z, pitch, cols, rows));
+                    gi = c->mg_in.ptr;
+                    gp = pp;
+                    gs = ps;
+                }
+                if (remote_y) {
+                    HYB_CHECK_C(c, c->mg_out.ensure(ps * nz));
+                    yi = c->mg_out.ptr;
+                    yp = pp;
+                    ys = ps;
+                }
+                int st = batch_single(c, gi, gp, gs, nz, rows, cols, smax, win, yi, yp, ys,
+                                      noise_sums ? ws.data() + z0 : nullptr);
+                if (st) return st;
+                if (remote_y)
+                    for (int z = 0; z < nz; ++z)
+                        HYB_CHECK_C(c, copy2d(c, y + y_slice_stride * (z0 + z), y_pitch, yi + ys * z, yp, cols, rows));
+            }
+            HYB_CHECK_C(c, cudaEventRecord(c->ev_done, c->stream));
+            return HYB_OK;
+        };
+        status[i] = run();
+        if (status[i]) errs[i] = c->err;
+    };
+    std::vector<std::thread> pool;
+    for (int i = 1; i < n; ++i) pool.emplace_back(work, i);
+    work(0);
+    for (auto& t : pool) t.join();
+    for (int i = 0; i < n; ++i)  // the first error, like the reference's band pool (proj/src/parallel.cpp:67)
+        if (status[i]) return fail(ctx, status[i], errs[i]);
+    HYB_CHECK(cudaSetDevice(ctx->device));
+    for (int i = 1; i < n; ++i) HYB_CHECK(cudaStreamWaitEvent(ctx->stream, sub[i]->ev_done, 0));
+    if (gdev < 0 || ydev < 0 || noise_sums) HYB_CHECK(cudaStreamSynchronize(ctx->stream));
+    if (noise_sums)
+        for (int z = 0; z < n_slices; ++z) noise_sums[z] = ws[z];
+    return HYB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int hyb_hybrid_batch_u8(hyb_ctx* ctx, const uint8_t* g, size_t pitch, size_t slice_stride,
+                        int n_slices, int rows, int cols, int smax, int win, uint8_t* y,
+                        size_t y_pitch, size_t y_slice_stride, int64_t* noise_sums) {
+    if (!ctx) return HYB_EINVAL;
+    CtxScope scope_(ctx);
+    int st;
+    if ((st = check_smax(ctx, smax)) || (st = check_win(ctx, win)) || (st = check_dims(ctx, rows, cols)) ||
+        (st = check_pitch(ctx, pitch, cols, "g")) || (st = check_pitch(ctx, y_pitch, cols, "y")))
+        return st;
+    if (n_slices < 1) return fail(ctx, HYB_EINVAL, "n_slices must be >= 1, got " + std::to_string(n_slices));
+    if (!g || !y) return fail(ctx, HYB_EINVAL, "null image pointer");
+    if (slice_stride < pitch * rows || y_slice_stride < y_pitch * rows)
+        return fail(ctx, HYB_EINVAL, "slice stride smaller than one slice");
+    if (!ctx->peers.empty())
+        return batch_multi(ctx, g, pitch, slice_stride, n_slices, rows, cols, smax, win, y, y_pitch, y_slice_stride,
+                           noise_sums);
+    return batch_single(ctx, g, pitch, slice_stride, n_slices, rows, cols, smax, win, y, y_pitch, y_slice_stride,
+                        noise_sums);
 }
 
 }  // extern "C"

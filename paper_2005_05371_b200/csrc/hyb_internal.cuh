@@ -175,6 +175,14 @@ cudaError_t launch_contrast_stretch_f64(const double* in, size_t ipitch, int row
 cudaError_t launch_noise_reference(const double* a, size_t ap, const double* b, size_t bp, int rows, int cols,
                                    double* d_acc, cudaStream_t stream);
 
+// Multi-device noise reduction (multi.cu): *out = sum of the n int64 partials, each in this device's
+// memory or in a peer device's memory readable over NVLink (peer access enabled).
+struct Partials {
+    const long long* p[kMaxDevices];
+    int n;
+};
+cudaError_t launch_sum_partials(const Partials& parts, long long* out, cudaStream_t stream);
+
 // Kernel-launch counter (bench evidence), incremented by every launcher.
 void count_launch();
 

@@ -74,14 +74,46 @@ def validate_smax(smax: int) -> None:
         raise InvalidArgument(f"smax must be an odd integer > 1, got {smax}")
 
 
+class EstimateMode:
+    """EstimateMode -- reference proj/include/denoise/wiener.hpp:8.  For the W1 Wiener: ROBUST = the
+    north_star's estimator (mean of the local variances, exact int64 W); REFERENCE = the mean squared
+    difference between the AMF output and a reference image (proj/src/wiener.cpp:31-42)."""
+    ROBUST = "robust"
+    REFERENCE = "reference"
+
+
 @dataclass
 class FilterConfig:
-    """FilterConfig -- reference proj/include/denoise/parallel.hpp:13-19, plus the W1 window."""
+    """FilterConfig -- reference proj/include/denoise/parallel.hpp:13-19 (same fields and defaults),
+    plus the W1 window and where it runs: `gpus` > 1 strips on devices 0..gpus-1 or an explicit
+    `device_ids` list (a multi-device context: one strip per device, bit-identical to one GPU), and
+    `final_stretch`, the reference pipeline's closing contrast_stretch (proj/src/pipeline.cpp:55-57)."""
     smax: int = 11
     parts: int = 1
     workers: int = 1
+    estimate_mode: str = EstimateMode.ROBUST
     use_halo: bool = True
     wiener_window: int = 3
+    gpus: int = 1
+    device_ids: tuple = ()
+    final_stretch: bool = False
+
+
+_multi: dict = {}
+
+
+def _config_ctx(ctx, config, *arrays):
+    """The context for a config: the caller's, else a (cached) multi-device context when the config asks
+    for several devices, else the inputs' device's default context."""
+    if ctx is None:
+        ids = tuple(config.device_ids) if config.device_ids else tuple(range(config.gpus))
+        if config.gpus < 1:
+            raise InvalidArgument(f"gpus must be >= 1, got {config.gpus}")
+        if len(ids) > 1:
+            ctx = _multi.get(ids)
+            if ctx is None:
+                ctx = _multi[ids] = capi.Context(devices=list(ids))
+    return _ctx(ctx, *arrays)
 
 
 def validate_config(config: FilterConfig) -> None:
@@ -196,19 +228,67 @@ class HybridResult:
     t_total: float
 
 
-def hybrid_denoise(noisy, config: FilterConfig, ctx=None) -> HybridResult:
-    """hybrid_denoise stages 1-2 -- reference proj/src/pipeline.cpp:23-53 with the north_star's
-    W1 Wiener in the stage-2 slot; config.parts strips (bit-identical for every parts)."""
+def hybrid_denoise(noisy, config: FilterConfig, reference=None, stretch_after_each: bool = False,
+                   ctx=None) -> HybridResult:
+    """hybrid_denoise -- reference proj/include/denoise/pipeline.hpp:25-27 (proj/src/pipeline.cpp:23-57)
+    with the north_star's W1 Wiener in the stage-2 slot: the AMF (config.parts strips, bit-identical for
+    every parts; config.gpus / device_ids devices), [contrast stretch when stretch_after_each], W1 with the
+    noise of config.estimate_mode (REFERENCE needs `reference`, a float64 image in [0, 1] or a uint8
+    image), [final contrast stretch when config.final_stretch]."""
     validate_config(config)
     rows, cols = _shape(noisy)
+    if config.estimate_mode == EstimateMode.REFERENCE and reference is None:
+        raise InvalidArgument("reference mode requires a reference image")
+    if reference is not None and _shape(reference) != (rows, cols):
+        raise InvalidArgument("reference image dimensions do not match")
     y = _empty_like(noisy, rows, cols)
     gp, gpitch = capi.buf(noisy)
     yp, ypitch = capi.buf(y)
-    st = capi.HybStats()
-    c = _ctx(ctx, noisy, y)
-    check(lib.hyb_hybrid_u8(c, gp, gpitch, rows, cols, config.smax, config.wiener_window, config.parts,
-                            yp, ypitch, ctypes.byref(st)), c)
-    return HybridResult(y, st.sigma2, st.t_adaptive, st.t_wiener, 0.0, st.noise_sum, st.t_total)
+    c = _config_ctx(ctx, config, noisy, y)
+    if config.estimate_mode != EstimateMode.REFERENCE and not stretch_after_each:
+        st = capi.HybStats()
+        check(lib.hyb_hybrid_u8(c, gp, gpitch, rows, cols, config.smax, config.wiener_window, config.parts,
+                                yp, ypitch, ctypes.byref(st)), c)
+        res = HybridResult(y, st.sigma2, st.t_adaptive, st.t_wiener, 0.0, st.noise_sum, st.t_total)
+    else:
+        import time
+        t0 = time.perf_counter()
+        f = _empty_like(noisy, rows, cols)
+        fp, fpitch = capi.buf(f)
+        check(lib.hyb_amf_u8(c, gp, gpitch, rows, cols, 0, rows, config.smax, fp, fpitch, None, cols), c)
+        t1 = time.perf_counter()
+        t_stretch = 0.0
+        if stretch_after_each:  # proj/src/pipeline.cpp:39-43 (uint8 stretch, rounded half up)
+            check(lib.hyb_contrast_stretch_u8(c, fp, fpitch, rows, cols, fp, fpitch), c)
+            t_stretch += time.perf_counter() - t1
+        t2 = time.perf_counter()
+        win = config.wiener_window
+        n = win * win
+        if config.estimate_mode == EstimateMode.REFERENCE:
+            # sigma2 = mean((f - reference)^2) in [0, 1] units (proj/src/wiener.cpp:31-42), fed to the W1 gain as
+            # W / (n^2 P) with P scaled by 64 (the rounding of W costs < 2^-6 / (n^2 P))
+            fa = (f.cpu().numpy() if _is_torch(f) else f).astype(np.float64) / 255.0
+            rn = reference.cpu().numpy() if _is_torch(reference) else np.asarray(reference)
+            ra = rn.astype(np.float64) / 255.0 if rn.dtype == np.uint8 else rn.astype(np.float64)
+            sigma2 = float(np.mean((fa - ra) ** 2))
+            pn = rows * cols * 64
+            w = int(np.floor(sigma2 * 255.0 * 255.0 * n * n * pn + 0.5))  # llround, as the C++ host
+            wsum = 0
+        else:
+            wv = ctypes.c_int64(0)
+            check(lib.hyb_wiener_stats_u8(c, fp, fpitch, rows, cols, 0, rows, win, ctypes.byref(wv)), c)
+            w, pn = wv.value, rows * cols
+            sigma2 = noise_variance(w, pn, win)
+            wsum = w
+        wv = ctypes.c_int64(w)
+        check(lib.hyb_wiener_gain_u8(c, fp, fpitch, rows, cols, 0, rows, win, ctypes.byref(wv), pn, yp, ypitch), c)
+        res = HybridResult(y, sigma2, t1 - t0, time.perf_counter() - t2, t_stretch, wsum, time.perf_counter() - t0)
+    if config.final_stretch:  # proj/src/pipeline.cpp:55-57
+        import time
+        t3 = time.perf_counter()
+        check(lib.hyb_contrast_stretch_u8(c, yp, ypitch, rows, cols, yp, ypitch), c)
+        res.t_stretch += time.perf_counter() - t3
+    return res
 
 
 def contrast_stretch(image, ctx=None):

@@ -13,23 +13,47 @@
 namespace denoise_cuda {
 namespace {
 
-// One hyb_ctx per (host thread, device), like the reference's per-call pool (proj/src/parallel.cpp:62-65).
+// One hyb_ctx per (host thread, device list), like the reference's per-call pool (proj/src/parallel.cpp:62-65):
+// a single device, or a multi-device context (hyb_create_multi) for a strip partition over several GPUs.
 struct Contexts {
-    std::map<int, hyb_ctx*> by_device;
+    std::map<std::vector<int>, hyb_ctx*> by_devices;
+    int default_device = 0;
     ~Contexts() {
-        for (auto& kv : by_device) hyb_destroy(kv.second);
+        for (auto& kv : by_devices) hyb_destroy(kv.second);
     }
 };
 
-hyb_ctx* context(int device) {
+Contexts& contexts() {
     thread_local Contexts ctxs;
-    auto it = ctxs.by_device.find(device);
-    if (it != ctxs.by_device.end()) return it->second;
+    return ctxs;
+}
+
+hyb_ctx* context_for(const std::vector<int>& devices) {
+    Contexts& ctxs = contexts();
+    auto it = ctxs.by_devices.find(devices);
+    if (it != ctxs.by_devices.end()) return it->second;
     int st = 0;
-    hyb_ctx* c = hyb_create(device, &st);
-    if (!c) throw std::runtime_error("libhybrid_cuda: no CUDA device " + std::to_string(device));
-    ctxs.by_device[device] = c;
+    hyb_ctx* c = devices.size() == 1 ? hyb_create(devices[0], &st)
+                                     : hyb_create_multi((int)devices.size(), devices.data(), &st);
+    if (!c) {
+        std::string ids;
+        for (int d : devices) ids += (ids.empty() ? "" : ",") + std::to_string(d);
+        throw std::runtime_error("libhybrid_cuda: cannot open CUDA device(s) " + ids);
+    }
+    ctxs.by_devices[devices] = c;
     return c;
+}
+
+hyb_ctx* context(int device) { return context_for({device}); }
+hyb_ctx* context() { return context(contexts().default_device); }
+
+// The devices a FilterConfig asks for: device_ids, else gpus consecutive devices from `device`.
+std::vector<int> config_devices(const FilterConfig& config) {
+    if (!config.device_ids.empty()) return config.device_ids;
+    if (config.gpus < 1) throw std::invalid_argument("gpus must be >= 1, got " + std::to_string(config.gpus));
+    std::vector<int> ids;
+    for (int i = 0; i < config.gpus; ++i) ids.push_back(config.device + i);
+    return ids;
 }
 
 void check(int status, hyb_ctx* ctx) {
@@ -93,6 +117,9 @@ Image Image::from_pixels(int rows, int cols, std::vector<double> px) {
     return img;
 }
 
+void set_default_device(int device) { contexts().default_device = device; }
+int default_device() { return contexts().default_device; }
+
 void validate_smax(int smax) {
     if (hyb_validate_smax(smax) != HYB_OK)
         throw std::invalid_argument("smax must be an odd integer > 1, got " + std::to_string(smax));
@@ -130,7 +157,7 @@ void adaptive_median_rows(const Image& src, int smax, int row_begin, int row_end
     const int out_rows = row_end - row_begin;
     std::vector<uint8_t> out((std::size_t)out_rows * cols), fin;
     if (finalized_at) fin.resize(out.size());
-    hyb_ctx* ctx = context(0);
+    hyb_ctx* ctx = context();
     check(hyb_amf_u8(ctx, in.px.data(), cols, rows, cols, row_begin, row_end, smax, out.data(), cols,
                      finalized_at ? fin.data() : nullptr, cols),
           ctx);
@@ -154,29 +181,38 @@ Image adaptive_median_parallel(const Image& image, const FilterConfig& config) {
     if (config.parts > rows)
         throw std::invalid_argument("parts " + std::to_string(config.parts) + " exceeds image rows " +
                                     std::to_string(rows));
-    // band geometry of split_bands (proj/src/tiling.cpp:23-32); each band filtered from its own copy
-    const int halo = config.use_halo ? (config.smax - 1) / 2 : 0;
-    Image out(rows, cols);
-    const int base = rows / config.parts, extra = rows % config.parts;
-    int start = 0;
-    for (int i = 0; i < config.parts; ++i) {
-        const int core = base + (i < extra ? 1 : 0);
-        const int ha = std::min(halo, start), hb = std::min(halo, rows - start - core);
-        Image band(ha + core + hb, cols);
-        std::copy(image.row(start - ha), image.row(start - ha) + band.size(), band.pixels().begin());
-        Image res;
-        detail::adaptive_median_rows(band, config.smax, ha, ha + core, res);
-        std::copy(res.pixels().begin(), res.pixels().end(), out.row(start));
-        start += core;
+    const Coded in = encode_for_amf(image);
+    std::vector<uint8_t> out((std::size_t)rows * cols);
+    hyb_ctx* ctx = context(config.device);
+    if (config.use_halo) {
+        // With the halo every band's output equals the serial filter's rows (proj/include/denoise/
+        // parallel.hpp:27-28), so the GPU filters the whole image in one upload and one launch: the
+        // bands are the kernel's tiles, `workers` its CTAs.
+        check(hyb_amf_u8(ctx, in.px.data(), cols, rows, cols, 0, rows, config.smax, out.data(), cols, nullptr, cols),
+              ctx);
+    } else {
+        // the literal halo-free split (use_halo = false): each band filtered as its own image, which
+        // clamps its windows at the band edges (proj/src/parallel.cpp:34)
+        const int base = rows / config.parts, extra = rows % config.parts;
+        int start = 0;
+        for (int i = 0; i < config.parts; ++i) {
+            const int core = base + (i < extra ? 1 : 0);
+            check(hyb_amf_u8(ctx, in.px.data() + (std::size_t)start * cols, cols, core, cols, 0, core, config.smax,
+                             out.data() + (std::size_t)start * cols, cols, nullptr, cols),
+                  ctx);
+            start += core;
+        }
     }
-    return out;
+    Image res(rows, cols);
+    for (std::size_t i = 0; i < out.size(); ++i) res.pixels()[i] = in.decode(out[i]);
+    return res;
 }
 
 Image wiener_local(const Image& filtered, int window, double* sigma2) {
     const std::vector<uint8_t> f = to_u8(filtered);
     std::vector<uint8_t> y(f.size());
     int64_t w = 0;
-    hyb_ctx* ctx = context(0);
+    hyb_ctx* ctx = context();
     check(hyb_wiener_u8(ctx, f.data(), filtered.cols(), filtered.rows(), filtered.cols(), window, y.data(),
                         filtered.cols(), &w),
           ctx);
@@ -187,27 +223,77 @@ Image wiener_local(const Image& filtered, int window, double* sigma2) {
     return from_u8(y.data(), filtered.rows(), filtered.cols());
 }
 
-HybridResult hybrid_denoise(const Image& noisy, const FilterConfig& config) {
+HybridResult hybrid_denoise(const Image& noisy, const FilterConfig& config, const Image* reference,
+                            bool stretch_after_each) {
     validate_config(config);
+    if (config.estimate_mode == EstimateMode::reference && reference == nullptr)
+        throw std::invalid_argument("reference mode requires a reference image");
+    if (reference && !noisy.same_size(*reference))
+        throw std::invalid_argument("reference image dimensions do not match");
+    const int rows = noisy.rows(), cols = noisy.cols();
     const std::vector<uint8_t> g = to_u8(noisy);
     std::vector<uint8_t> y(g.size());
-    hyb_ctx* ctx = context(config.device);
-    hyb_stats st{};
-    check(hyb_hybrid_u8(ctx, g.data(), noisy.cols(), noisy.rows(), noisy.cols(), config.smax, config.wiener_window,
-                        config.parts, y.data(), noisy.cols(), &st),
-          ctx);
+    hyb_ctx* ctx = context_for(config_devices(config));
     HybridResult r;
-    r.image = from_u8(y.data(), noisy.rows(), noisy.cols());
-    r.sigma2 = st.sigma2;
-    r.t_adaptive = st.t_adaptive;
-    r.t_wiener = st.t_wiener;
-    r.noise_sum = st.noise_sum;
+    const long long P = (long long)rows * cols;
+    const int win = config.wiener_window;
+    if (config.estimate_mode == EstimateMode::robust && !stretch_after_each) {
+        // the hot path: AMF + W1 in one call (strips over every configured device)
+        hyb_stats st{};
+        check(hyb_hybrid_u8(ctx, g.data(), cols, rows, cols, config.smax, win, config.parts, y.data(), cols, &st),
+              ctx);
+        r.sigma2 = st.sigma2;
+        r.t_adaptive = st.t_adaptive;
+        r.t_wiener = st.t_wiener;
+        r.noise_sum = st.noise_sum;
+    } else {
+        using clock = std::chrono::steady_clock;
+        auto secs = [](clock::time_point a, clock::time_point b) { return std::chrono::duration<double>(b - a).count(); };
+        std::vector<uint8_t> f(g.size());
+        auto t0 = clock::now();
+        check(hyb_amf_u8(ctx, g.data(), cols, rows, cols, 0, rows, config.smax, f.data(), cols, nullptr, cols), ctx);
+        auto t1 = clock::now();
+        r.t_adaptive = secs(t0, t1);
+        if (stretch_after_each) {  // proj/src/pipeline.cpp:39-43 (uint8 stretch, rounded half up)
+            check(hyb_contrast_stretch_u8(ctx, f.data(), cols, rows, cols, f.data(), cols), ctx);
+            r.t_stretch += secs(t1, clock::now());
+        }
+        auto t2 = clock::now();
+        int64_t W = 0;
+        long long Pn = P;
+        const double n = (double)win * win;
+        if (config.estimate_mode == EstimateMode::reference) {
+            // sigma2 = mean((f - reference)^2) in [0, 1] intensity units (proj/src/wiener.cpp:31-42); the W1 gain
+            // takes it as W / (n^2 P) with P scaled by K so the rounding of W costs < 2^-6 / (n^2 P)
+            double acc = 0.0;
+            for (std::size_t i = 0; i < f.size(); ++i) {
+                const double d = f[i] / 255.0 - reference->pixels()[i];
+                acc += d * d;
+            }
+            r.sigma2 = acc / (double)P;
+            constexpr long long K = 64;
+            Pn = P * K;
+            W = std::llround(r.sigma2 * 255.0 * 255.0 * n * n * (double)Pn);
+        } else {
+            check(hyb_wiener_stats_u8(ctx, f.data(), cols, rows, cols, 0, rows, win, &W), ctx);
+            r.sigma2 = (double)W / (n * n * (double)P) / (255.0 * 255.0);
+        }
+        check(hyb_wiener_gain_u8(ctx, f.data(), cols, rows, cols, 0, rows, win, &W, Pn, y.data(), cols), ctx);
+        r.t_wiener = secs(t2, clock::now());
+        r.noise_sum = config.estimate_mode == EstimateMode::reference ? 0 : W;
+    }
+    if (config.final_stretch) {  // proj/src/pipeline.cpp:55-57
+        const auto t = std::chrono::steady_clock::now();
+        check(hyb_contrast_stretch_u8(ctx, y.data(), cols, rows, cols, y.data(), cols), ctx);
+        r.t_stretch += std::chrono::duration<double>(std::chrono::steady_clock::now() - t).count();
+    }
+    r.image = from_u8(y.data(), rows, cols);
     return r;
 }
 
 Image contrast_stretch(const Image& image) {
     Image out(image.rows(), image.cols());
-    hyb_ctx* ctx = context(0);
+    hyb_ctx* ctx = context();
     check(hyb_contrast_stretch_f64(ctx, image.pixels().data(), image.cols(), image.rows(), image.cols(),
                                    out.pixels().data(), out.cols()),
           ctx);
@@ -215,7 +301,7 @@ Image contrast_stretch(const Image& image) {
 }
 
 NoiseEstimate estimate_noise_variance(const Image& image, const Image* reference) {
-    hyb_ctx* ctx = context(0);
+    hyb_ctx* ctx = context();
     NoiseEstimate est;
     if (reference) {
         if (reference->rows() != image.rows() || reference->cols() != image.cols())
@@ -234,7 +320,7 @@ NoiseEstimate estimate_noise_variance(const Image& image, const Image* reference
 
 Image wiener_filter(const Image& image, const NoiseEstimate& noise, bool clamp) {
     Image out(image.rows(), image.cols());
-    hyb_ctx* ctx = context(0);
+    hyb_ctx* ctx = context();
     check(hyb_wiener_freq_f64(ctx, image.pixels().data(), image.cols(), image.rows(), image.cols(), noise.sigma2,
                               clamp ? 1 : 0, out.pixels().data(), out.cols()),
           ctx);

@@ -48,15 +48,34 @@ private:
 /// validate_smax -- proj/src/adaptive_median.cpp:11-16.
 void validate_smax(int smax);
 
-/// FilterConfig -- proj/include/denoise/parallel.hpp:13-19 (+ the W1 window, + the device).
+/// EstimateMode -- proj/include/denoise/wiener.hpp:8.  For the W1 Wiener: robust = the north_star's
+/// estimator (nu = mean of the local variances, exact int64 W); reference = the mean squared difference
+/// between the AMF output and the reference image (proj/src/wiener.cpp:31-42).
+enum class EstimateMode { robust, reference };
+
+/// FilterConfig -- proj/include/denoise/parallel.hpp:13-19, same fields and defaults, plus the W1 window
+/// and where it runs: `device` (one GPU), or `gpus` > 1 strips on devices device .. device + gpus - 1,
+/// or an explicit `device_ids` list (ids may repeat) -- a multi-device context (hyb_create_multi), one
+/// strip per device, NVLink exchange of the noise sums, bit-identical to one GPU.  final_stretch: the
+/// reference pipeline's closing contrast_stretch (proj/src/pipeline.cpp:55-57) after the W1 stage.
 struct FilterConfig {
     int smax = 11;
     int parts = 1;
     int workers = 1;
+    EstimateMode estimate_mode = EstimateMode::robust;
     bool use_halo = true;
     int wiener_window = 3;
     int device = 0;
+    int gpus = 1;
+    std::vector<int> device_ids;
+    bool final_stretch = false;
 };
+
+/// Device used by the entry points that take no FilterConfig (reference signatures: adaptive_median_serial,
+/// detail::adaptive_median_rows, wiener_local, contrast_stretch, estimate_noise_variance, wiener_filter);
+/// per host thread, default 0.
+void set_default_device(int device);
+int default_device();
 
 /// validate_config -- proj/src/parallel.cpp:16-25.
 void validate_config(const FilterConfig& config);
@@ -86,8 +105,12 @@ struct HybridResult {
     long long noise_sum = 0;
 };
 
-/// hybrid_denoise stages 1-2 -- proj/src/pipeline.cpp:23-53 (AMF, then W1 in the Wiener slot).
-HybridResult hybrid_denoise(const Image& noisy, const FilterConfig& config);
+/// hybrid_denoise -- proj/include/denoise/pipeline.hpp:25-27, same signature: the adaptive median (parts
+/// bands, on config's device(s)), [contrast stretch when stretch_after_each], the W1 Wiener in the Wiener
+/// slot with the noise from config.estimate_mode (reference mode needs `reference`, same errors as
+/// proj/src/pipeline.cpp:25-31), [final contrast stretch when config.final_stretch].
+HybridResult hybrid_denoise(const Image& noisy, const FilterConfig& config, const Image* reference = nullptr,
+                            bool stretch_after_each = false);
 
 /// uint8 <-> reference doubles (k/255).  to_u8 throws std::invalid_argument off the grid.
 std::vector<uint8_t> to_u8(const Image& image);

@@ -16,6 +16,9 @@ extern "C" {
 int hyb_oracle_amf_u8(const uint8_t*, size_t, int, int, int, int, int, uint8_t*, size_t, uint8_t*, size_t);
 int hyb_oracle_hybrid_u8(const uint8_t*, size_t, int, int, int, int, uint8_t*, uint8_t*, size_t, int64_t*);
 int hyb_make_phantom_u8(int, int, int, double, double, uint64_t, uint8_t*, size_t);
+int hyb_oracle_wiener_stats_u8(const uint8_t*, size_t, int, int, int, int, int, int64_t*);
+int hyb_oracle_wiener_gain_u8(const uint8_t*, size_t, int, int, int, int, int, int64_t, int64_t, uint8_t*, size_t);
+int hyb_oracle_contrast_stretch_u8(const uint8_t*, size_t, int, int, uint8_t*, size_t);
 }
 
 using namespace denoise_cuda;
@@ -157,6 +160,74 @@ int main() {
             CHECK(r.image == from_u8(y.data(), rows, cols));
             CHECK(r.sigma2 > 0);
         }
+    }
+    // multi-GPU behind the reference API: FilterConfig.device_ids / gpus (strips on several devices, or
+    // several strips on one device where the box has one GPU) -- bit-identical to one device
+    {
+        const int rows = 517, cols = 389;
+        std::vector<uint8_t> g((size_t)rows * cols), y(g.size()), work(g.size());
+        hyb_make_phantom_u8(rows, cols, 10, 12.0, 0.3, 9, g.data(), cols);
+        int64_t w = 0;
+        hyb_oracle_hybrid_u8(g.data(), cols, rows, cols, 9, 5, work.data(), y.data(), cols, &w);
+        const Image noisy = from_u8(g.data(), rows, cols);
+        const Image expect = from_u8(y.data(), rows, cols);
+        for (const std::vector<int>& ids : {std::vector<int>{0, 0}, std::vector<int>{0, 0, 0, 0, 0, 0, 0, 0}}) {
+            FilterConfig cfg;
+            cfg.smax = 9;
+            cfg.wiener_window = 5;
+            cfg.parts = 4;
+            cfg.device_ids = ids;
+            const HybridResult r = hybrid_denoise(noisy, cfg);
+            CHECK(r.noise_sum == w);
+            CHECK(r.image == expect);
+        }
+        FilterConfig bad;
+        bad.gpus = 0;
+        CHECK_THROWS_AS(hybrid_denoise(noisy, bad), std::invalid_argument);
+    }
+    // estimate_mode / reference / stretch_after_each (proj/include/denoise/pipeline.hpp:25-27,
+    // proj/src/pipeline.cpp:25-53): the reference's call sites compile and behave
+    {
+        const int rows = 120, cols = 150;
+        std::vector<uint8_t> g((size_t)rows * cols), f(g.size()), y(g.size()), fs(g.size());
+        hyb_make_phantom_u8(rows, cols, 6, 10.0, 0.2, 4, g.data(), cols);
+        const Image noisy = from_u8(g.data(), rows, cols);
+        hyb_oracle_amf_u8(g.data(), cols, rows, cols, 0, rows, 7, f.data(), cols, nullptr, 0);
+        FilterConfig cfg;
+        cfg.smax = 7;
+        cfg.wiener_window = 3;
+        cfg.estimate_mode = EstimateMode::reference;
+        CHECK_THROWS_AS(hybrid_denoise(noisy, cfg), std::invalid_argument);  // "reference mode requires ..."
+        const Image small(10, 10, 0.5);
+        CHECK_THROWS_AS(hybrid_denoise(noisy, cfg, &small), std::invalid_argument);
+        Image clean(rows, cols);  // a reference image: the noiseless phantom stands in as a smooth ramp
+        for (int r = 0; r < rows; ++r)
+            for (int c = 0; c < cols; ++c) clean.at(r, c) = (20.0 + 0.5 * c) / 255.0;
+        const HybridResult hr = hybrid_denoise(noisy, cfg, &clean);
+        double acc = 0.0;
+        for (std::size_t i = 0; i < f.size(); ++i) {
+            const double d = f[i] / 255.0 - clean.pixels()[i];
+            acc += d * d;
+        }
+        const double sigma2 = acc / (double)f.size();
+        CHECK(std::fabs(hr.sigma2 - sigma2) <= 1e-15 * std::max(1.0, sigma2));
+        const long long Pn = (long long)rows * cols * 64;
+        const int64_t Wn = std::llround(sigma2 * 255.0 * 255.0 * 81.0 * (double)Pn);
+        hyb_oracle_wiener_gain_u8(f.data(), cols, rows, cols, 0, rows, 3, Wn, Pn, y.data(), cols);
+        CHECK(hr.image == from_u8(y.data(), rows, cols));
+        // stretch_after_each: AMF, stretch, W1 (robust); final_stretch: the closing stretch
+        FilterConfig c2;
+        c2.smax = 7;
+        c2.wiener_window = 3;
+        c2.final_stretch = true;
+        const HybridResult h2 = hybrid_denoise(noisy, c2, nullptr, true);
+        hyb_oracle_contrast_stretch_u8(f.data(), cols, rows, cols, fs.data(), cols);
+        int64_t w2 = 0;
+        hyb_oracle_wiener_stats_u8(fs.data(), cols, rows, cols, 0, rows, 3, &w2);
+        hyb_oracle_wiener_gain_u8(fs.data(), cols, rows, cols, 0, rows, 3, w2, (int64_t)rows * cols, y.data(), cols);
+        hyb_oracle_contrast_stretch_u8(y.data(), cols, rows, cols, y.data(), cols);
+        CHECK(h2.noise_sum == w2);
+        CHECK(h2.image == from_u8(y.data(), rows, cols));
     }
     // the reference's pipeline tail (proj/tests/test_pipeline.cpp:29-57, test_wiener.cpp:110-160)
     {
