@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "amf_core.cuh"
 #include "hyb_internal.cuh"
@@ -301,6 +302,183 @@ __global__ void __launch_bounds__(GNT, C::MINB) amf_grow_kernel(const __grid_con
     }
 }
 
+// ------------------------------------------------------------------------------------------
+// fused AMF kernel: k = 3 and the growth of a batch of tiles in one CTA
+// ------------------------------------------------------------------------------------------
+//
+// The separate kernels above write f, record the level-A failures in a global bitmap, and reload every
+// tile with failures (+ R halo) for the growth: the growth re-reads g (with halo), re-reads the bitmap
+// and rewrites the f sectors it touches (read-for-ownership) -- 3.7x the image in DRAM reads at config 4.
+// Here one CTA owns a batch of BT consecutive tiles end to end: TMA-loads them once with the growth halo
+// R, runs the k = 3 strips (k3_strip: f stored, failures appended straight to a shared-memory queue),
+// then the growth levels k = 5..smax over the batch's pooled queue from the resident tiles (grow_levels),
+// whose f byte stores land in L2 lines the k = 3 stores of the same CTA just wrote.  g is read once, f
+// written once; no bitmap, no records, no second launch.  Batches are claimed from a global counter, so
+// SMs that meet cheap batches take more.  Tile geometry: R <= 16 (smax <= 33), so the k = 3 byte-tile
+// layout (CP = 16, BS = 160) is the growth tile's.
+template <int NETMAX_, int MINB_, int BT_>
+struct FusedCfg {
+    static constexpr int NETMAX = NETMAX_, MINB = MINB_, BT = BT_;
+};
+#ifndef HYB_FUSED_BT_WIDE
+#define HYB_FUSED_BT_WIDE 4
+#endif
+#ifndef HYB_FUSED_BT_LEAN
+#define HYB_FUSED_BT_LEAN 3
+#endif
+using FusedWide = FusedCfg<9, 2, HYB_FUSED_BT_WIDE>;  // k = 9 network (114 registers): 2 CTAs / SM
+using FusedLean = FusedCfg<7, 3, HYB_FUSED_BT_LEAN>;  // networks to k = 7, radix above: 3 CTAs / SM
+static_assert(FusedWide::BT <= 8 && FusedLean::BT <= 8, "header layout / 3-bit queue slots");
+
+constexpr int FHDR = 1024;  // mbarriers [8], tile info [8][4], level counters [128], batch claim
+
+struct FArgs {
+    GGeo geo;
+    uint8_t* dst;
+    size_t dpitch, dslice;
+    uint8_t* fin;
+    size_t fpitch, fslice;
+    int rows, cols, row_begin, row_end, n_slices, smax;
+    int tiles_x, tiles_y;
+    int* claim;  // batch claims (reset by the last CTA)
+    int* done;
+};
+
+template <bool FIN, class C>
+inline size_t fused_smem(const GGeo& g) {  // header, tiles, k = 3 staging (+ finalized_at), two queues
+    return FHDR + (size_t)C::BT * g.b_bytes + (size_t)NW * (FIN ? 2 : 1) * WPIX + 2 * (size_t)C::BT * (TW * TH) * 2 + 128;
+}
+
+template <bool FIN, class C>
+__global__ void __launch_bounds__(NT, C::MINB) amf_fused_kernel(const __grid_constant__ CUtensorMap tm,
+                                                              const __grid_constant__ FArgs a) {
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+    const GGeo& geo = a.geo;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);     // [BT] tile loads
+    int* tinfo = reinterpret_cast<int*>(smem + 64);         // [BT][4]: x0, y0, z, border
+    int* qcount = reinterpret_cast<int*>(smem + 256);       // [MAX_LEVELS]
+    int* batch = reinterpret_cast<int*>(smem + 768);        // claimed first tile
+    uint8_t* slots = smem + FHDR;                           // [BT][geo.b_bytes]
+    uint8_t* stage = slots + (size_t)C::BT * geo.b_bytes;  // [NW][1 + FIN][WPIX] k = 3 output / finalized_at
+    uint16_t* Q0 = reinterpret_cast<uint16_t*>(stage + NW * (FIN ? 2 : 1) * WPIX);
+    uint16_t* Q1 = Q0 + C::BT * TW * TH;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int per_slice = a.tiles_x * a.tiles_y;
+    const int ntiles = per_slice * a.n_slices;
+    const bool grow = a.smax >= 5;
+    if (tid == 0) {
+        for (int i = 0; i < C::BT; ++i) mbar_init(&bar[i], 1);
+        prefetch_tmap(&tm);
+        fence_mbar_init();
+    }
+    if (tid < MAX_LEVELS) qcount[tid] = 0;
+    grid_dep_wait();  // the previous grid (e.g. the last step's gain reading dst) has completed
+    uint32_t phase = 0;
+    uint8_t* O = stage + warp * (FIN ? 2 : 1) * WPIX;
+    uint8_t* F = FIN ? O + WPIX : O;
+    auto out = [&](int sl, int pix, uint8_t v, int k) {
+        const int* ti = tinfo + 4 * sl;
+        const size_t row = (size_t)(ti[1] - a.row_begin + (pix >> 7));
+        a.dst[(size_t)ti[2] * a.dslice + row * a.dpitch + ti[0] + (pix & 127)] = v;
+        if (FIN) a.fin[(size_t)ti[2] * a.fslice + row * a.fpitch + ti[0] + (pix & 127)] = (uint8_t)k;
+    };
+    for (;;) {
+        if (tid == 0) *batch = atomicAdd(a.claim, C::BT);
+        __syncthreads();  // also: the previous batch's slot reads and queue use are complete
+        const int t0 = *batch;
+        if (t0 >= ntiles) break;
+        const int nt = min(C::BT, ntiles - t0);
+        if (tid == 0) {
+            fence_proxy_async_smem();  // the previous batch's generic slot accesses before the async writes
+            for (int i = 0; i < nt; ++i) {
+                const int t = t0 + i, z = t / per_slice, rem = t - z * per_slice, by = rem / a.tiles_x;
+                int* ti = tinfo + 4 * i;
+                ti[0] = (rem - by * a.tiles_x) * TW;
+                ti[1] = a.row_begin + by * TH;
+                ti[2] = z;
+                const int sx0 = ti[0] - geo.CP, sy0 = ti[1] - geo.R;
+                ti[3] = sx0 < 0 || sx0 + geo.BS > a.cols || sy0 < 0 || sy0 + geo.BH > a.rows;
+                grow_tile_load(&tm, geo, slots + (size_t)i * geo.b_bytes, &bar[i], ti[0], ti[1], z);
+            }
+        }
+        __syncthreads();  // tinfo
+        for (int i = 0; i < nt; ++i) mbar_wait(&bar[i], phase);
+        phase ^= 1u;
+        for (int i = 0; i < nt; ++i) {  // border tiles: edge replication within the growth reach R
+            const int* ti = tinfo + 4 * i;
+            if (!ti[3]) continue;  // uniform
+            const int sx0 = ti[0] - geo.CP, sy0 = ti[1] - geo.R;
+            replicate_edges<NT>(slots + (size_t)i * geo.b_bytes, geo.BS, max(0, -sx0), min(geo.BS, a.cols - sx0),
+                                max(0, -sy0), min(geo.BH, a.rows - sy0), 0, geo.BH, geo.R);
+        }
+        // ---- k = 3 on every pixel of the batch: f stored, level-A failures queued ----
+        for (int j = warp; j < nt * NW; j += NW) {
+            const int i = j / NW, sub = j % NW;
+            const int* ti = tinfo + 4 * i;
+            const int x0 = ti[0], y0 = ti[1], z = ti[2];
+            const uint8_t* B = slots + (size_t)i * geo.b_bytes + (size_t)(geo.R - 1) * geo.BS;  // row 0 = y0 - 1
+            k3_strip<FIN>(B, O, F, sub, nullptr,
+                          a.dst + (size_t)z * a.dslice + (size_t)(y0 - a.row_begin) * a.dpitch + x0, a.dpitch,
+                          FIN ? a.fin + (size_t)z * a.fslice + (size_t)(y0 - a.row_begin) * a.fpitch + x0 : nullptr,
+                          a.fpitch, a.row_end - y0, a.cols - x0, grow ? Q0 : nullptr, qcount, (uint32_t)i << 12);
+        }
+        __syncthreads();
+        // ---- growth k = 5..smax over the batch's pooled failures, from the resident tiles ----
+        const int total = qcount[0];
+        if (grow && total > 0) grow_levels<FIN, NT, decltype(out), C::NETMAX>(slots, geo, Q0, Q1, qcount, total,
+                                                                            a.smax, out);
+        __syncthreads();
+        if (tid < MAX_LEVELS) qcount[tid] = 0;
+    }
+    // the last CTA resets the claim counter for the next launch
+    if (tid == 0) {
+        __threadfence();
+        if (atomicAdd(a.done, 1) == (int)gridDim.x - 1) {
+            *a.claim = 0;
+            *a.done = 0;
+        }
+    }
+}
+
+template <bool FIN, class C>
+cudaError_t launch_fused_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, size_t fslice, const AmfWork& work,
+                             cudaStream_t stream) {
+    static PerDevice attr, occ;
+    const GGeo geo = make_ggeo(smax);
+    const size_t smem = fused_smem<FIN, C>(geo);
+    auto kern = amf_fused_kernel<FIN, C>;
+    cudaError_t e = ensure_smem_attr(attr, (const void*)kern, smem);
+    if (e != cudaSuccess) return e;
+    CUtensorMap tm;
+    e = make_tmap_u8(&tm, p.src, p.cols, p.rows, p.n_slices, p.spitch, p.sslice, geo.box_w, geo.box_h);
+    if (e != cudaSuccess) return e;
+    FArgs a;
+    a.geo = geo;
+    a.dst = p.dst;
+    a.dpitch = p.dpitch;
+    a.dslice = p.dslice;
+    a.fin = fin;
+    a.fpitch = fpitch;
+    a.fslice = fslice;
+    a.rows = p.rows;
+    a.cols = p.cols;
+    a.row_begin = p.row_begin;
+    a.row_end = p.row_end;
+    a.n_slices = p.n_slices;
+    a.smax = smax;
+    a.tiles_x = (p.cols + TW - 1) / TW;
+    a.tiles_y = (p.row_end - p.row_begin + TH - 1) / TH;
+    a.claim = work.counters + 2;
+    a.done = work.counters + 3;
+    const long long ntiles = (long long)a.tiles_x * a.tiles_y * a.n_slices;
+    const int per_sm = occupancy(occ, (const void*)kern, NT, smem);
+    const int grid = (int)std::min<long long>((ntiles + C::BT - 1) / C::BT, (long long)device_sms() * per_sm);
+    e = launch_pdl(kern, dim3(grid), dim3(NT), smem, stream, tm, a);
+    count_launch();
+    return e;
+}
+
 }  // namespace
 
 size_t amf_work_bytes(const Plane& p) {
@@ -321,6 +499,21 @@ AmfWork amf_work(uint8_t* base, const Plane& p) {
 
 cudaError_t launch_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, size_t fslice, const AmfWork& work,
                        cudaStream_t stream) {
+    // k = 3 + growth in one kernel per tile batch (amf_fused_kernel) for single images with smax 5..9
+    // (config 2: -6 % AMF time); the two-kernel path (pipelined k = 3 kernel, pooled growth over 8-tile
+    // batches) for smax >= 11 and for stacks, where it measured faster (config 4
+    // 2.13 vs 2.26 ms, config 3 0.24 vs 0.27 ms).  HYB_AMF_SPLIT / HYB_AMF_FUSED force one path (A/B).
+    static const bool force_split = getenv("HYB_AMF_SPLIT") != nullptr;
+    static const bool force_fused = getenv("HYB_AMF_FUSED") != nullptr;
+    static const bool lean11 = getenv("HYB_FUSED_LEAN11") != nullptr;
+    const bool fusable = smax >= 5 && (smax - 1) / 2 <= 16;
+    if (fusable && !force_split && (force_fused || (smax <= 9 && p.n_slices == 1))) {
+        if (smax >= 11 && !lean11)
+            return fin ? launch_fused_amf<true, FusedWide>(p, smax, fin, fpitch, fslice, work, stream)
+                       : launch_fused_amf<false, FusedWide>(p, smax, fin, fpitch, fslice, work, stream);
+        return fin ? launch_fused_amf<true, FusedLean>(p, smax, fin, fpitch, fslice, work, stream)
+                   : launch_fused_amf<false, FusedLean>(p, smax, fin, fpitch, fslice, work, stream);
+    }
     static PerDevice attr_k3[2], occ_k3;
     cudaError_t e = ensure_smem_attr(attr_k3[0], (const void*)amf_k3_kernel<false>, SMEM);
     if (e == cudaSuccess) e = ensure_smem_attr(attr_k3[1], (const void*)amf_k3_kernel<true>, SMEM);

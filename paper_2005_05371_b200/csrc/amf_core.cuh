@@ -387,13 +387,10 @@ __device__ __forceinline__ uint32_t select_rank(const uint32_t (&w)[K][Win<K>::A
     return prefix;
 }
 
-// k = 9, 11: one pixel per thread; level A from SWAR counts, median by radix select if needed.
+// Window extremes of a K x K window (aligned words): zmin / zmax.
 template <int K>
-__device__ __forceinline__ bool level_radix(const uint8_t* __restrict__ B, const GGeo& geo, int ty, int tx,
-                                            uint8_t* out) {
+__device__ __forceinline__ void window_minmax(const uint32_t (&w)[K][Win<K>::AW], uint32_t& zmin, uint32_t& zmax) {
     using W = Win<K>;
-    uint32_t w[K][W::AW];
-    load_window<K>(B, geo, ty, tx, w);
     uint32_t mn = 0x00FF00FFu, mx = 0u;
 #pragma unroll
     for (int r = 0; r < K; ++r)
@@ -415,12 +412,40 @@ __device__ __forceinline__ bool level_radix(const uint8_t* __restrict__ B, const
             mn = __vimin3_u16x2(mn, lo, hi);
             mx = __vimax3_u16x2(mx, lo, hi);
         }
-    const uint32_t zmin = min(mn & 0xFFFFu, mn >> 16), zmax = max(mx & 0xFFFFu, mx >> 16);
-    // level A <=> zmin < zmax, #(v == zmin) <= m and #(v == zmax) <= m
-    if (zmin == zmax || count_eq<K>(w, zmin) > W::M || count_eq<K>(w, zmax) > W::M) return false;
+    zmin = min(mn & 0xFFFFu, mn >> 16);
+    zmax = max(mx & 0xFFFFu, mx >> 16);
+}
+
+// k = 9, 11, one pixel per thread, first pass: level A from SWAR counts without a median
+// (zmin < zmed < zmax <=> zmin < zmax, #(v == zmin) <= m and #(v == zmax) <= m).  Returns 0: level A
+// fails; 1: resolved, *out = g (zmin < g < zmax); 2: resolved to the median, which the caller computes
+// in a second, compacted pass (level_radix_median) so the radix select runs on full warps.
+template <int K>
+__device__ __forceinline__ int level_radix_test(const uint8_t* __restrict__ B, const GGeo& geo, int ty, int tx,
+                                                uint8_t* out) {
+    using W = Win<K>;
+    uint32_t w[K][W::AW];
+    load_window<K>(B, geo, ty, tx, w);
+    uint32_t zmin, zmax;
+    window_minmax<K>(w, zmin, zmax);
+    if (zmin == zmax || count_eq<K>(w, zmin) > W::M || count_eq<K>(w, zmax) > W::M) return 0;
     const uint32_t g = B[(size_t)(ty + geo.R) * geo.BS + tx + geo.CP];
-    *out = (uint8_t)((g != zmin && g != zmax) ? g : select_rank<K>(w, W::M, zmin, zmax));
-    return true;
+    if (g != zmin && g != zmax) {
+        *out = (uint8_t)g;
+        return 1;
+    }
+    return 2;
+}
+
+// Second pass: the window median by bitwise radix select (values within [zmin, zmax]).
+template <int K>
+__device__ __forceinline__ uint8_t level_radix_median(const uint8_t* __restrict__ B, const GGeo& geo, int ty, int tx) {
+    using W = Win<K>;
+    uint32_t w[K][W::AW];
+    load_window<K>(B, geo, ty, tx, w);
+    uint32_t zmin, zmax;
+    window_minmax<K>(w, zmin, zmax);
+    return (uint8_t)select_rank<K>(w, W::M, zmin, zmax);
 }
 
 // k > 11: same algorithm on byte reads from the tile.
@@ -611,26 +636,41 @@ __device__ __forceinline__ void grow_levels_at(Slot slot, const GGeo& geo, uint1
                 }
             }
         } else {
+            // one pixel per thread.  k = 9 / 11: the level-A test first; pixels resolved to the median
+            // (g at a window extreme) are compacted per warp over the warp's already consumed queue
+            // slots (entry s at qw[warp * 32 + (s / 32) * NTHR + s % 32]) and get their radix select in a
+            // second pass on full warps -- in one pass, every warp with any such lane paid the whole select.
+            const bool radix = k == 9 || k == 11;
+            uint16_t* qw = const_cast<uint16_t*>(qin);
+            int nmed = 0;  // warp-uniform
             for (int base = warp * 32; base < n; base += NTHR) {
                 const int i = base + lane;
-                bool keep = false;
+                bool keep = false, med = false;
                 int e = 0;
                 if (i < n) {
                     e = qin[i];
                     const int sl = e >> 12, pix = e & 4095, ty = pix >> 7, tx = pix & 127;
                     const uint8_t* B = slot(sl);
                     uint8_t o = 0;
-                    bool done;
-                    switch (k) {
-                        case 9: done = level_radix<9>(B, geo, ty, tx, &o); break;
-                        case 11: done = level_radix<11>(B, geo, ty, tx, &o); break;
-                        default: done = level_generic(B, geo, ty, tx, k, &o); break;
-                    }
-                    if (done) {
+                    if (radix) {
+                        const int st = k == 9 ? level_radix_test<9>(B, geo, ty, tx, &o)
+                                              : level_radix_test<11>(B, geo, ty, tx, &o);
+                        if (st == 1) out(sl, pix, o, k);
+                        med = st == 2;
+                        keep = st == 0;
+                    } else if (level_generic(B, geo, ty, tx, k, &o)) {
                         out(sl, pix, o, k);
                     } else {
                         keep = true;
                     }
+                }
+                if (radix) {
+                    const uint32_t bm = __ballot_sync(0xFFFFFFFFu, med);
+                    if (med) {
+                        const int s = nmed + __popc(bm & ((1u << lane) - 1u));
+                        qw[warp * 32 + (s >> 5) * NTHR + (s & 31)] = (uint16_t)e;
+                    }
+                    nmed += __popc(bm);
                 }
                 if (!last) {
                     const uint32_t bal = __ballot_sync(0xFFFFFFFFu, keep);
@@ -640,6 +680,17 @@ __device__ __forceinline__ void grow_levels_at(Slot slot, const GGeo& geo, uint1
                         qb = __shfl_sync(0xFFFFFFFFu, qb, 0);
                         if (keep) qout[qb + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)e;
                     }
+                }
+            }
+            __syncwarp();
+            for (int s0 = 0; s0 < nmed; s0 += 32) {
+                const int s = s0 + lane;
+                if (s < nmed) {
+                    const int e = qw[warp * 32 + (s >> 5) * NTHR + (s & 31)];
+                    const int sl = e >> 12, pix = e & 4095, ty = pix >> 7, tx = pix & 127;
+                    const uint8_t* B = slot(sl);
+                    const uint8_t o = k == 9 ? level_radix_median<9>(B, geo, ty, tx) : level_radix_median<11>(B, geo, ty, tx);
+                    out(sl, pix, o, k);
                 }
             }
         }

@@ -1,0 +1,10 @@
+o=gpurun_out/r2h; mkdir -p $o
+timeout 900 python -m pytest tests/test_gpu_paths.py -x -q > $o/gpu_tests.txt 2>&1; echo "gpu tests rc=$?"; tail -2 $o/gpu_tests.txt
+for lib in libhybrid_cuda.so libhybrid_cuda_alt.so libhybrid_cuda.so libhybrid_cuda_alt.so; do
+HYB_LIB=$lib timeout 300 python bench.py --config 4 --no-cpu-baseline > $o/bench_c4.json 2> $o/bench_c4.err
+python - <<PY
+import json
+d=json.loads(open("$o/bench_c4.json").read().strip().splitlines()[-1])
+print("C4 $lib", d["value"], d["ms_per_step"], d["roofline"]["kernel_ms"], d["clocks"]["sm_mhz"], d["clocks"]["samples"])
+PY
+done
