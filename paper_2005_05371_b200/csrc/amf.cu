@@ -316,21 +316,29 @@ __global__ void __launch_bounds__(GNT, C::MINB) amf_grow_kernel(const __grid_con
 // written once; no bitmap, no records, no second launch.  Batches are claimed from a global counter, so
 // SMs that meet cheap batches take more.  Tile geometry: R <= 16 (smax <= 33), so the k = 3 byte-tile
 // layout (CP = 16, BS = 160) is the growth tile's.
-template <int NETMAX_, int MINB_, int BT_>
+template <int NETMAX_, int MINB_, int BT_, int NSET_>
 struct FusedCfg {
     static constexpr int NETMAX = NETMAX_, MINB = MINB_, BT = BT_;
+    static constexpr int NSET = NSET_;  // slot sets: 2 = the next batch's tiles load while this one computes
 };
+// Measured (config 2 / 3 / 4 AMF ms): one slot set with 3 / 4 tiles per batch 0.182 / 0.270 / 2.26; two sets
+// (the next batch's tiles load during this one) with 2 / 3 tiles 0.197 / 0.286 / 2.47 -- the growth pool size
+// matters more than the exposed load latency, which the co-resident CTAs cover.
 #ifndef HYB_FUSED_BT_WIDE
 #define HYB_FUSED_BT_WIDE 4
 #endif
 #ifndef HYB_FUSED_BT_LEAN
 #define HYB_FUSED_BT_LEAN 3
 #endif
-using FusedWide = FusedCfg<9, 2, HYB_FUSED_BT_WIDE>;  // k = 9 network (114 registers): 2 CTAs / SM
-using FusedLean = FusedCfg<7, 3, HYB_FUSED_BT_LEAN>;  // networks to k = 7, radix above: 3 CTAs / SM
-static_assert(FusedWide::BT <= 8 && FusedLean::BT <= 8, "header layout / 3-bit queue slots");
+#ifndef HYB_FUSED_NSET
+#define HYB_FUSED_NSET 1
+#endif
+using FusedWide = FusedCfg<9, 2, HYB_FUSED_BT_WIDE, HYB_FUSED_NSET>;  // k = 9 network (~115 registers): 2 CTAs / SM
+using FusedLean = FusedCfg<7, 3, HYB_FUSED_BT_LEAN, HYB_FUSED_NSET>;  // networks to k = 7, radix above: 3 CTAs / SM
+static_assert(FusedWide::BT * FusedWide::NSET <= 16 && FusedLean::BT * FusedLean::NSET <= 16, "header layout");
+static_assert(FusedWide::BT <= 8 && FusedLean::BT <= 8, "3-bit queue slots");
 
-constexpr int FHDR = 1024;  // mbarriers [8], tile info [8][4], level counters [128], batch claim
+constexpr int FHDR = 1024;  // mbarriers [16], tile info [16][4], level counters [128], batch claims [2]
 
 struct FArgs {
     GGeo geo;
@@ -345,79 +353,84 @@ struct FArgs {
 };
 
 template <bool FIN, class C>
-inline size_t fused_smem(const GGeo& g) {  // header, tiles, k = 3 staging (+ finalized_at), two queues
-    return FHDR + (size_t)C::BT * g.b_bytes + (size_t)NW * (FIN ? 2 : 1) * WPIX + 2 * (size_t)C::BT * (TW * TH) * 2 + 128;
+inline size_t fused_smem(const GGeo& g) {  // header, tile sets, k = 3 staging (+ finalized_at), two queues
+    return FHDR + (size_t)C::NSET * C::BT * g.b_bytes + (size_t)NW * (FIN ? 2 : 1) * WPIX +
+           2 * (size_t)C::BT * (TW * TH) * 2 + 128;
 }
 
 template <bool FIN, class C>
 __global__ void __launch_bounds__(NT, C::MINB) amf_fused_kernel(const __grid_constant__ CUtensorMap tm,
                                                               const __grid_constant__ FArgs a) {
+    constexpr int BT = C::BT, NSET = C::NSET;
     extern __shared__ __align__(128) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
     const GGeo& geo = a.geo;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);     // [BT] tile loads
-    int* tinfo = reinterpret_cast<int*>(smem + 64);         // [BT][4]: x0, y0, z, border
-    int* qcount = reinterpret_cast<int*>(smem + 256);       // [MAX_LEVELS]
-    int* batch = reinterpret_cast<int*>(smem + 768);        // claimed first tile
-    uint8_t* slots = smem + FHDR;                           // [BT][geo.b_bytes]
-    uint8_t* stage = slots + (size_t)C::BT * geo.b_bytes;  // [NW][1 + FIN][WPIX] k = 3 output / finalized_at
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);     // [NSET][BT] tile loads
+    int* tinfo = reinterpret_cast<int*>(smem + 128);        // [NSET][BT][4]: x0, y0, z, border
+    int* qcount = reinterpret_cast<int*>(smem + 384);       // [MAX_LEVELS]
+    int* batch = reinterpret_cast<int*>(smem + 896);        // [NSET] claimed first tile
+    uint8_t* slots = smem + FHDR;                           // [NSET][BT][geo.b_bytes]
+    uint8_t* stage = slots + (size_t)NSET * BT * geo.b_bytes;  // [NW][1 + FIN][WPIX] k = 3 output / finalized_at
     uint16_t* Q0 = reinterpret_cast<uint16_t*>(stage + NW * (FIN ? 2 : 1) * WPIX);
-    uint16_t* Q1 = Q0 + C::BT * TW * TH;
+    uint16_t* Q1 = Q0 + BT * TW * TH;
     const int tid = threadIdx.x, warp = tid >> 5;
     const int per_slice = a.tiles_x * a.tiles_y;
     const int ntiles = per_slice * a.n_slices;
     const bool grow = a.smax >= 5;
     if (tid == 0) {
-        for (int i = 0; i < C::BT; ++i) mbar_init(&bar[i], 1);
+        for (int i = 0; i < NSET * BT; ++i) mbar_init(&bar[i], 1);
         prefetch_tmap(&tm);
         fence_mbar_init();
     }
     if (tid < MAX_LEVELS) qcount[tid] = 0;
     grid_dep_wait();  // the previous grid (e.g. the last step's gain reading dst) has completed
-    uint32_t phase = 0;
+    // thread 0: claim the next BT tiles for slot set `set` and start their TMA loads (+ growth halo R)
+    auto claim_issue = [&](int set) {
+        const int t0 = atomicAdd(a.claim, BT);
+        batch[set] = t0;
+        if (t0 >= ntiles) return;
+        fence_proxy_async_smem();  // the slot set's previous generic accesses before the async writes
+        for (int i = 0; i < min(BT, ntiles - t0); ++i) {
+            const int t = t0 + i, z = t / per_slice, rem = t - z * per_slice, by = rem / a.tiles_x;
+            int* ti = tinfo + 4 * (set * BT + i);
+            ti[0] = (rem - by * a.tiles_x) * TW;
+            ti[1] = a.row_begin + by * TH;
+            ti[2] = z;
+            const int sx0 = ti[0] - geo.CP, sy0 = ti[1] - geo.R;
+            ti[3] = sx0 < 0 || sx0 + geo.BS > a.cols || sy0 < 0 || sy0 + geo.BH > a.rows;
+            grow_tile_load(&tm, geo, slots + (size_t)(set * BT + i) * geo.b_bytes, &bar[set * BT + i], ti[0], ti[1],
+                           z);
+        }
+    };
     uint8_t* O = stage + warp * (FIN ? 2 : 1) * WPIX;
     uint8_t* F = FIN ? O + WPIX : O;
-    auto out = [&](int sl, int pix, uint8_t v, int k) {
-        const int* ti = tinfo + 4 * sl;
-        const size_t row = (size_t)(ti[1] - a.row_begin + (pix >> 7));
-        a.dst[(size_t)ti[2] * a.dslice + row * a.dpitch + ti[0] + (pix & 127)] = v;
-        if (FIN) a.fin[(size_t)ti[2] * a.fslice + row * a.fpitch + ti[0] + (pix & 127)] = (uint8_t)k;
-    };
-    for (;;) {
-        if (tid == 0) *batch = atomicAdd(a.claim, C::BT);
-        __syncthreads();  // also: the previous batch's slot reads and queue use are complete
-        const int t0 = *batch;
+    uint32_t phases = 0;  // bit s: parity of slot set s's next wait
+    if (tid == 0) claim_issue(0);
+    for (int it = 0;; ++it) {
+        const int cur = NSET == 2 ? (it & 1) : 0;
+        if (NSET == 1 && it > 0 && tid == 0) claim_issue(0);
+        __syncthreads();  // batch / tile info of this set; the previous batch's slot and queue use complete
+        const int t0 = batch[cur];
         if (t0 >= ntiles) break;
-        const int nt = min(C::BT, ntiles - t0);
-        if (tid == 0) {
-            fence_proxy_async_smem();  // the previous batch's generic slot accesses before the async writes
-            for (int i = 0; i < nt; ++i) {
-                const int t = t0 + i, z = t / per_slice, rem = t - z * per_slice, by = rem / a.tiles_x;
-                int* ti = tinfo + 4 * i;
-                ti[0] = (rem - by * a.tiles_x) * TW;
-                ti[1] = a.row_begin + by * TH;
-                ti[2] = z;
-                const int sx0 = ti[0] - geo.CP, sy0 = ti[1] - geo.R;
-                ti[3] = sx0 < 0 || sx0 + geo.BS > a.cols || sy0 < 0 || sy0 + geo.BH > a.rows;
-                grow_tile_load(&tm, geo, slots + (size_t)i * geo.b_bytes, &bar[i], ti[0], ti[1], z);
-            }
-        }
-        __syncthreads();  // tinfo
-        for (int i = 0; i < nt; ++i) mbar_wait(&bar[i], phase);
-        phase ^= 1u;
+        if (NSET == 2 && tid == 0) claim_issue(cur ^ 1);  // the next batch loads while this one computes
+        const int nt = min(BT, ntiles - t0);
+        uint8_t* bufs = slots + (size_t)cur * BT * geo.b_bytes;
+        const int* tset = tinfo + 4 * cur * BT;
+        for (int i = 0; i < nt; ++i) mbar_wait(&bar[cur * BT + i], (phases >> cur) & 1u);
+        phases ^= 1u << cur;
         for (int i = 0; i < nt; ++i) {  // border tiles: edge replication within the growth reach R
-            const int* ti = tinfo + 4 * i;
+            const int* ti = tset + 4 * i;
             if (!ti[3]) continue;  // uniform
             const int sx0 = ti[0] - geo.CP, sy0 = ti[1] - geo.R;
-            replicate_edges<NT>(slots + (size_t)i * geo.b_bytes, geo.BS, max(0, -sx0), min(geo.BS, a.cols - sx0),
+            replicate_edges<NT>(bufs + (size_t)i * geo.b_bytes, geo.BS, max(0, -sx0), min(geo.BS, a.cols - sx0),
                                 max(0, -sy0), min(geo.BH, a.rows - sy0), 0, geo.BH, geo.R);
         }
         // ---- k = 3 on every pixel of the batch: f stored, level-A failures queued ----
         for (int j = warp; j < nt * NW; j += NW) {
             const int i = j / NW, sub = j % NW;
-            const int* ti = tinfo + 4 * i;
+            const int* ti = tset + 4 * i;
             const int x0 = ti[0], y0 = ti[1], z = ti[2];
-            const uint8_t* B = slots + (size_t)i * geo.b_bytes + (size_t)(geo.R - 1) * geo.BS;  // row 0 = y0 - 1
+            const uint8_t* B = bufs + (size_t)i * geo.b_bytes + (size_t)(geo.R - 1) * geo.BS;  // row 0 = y0 - 1
             k3_strip<FIN>(B, O, F, sub, nullptr,
                           a.dst + (size_t)z * a.dslice + (size_t)(y0 - a.row_begin) * a.dpitch + x0, a.dpitch,
                           FIN ? a.fin + (size_t)z * a.fslice + (size_t)(y0 - a.row_begin) * a.fpitch + x0 : nullptr,
@@ -426,8 +439,15 @@ __global__ void __launch_bounds__(NT, C::MINB) amf_fused_kernel(const __grid_con
         __syncthreads();
         // ---- growth k = 5..smax over the batch's pooled failures, from the resident tiles ----
         const int total = qcount[0];
-        if (grow && total > 0) grow_levels<FIN, NT, decltype(out), C::NETMAX>(slots, geo, Q0, Q1, qcount, total,
-                                                                            a.smax, out);
+        if (grow && total > 0) {
+            auto out = [&](int sl, int pix, uint8_t v, int k) {
+                const int* ti = tset + 4 * sl;
+                const size_t row = (size_t)(ti[1] - a.row_begin + (pix >> 7));
+                a.dst[(size_t)ti[2] * a.dslice + row * a.dpitch + ti[0] + (pix & 127)] = v;
+                if (FIN) a.fin[(size_t)ti[2] * a.fslice + row * a.fpitch + ti[0] + (pix & 127)] = (uint8_t)k;
+            };
+            grow_levels<FIN, NT, decltype(out), C::NETMAX>(bufs, geo, Q0, Q1, qcount, total, a.smax, out);
+        }
         __syncthreads();
         if (tid < MAX_LEVELS) qcount[tid] = 0;
     }
