@@ -239,7 +239,13 @@ struct GrowCfg {
 #define HYB_LEAN_DYN 0
 #endif
 using GrowWide = GrowCfg<9, 2, 8, 8192, true, 13>;
-using GrowLean = GrowCfg<7, 3, 8, 4096, HYB_LEAN_DYN != 0, 11>;
+#ifndef HYB_LEAN_SLOTS
+#define HYB_LEAN_SLOTS 8
+#endif
+#ifndef HYB_WIDE_MIN_SMAX
+#define HYB_WIDE_MIN_SMAX 11  // smallest smax grown by the wide variant
+#endif
+using GrowLean = GrowCfg<7, 3, HYB_LEAN_SLOTS, 4096, HYB_LEAN_DYN != 0, 11>;
 static_assert(GrowWide::SLOTS <= 8 && GrowLean::SLOTS <= 8, "header layout");
 static_assert(GrowWide::CHUNK_SHIFT >= 11 && GrowLean::CHUNK_SHIFT >= 11, "chunk table sized for chunks >= 2048");
 
@@ -565,7 +571,7 @@ cudaError_t launch_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, si
     a.rec_ctr = reinterpret_cast<unsigned long long*>(work.counters);
     a.records = work.records;
     a.chunk_rec = work.chunk_rec;
-    a.chunk_shift = smax >= 11 ? GrowWide::CHUNK_SHIFT : GrowLean::CHUNK_SHIFT;  // the growth variant below
+    a.chunk_shift = smax >= HYB_WIDE_MIN_SMAX ? GrowWide::CHUNK_SHIFT : GrowLean::CHUNK_SHIFT;  // the growth variant below
     const int per_sm = occupancy(occ_k3, (const void*)amf_k3_kernel<false>, K3T, SMEM);
     const long long ntiles = (long long)a.tiles_x * a.tiles_y * a.n_slices;
     const int grid = (int)std::min<long long>(ntiles, (long long)num_sms * per_sm);
@@ -576,7 +582,7 @@ cudaError_t launch_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, si
 
     // ---- growth: one batched launch for every window size k = 5..smax ----
     const GGeo geo = make_ggeo(smax);
-    const bool wide = smax >= 11;
+    const bool wide = smax >= HYB_WIDE_MIN_SMAX;
     const size_t gsm = wide ? grow_smem<GrowWide>(geo) : grow_smem<GrowLean>(geo);
     auto kern = wide ? (fin ? amf_grow_kernel<true, GrowWide> : amf_grow_kernel<false, GrowWide>)
                      : (fin ? amf_grow_kernel<true, GrowLean> : amf_grow_kernel<false, GrowLean>);
