@@ -76,6 +76,14 @@ int hyb_set_stream(hyb_ctx* ctx, void* stream);
  * launch, which guarantees co-residency even with concurrent work.  (Library extension; the
  * reference has no device.) */
 int hyb_set_exclusive(hyb_ctx* ctx, int exclusive);
+/* async_host != 0: hyb_hybrid_u8 calls (parts = 1, no hyb_stats) on PINNED host buffers return as soon
+ * as the work is enqueued.  Device staging is double-buffered, so the next call's upload overlaps this
+ * call's download (a stream of images keeps both PCIe directions busy).  The caller must not touch the
+ * buffers of a pending call; results are complete after hyb_synchronize() (or hyb_set_async(ctx, 0)).
+ * Other calls and pageable buffers keep the synchronous behaviour.  (Library extension.) */
+int hyb_set_async(hyb_ctx* ctx, int async_host);
+/* Waits for every call enqueued on the context (all its streams, all its devices). */
+int hyb_synchronize(hyb_ctx* ctx);
 const char* hyb_last_error(const hyb_ctx* ctx);
 /* Number of kernels this context has launched so far (bench evidence). */
 int64_t hyb_kernel_launches(const hyb_ctx* ctx);

@@ -22,7 +22,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)),
 
 # Every symbol include/hybrid_cuda.h declares (checked by tests/test_capi_symbols.py).
 EXPORTED = (
-    "hyb_create", "hyb_create_multi", "hyb_context_devices", "hyb_destroy", "hyb_set_stream", "hyb_set_exclusive", "hyb_last_error", "hyb_kernel_launches",
+    "hyb_create", "hyb_create_multi", "hyb_context_devices", "hyb_destroy", "hyb_set_stream", "hyb_set_exclusive", "hyb_set_async", "hyb_synchronize", "hyb_last_error", "hyb_kernel_launches",
     "hyb_validate_smax", "hyb_validate_config", "hyb_amf_u8", "hyb_amf_batch_u8",
     "hyb_wiener_stats_u8", "hyb_wiener_gain_u8", "hyb_wiener_u8", "hyb_hybrid_u8",
     "hyb_hybrid_batch_u8", "hyb_contrast_stretch_u8", "hyb_hybrid_stretch_u8",
@@ -63,6 +63,8 @@ def _load():
         "hyb_destroy": (c_int, [P]),
         "hyb_set_stream": (c_int, [P, c_void_p]),
         "hyb_set_exclusive": (c_int, [P, c_int]),
+        "hyb_set_async": (c_int, [P, c_int]),
+        "hyb_synchronize": (c_int, [P]),
         "hyb_last_error": (c_char_p, [P]),
         "hyb_kernel_launches": (c_int64, [P]),
         "hyb_validate_smax": (c_int, [c_int]),
@@ -145,6 +147,13 @@ class Context:
     def set_exclusive(self, exclusive: bool) -> None:
         """Dedicated-GPU mode (hyb_set_exclusive): plain instead of cooperative fused launches."""
         check(lib.hyb_set_exclusive(self.ptr, int(bool(exclusive))), self.ptr)
+
+    def set_async(self, on: bool) -> None:
+        """hyb_set_async: host-buffer calls return once enqueued (double-buffered staging); synchronize()."""
+        check(lib.hyb_set_async(self.ptr, int(bool(on))), self.ptr)
+
+    def synchronize(self) -> None:
+        check(lib.hyb_synchronize(self.ptr), self.ptr)
 
     def launches(self) -> int:
         return int(lib.hyb_kernel_launches(self.ptr))

@@ -95,6 +95,13 @@ struct hyb_ctx {
     std::vector<hyb_ctx*> peers;
     std::vector<char> peer_ok;
     DevBuf wparts, wtot, mg_in, mg_out;  // gathered partial W, total W, staged batch chunk
+    // Asynchronous host-buffer calls (hyb_set_async): double-buffered staging, so call i + 1's upload
+    // (copy stream) runs while call i's result downloads (copy2 stream) -- both PCIe directions busy.
+    bool async_host = false;
+    int async_parity = 0;
+    DevBuf ain[2], aout[2];
+    cudaEvent_t ev_in_free[2] = {}, ev_out_free[2] = {};
+    cudaEvent_t ev_ah2d[2][16] = {}, ev_again[2][16] = {};
     cudaEvent_t ev_stats = nullptr, ev_done = nullptr, ev_start = nullptr;
     static constexpr int kMaxChunks = 16;
     cudaEvent_t ev_h2d[kMaxChunks] = {}, ev_gain[kMaxChunks] = {};
@@ -604,6 +611,96 @@ int hybrid_multi(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int col
     return HYB_OK;
 }
 
+// Asynchronous host-buffer hybrid (hyb_set_async, pinned host buffers, one device): the same chunked
+// pipeline as hybrid_host_pipelined, but with double-buffered device staging (call parity b) and the
+// download on its own stream, and no host synchronisation: call i + 1's H2D (copy stream) overlaps call
+// i's D2H (copy2 stream), so a sequence of images keeps both PCIe directions busy.  Cross-call hazards
+// are events: in[b] is refilled after call i - 2's last AMF read (ev_in_free), out[b] rewritten after
+// call i - 2's download (ev_out_free); f and W are used on the compute stream only (serialised).
+int hybrid_host_async(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int cols, int smax, int win, uint8_t* y,
+                      size_t y_pitch) {
+    const int b = ctx->async_parity;
+    const int rA = (smax - 1) / 2, rW = (win - 1) / 2;
+    const long long bytes = (long long)rows * cols;
+    const int want = bytes < (8ll << 20) ? 1 : 4;
+    const int K = std::max(1, std::min(want, rows / std::max(64, 2 * (rA + rW) + 1)));
+    const size_t pp = round_pitch(cols);
+    if (!ctx->ev_in_free[b]) {
+        for (int i = 0; i < 2; ++i) {
+            HYB_CHECK(cudaEventCreateWithFlags(&ctx->ev_in_free[i], cudaEventDisableTiming));
+            HYB_CHECK(cudaEventCreateWithFlags(&ctx->ev_out_free[i], cudaEventDisableTiming));
+            for (int k = 0; k < hyb_ctx::kMaxChunks; ++k) {
+                HYB_CHECK(cudaEventCreateWithFlags(&ctx->ev_ah2d[i][k], cudaEventDisableTiming));
+                HYB_CHECK(cudaEventCreateWithFlags(&ctx->ev_again[i][k], cudaEventDisableTiming));
+            }
+        }
+    }
+    HYB_CHECK(ctx->ain[b].ensure(pp * rows));
+    HYB_CHECK(ctx->aout[b].ensure(pp * rows));
+    HYB_CHECK(ctx->f.ensure(pp * rows));
+    HYB_CHECK(ctx->wsum.ensure(sizeof(long long)));
+    unsigned long long* W = reinterpret_cast<unsigned long long*>(ctx->wsum.ptr);
+    uint8_t* in = ctx->ain[b].ptr;
+    uint8_t* out = ctx->aout[b].ptr;
+    cudaStream_t cs = ctx->stream, xs = ctx->copy, ys = ctx->copy2;
+    std::vector<int> a(K + 1);
+    for (int k = 0; k <= K; ++k) a[k] = (int)((long long)rows * k / K);
+    auto cp = [&](void* dst, size_t dp, const void* src, size_t sp, int nrows, cudaStream_t st) {
+        if (dp == (size_t)cols && sp == (size_t)cols)
+            return cudaMemcpyAsync(dst, src, (size_t)cols * nrows, cudaMemcpyDefault, st);
+        return cudaMemcpy2DAsync(dst, dp, src, sp, (size_t)cols, (size_t)nrows, cudaMemcpyDefault, st);
+    };
+    // upload (copy stream), once call i - 2 is done reading in[b]
+    HYB_CHECK(cudaStreamWaitEvent(xs, ctx->ev_in_free[b], 0));
+    for (int k = 0; k < K; ++k) {
+        HYB_CHECK(cp(in + (size_t)a[k] * pp, pp, g + (size_t)a[k] * pitch, pitch, a[k + 1] - a[k], xs));
+        HYB_CHECK(cudaEventRecord(ctx->ev_ah2d[b][k], xs));
+    }
+    // compute stream: AMF + statistics per chunk as the rows land, then the gains
+    if (K == 1 && hyb::plan_small(rows, cols, smax, win).ok) {
+        HYB_CHECK(cudaStreamWaitEvent(cs, ctx->ev_ah2d[b][0], 0));
+        HYB_CHECK(cudaStreamWaitEvent(cs, ctx->ev_out_free[b], 0));
+        int st;
+        if (!try_small(ctx, in, pp, rows, cols, smax, win, out, pp, false, &st))
+            st = hybrid_device(ctx, in, pp, rows, cols, smax, win, 1, out, pp, false);
+        if (st) return st;
+        HYB_CHECK(cudaEventRecord(ctx->ev_in_free[b], cs));
+        HYB_CHECK(cudaEventRecord(ctx->ev_again[b][0], cs));
+    } else {
+        HYB_CHECK(cudaMemsetAsync(W, 0, sizeof(long long), cs));
+        auto stats = [&](int k) -> cudaError_t {
+            hyb::Plane w{ctx->f.ptr, pp, 0, nullptr, 0, 0, rows, cols, a[k], a[k + 1], 1};
+            return hyb::launch_wiener_stats(w, win, W, cs);
+        };
+        for (int k = 0; k < K; ++k) {
+            int need = k;  // last chunk holding input rows < a[k+1] + rA
+            while (need + 1 < K && a[need + 1] < std::min(rows, a[k + 1] + rA)) ++need;
+            HYB_CHECK(cudaStreamWaitEvent(cs, ctx->ev_ah2d[b][need], 0));
+            hyb::Plane am{in, pp, 0, ctx->f.ptr + (size_t)a[k] * pp, pp, 0, rows, cols, a[k], a[k + 1], 1};
+            HYB_CHECK(run_amf(ctx, am, smax, nullptr, 0, 0));
+            if (k >= 1 && a[k + 1] - a[k] >= rW) HYB_CHECK(stats(k - 1));
+            else if (k >= 1) return fail(ctx, HYB_EINVAL, "chunk thinner than the Wiener halo");
+        }
+        HYB_CHECK(stats(K - 1));
+        HYB_CHECK(cudaEventRecord(ctx->ev_in_free[b], cs));
+        HYB_CHECK(cudaStreamWaitEvent(cs, ctx->ev_out_free[b], 0));
+        for (int k = 0; k < K; ++k) {
+            hyb::Plane w{ctx->f.ptr, pp, 0, out + (size_t)a[k] * pp, pp, 0, rows, cols, a[k], a[k + 1], 1};
+            HYB_CHECK(hyb::launch_wiener_gain(w, win, reinterpret_cast<const long long*>(W), bytes, cs));
+            HYB_CHECK(cudaEventRecord(ctx->ev_again[b][k], cs));
+        }
+    }
+    // download (copy2 stream) chunk by chunk as the gains finish
+    const int Kd = (K == 1 && hyb::plan_small(rows, cols, smax, win).ok) ? 1 : K;
+    for (int k = 0; k < Kd; ++k) {
+        HYB_CHECK(cudaStreamWaitEvent(ys, ctx->ev_again[b][k], 0));
+        HYB_CHECK(cp(y + (size_t)a[k] * y_pitch, y_pitch, out + (size_t)a[k] * pp, pp, a[k + 1] - a[k], ys));
+    }
+    HYB_CHECK(cudaEventRecord(ctx->ev_out_free[b], ys));
+    ctx->async_parity ^= 1;
+    return HYB_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -670,6 +767,16 @@ int hyb_destroy(hyb_ctx* ctx) {
     for (auto& b : ctx->strip_f) b.release();
     ctx->wparts.release();
     ctx->wtot.release();
+    for (int b = 0; b < 2; ++b) {
+        ctx->ain[b].release();
+        ctx->aout[b].release();
+        for (cudaEvent_t ev : {ctx->ev_in_free[b], ctx->ev_out_free[b]})
+            if (ev) cudaEventDestroy(ev);
+        for (int k = 0; k < hyb_ctx::kMaxChunks; ++k) {
+            if (ctx->ev_ah2d[b][k]) cudaEventDestroy(ctx->ev_ah2d[b][k]);
+            if (ctx->ev_again[b][k]) cudaEventDestroy(ctx->ev_again[b][k]);
+        }
+    }
     ctx->mg_in.release();
     ctx->mg_out.release();
     if (ctx->host_w) cudaFreeHost(ctx->host_w);
@@ -694,6 +801,35 @@ int hyb_set_stream(hyb_ctx* ctx, void* stream) {
     if (!ctx) return HYB_EINVAL;
     CtxScope scope_(ctx);
     ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own;
+    return HYB_OK;
+}
+
+int hyb_set_async(hyb_ctx* ctx, int async_host) {
+    if (!ctx) return HYB_EINVAL;
+    CtxScope scope_(ctx);
+    if (ctx->async_host && !async_host) {  // leaving async mode: complete the pending calls
+        const int st = hyb_synchronize(ctx);
+        if (st) return st;
+    }
+    ctx->async_host = async_host != 0;
+    return HYB_OK;
+}
+
+int hyb_synchronize(hyb_ctx* ctx) {
+    if (!ctx) return HYB_EINVAL;
+    CtxScope scope_(ctx);
+    HYB_CHECK(cudaSetDevice(ctx->device));
+    // join the copy streams into the context stream first, so work the caller enqueues on that stream
+    // afterwards (or an event recorded there) is ordered after every pending call
+    HYB_CHECK(cudaEventRecord(ctx->ev_h2d[hyb_ctx::kMaxChunks - 1], ctx->copy));
+    HYB_CHECK(cudaStreamWaitEvent(ctx->stream, ctx->ev_h2d[hyb_ctx::kMaxChunks - 1], 0));
+    HYB_CHECK(cudaEventRecord(ctx->ev_gain[hyb_ctx::kMaxChunks - 1], ctx->copy2));
+    HYB_CHECK(cudaStreamWaitEvent(ctx->stream, ctx->ev_gain[hyb_ctx::kMaxChunks - 1], 0));
+    HYB_CHECK(cudaStreamSynchronize(ctx->stream));
+    for (hyb_ctx* p : ctx->peers) {
+        const int st = hyb_synchronize(p);
+        if (st) return fail(ctx, st, p->err);
+    }
     return HYB_OK;
 }
 
@@ -973,6 +1109,20 @@ int hyb_hybrid_u8(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int co
     if (!ctx) return HYB_EINVAL;
     CtxScope scope_(ctx);
     if (!ctx->peers.empty()) return hybrid_multi(ctx, g, pitch, rows, cols, smax, win, parts, y, y_pitch, stats);
+    if (ctx->async_host && !stats && parts == 1) {
+        cudaPointerAttributes pa{}, pb{};
+        const bool pinned = g && y && cudaPointerGetAttributes(&pa, g) == cudaSuccess &&
+                            cudaPointerGetAttributes(&pb, y) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+                            pb.type == cudaMemoryTypeHost;
+        cudaGetLastError();
+        int st;
+        if (pinned && !(st = check_smax(ctx, smax)) && !(st = check_win(ctx, win)) && !(st = check_dims(ctx, rows, cols)) &&
+            !(st = check_pitch(ctx, pitch, cols, "g")) && !(st = check_pitch(ctx, y_pitch, cols, "y"))) {
+            HYB_CHECK(cudaSetDevice(ctx->device));
+            return hybrid_host_async(ctx, g, pitch, rows, cols, smax, win, y, y_pitch);
+        }
+        if (pinned) return st;
+    }
     // Untimed calls on device buffers or pinned host buffers replay a cached CUDA graph.
     cudaPointerAttributes ga{}, ya{};
     const bool gok = g && cudaPointerGetAttributes(&ga, g) == cudaSuccess;

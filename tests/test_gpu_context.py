@@ -84,3 +84,32 @@ def test_mirror_uses_the_inputs_device_context():
             denoise.hybrid_denoise(g, denoise.FilterConfig(smax=7, wiener_window=3), ctx=fake)
     finally:
         fake.device = real_dev
+
+
+@pytest.mark.parametrize("shape", [(300, 420), (3000, 2900)])  # one-piece (fused kernel) and chunked pipelines
+def test_async_host_calls_pipeline_bit_exact(shape):
+    """hyb_set_async: calls on pinned host buffers return once enqueued; consecutive calls overlap (double-
+    buffered staging); after synchronize() every output equals the oracle, and the context returns to
+    synchronous behaviour."""
+    ctx = capi.Context(0)
+    ctx.set_exclusive(True)
+    rows, cols = shape
+    imgs = [torch.from_numpy(_img(rows, cols, 20 + i)).pin_memory() for i in range(5)]
+    outs = [torch.empty((rows, cols), dtype=torch.uint8).pin_memory() for _ in range(5)]
+    refs = [oracle.hybrid_threaded(g.numpy(), 9, 5)[0] for g in imgs]
+    ctx.set_async(True)
+    for rep in range(2):
+        for o in outs:
+            o.zero_()
+        for g, o in zip(imgs, outs):
+            capi.check(capi.lib.hyb_hybrid_u8(ctx.ptr, g.data_ptr(), cols, rows, cols, 9, 5, 1, o.data_ptr(), cols,
+                                              None), ctx.ptr)
+        ctx.synchronize()
+        for i, (o, r) in enumerate(zip(outs, refs)):
+            np.testing.assert_array_equal(o.numpy(), r, err_msg=f"rep {rep} image {i}")
+    ctx.set_async(False)
+    outs[0].zero_()
+    capi.check(capi.lib.hyb_hybrid_u8(ctx.ptr, imgs[0].data_ptr(), cols, rows, cols, 9, 5, 1, outs[0].data_ptr(), cols,
+                                      None), ctx.ptr)
+    np.testing.assert_array_equal(outs[0].numpy(), refs[0])  # synchronous again: complete on return
+    ctx.close()
