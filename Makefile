@@ -40,7 +40,7 @@ $(PGMTEST): tests/cpp/test_pgm.cpp $(HOSTLIB)
 # A/B variant of the same library (tools/ab.sh): make alt ALTDEF=-DHYB_SMALL_NT=256
 ALTDEF ?=
 alt: $(SRCS) $(HDRS)
-	$(NVCC) $(NVFLAGS) $(ALTDEF) -shared -o $(PKG)/libhybrid_cuda_alt.so $(SRCS) -lcufft -Xlinker -rpath,/usr/local/cuda/lib64 2> /dev/null
+	$(NVCC) $(NVFLAGS) $(ALTDEF) -shared -o $(PKG)/libhybrid_cuda_alt.so $(SRCS) -lcufft -Xlinker -rpath,/usr/local/cuda/lib64 2> build_alt.log || (grep -i error build_alt.log; exit 1)
 
 oracle:
 	$(MAKE) -C oracle --no-print-directory

@@ -195,7 +195,10 @@ __global__ void __launch_bounds__(K3T, 3)
 // growth kernel (k = 5..smax): tile-wise, all levels from shared memory
 // ------------------------------------------------------------------------------------------
 
-constexpr int GNT = 256;         // threads per growth CTA
+#ifndef HYB_GNT
+#define HYB_GNT 256
+#endif
+constexpr int GNT = HYB_GNT;     // threads per growth CTA
 
 constexpr int GHDR = 1536;       // mbarriers, tile coordinates, level counters, scan scratch
 
@@ -238,7 +241,19 @@ struct GrowCfg {
 #ifndef HYB_LEAN_DYN
 #define HYB_LEAN_DYN 0
 #endif
-using GrowWide = GrowCfg<9, 2, 8, 8192, true, 13>;
+#ifndef HYB_WIDE_MINB
+#define HYB_WIDE_MINB 2  // CTAs / SM
+#endif
+#ifndef HYB_WIDE_SLOTS
+#define HYB_WIDE_SLOTS 8  // tiles per batch
+#endif
+#ifndef HYB_WIDE_CAP
+#define HYB_WIDE_CAP 8192  // pooled queue capacity
+#endif
+#ifndef HYB_WIDE_CHUNK
+#define HYB_WIDE_CHUNK 13  // log2 of a dynamic claim
+#endif
+using GrowWide = GrowCfg<9, HYB_WIDE_MINB, HYB_WIDE_SLOTS, HYB_WIDE_CAP, true, HYB_WIDE_CHUNK>;
 #ifndef HYB_LEAN_SLOTS
 #define HYB_LEAN_SLOTS 8
 #endif
@@ -247,6 +262,7 @@ using GrowWide = GrowCfg<9, 2, 8, 8192, true, 13>;
 #endif
 using GrowLean = GrowCfg<7, 3, HYB_LEAN_SLOTS, 4096, HYB_LEAN_DYN != 0, 11>;
 static_assert(GrowWide::SLOTS <= 8 && GrowLean::SLOTS <= 8, "header layout");
+static_assert(GrowWide::SLOTS <= GNT / 32 && GrowLean::SLOTS <= GNT / 32, "queue build: one warp per slot");
 static_assert(GrowWide::CHUNK_SHIFT >= 11 && GrowLean::CHUNK_SHIFT >= 11, "chunk table sized for chunks >= 2048");
 
 template <class C>
