@@ -4,7 +4,7 @@ NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 -Xptxas -v -cudart static
 PKG := paper_2005_05371_b200
-SRCS := $(PKG)/csrc/tma_host.cu $(PKG)/csrc/amf.cu $(PKG)/csrc/wiener.cu $(PKG)/csrc/small.cu $(PKG)/csrc/stretch.cu $(PKG)/csrc/freq.cu $(PKG)/csrc/multi.cu $(PKG)/csrc/capi.cu $(PKG)/csrc/phantom.cpp
+SRCS := $(PKG)/csrc/tma_host.cu $(PKG)/csrc/amf.cu $(PKG)/csrc/wiener.cu $(PKG)/csrc/small.cu $(PKG)/csrc/stretch.cu $(PKG)/csrc/wstats.cu $(PKG)/csrc/freq.cu $(PKG)/csrc/multi.cu $(PKG)/csrc/capi.cu $(PKG)/csrc/phantom.cpp
 HDRS := $(PKG)/csrc/hyb_internal.cuh $(PKG)/csrc/tma.cuh $(PKG)/csrc/networks.cuh $(PKG)/csrc/amf_core.cuh $(PKG)/csrc/w1_core.cuh include/hybrid_cuda.h
 LIB := $(PKG)/libhybrid_cuda.so
 HOSTLIB := $(PKG)/libdenoise_cuda.so

@@ -76,6 +76,15 @@ def issue_roofline(kernel, counters, ms, sm_mhz):
             "source": "warp instructions per launch from profiles/ncu_counters.json, duration live"}
 
 
+# min/max lane operations per pixel of the zmin / zmed / zmax selection for a k x k window (SURVEY.md 8(d)
+# algorithmic work): k = 3 as the k = 3 kernel formulates it (10 column sorts reused by 3 outputs each +
+# 8 three-input min/max per u16x2 output pair word, 168 ops per 16 pixels = 10.5 word ops = 21 lane ops
+# per pixel); k >= 5: the pruned Batcher networks of tools/gen_networks.py, 2 ops per compare-exchange + 1
+# per one-sided op (k = 5: 96 CE + 22, 7: 281 + 46, 9: 641 + 78, 11: 1030 + 118, 13: 1856 + 166,
+# 15: 2546 + 222).
+AMF_OPS = {3: 21, 5: 214, 7: 608, 9: 1360, 11: 2178, 13: 3878, 15: 5314}
+
+
 def int_peak():
     """Measured VIMNMX.U16x2 throughput (tools/int_peak.cu on a B200, committed as profiles/int_peak.json)."""
     try:
@@ -455,20 +464,22 @@ def run_gpu(args, cfg, c):
         t_w = timed_local(wiener_only, k_stage) / k_stage
     kern = {"amf_ms": round(t_amf, 4), "wiener_ms": round(t_w, 4) if t_w else None}
 
-    # algorithmic work of the AMF: window-element visits sum_k reach(k) k^2 per pixel,
-    # from this rank's finalized_at histogram (the kernels' finalized_at is bit-exact vs the oracle,
-    # tests/test_gpu_parity.py); unresolved pixels (0) reached every level
-    visits = None
+    # algorithmic work of the AMF: for every window size k a pixel reaches, the min/max lane
+    # operations of a selection network giving zmin / zmed / zmax (AMF_OPS), summed from this rank's
+    # finalized_at histogram (the kernels' finalized_at is bit-exact vs the oracle, tests/test_gpu_parity.py;
+    # unresolved pixels (0) reached every level).  Element visits sum_k reach(k) k^2 are kept beside it.
+    visits = ops = None
     if slices == 1:
         fin = torch.empty((o_rows, cols), dtype=torch.uint8, device=dev)
         capi.check(lib.hyb_amf_u8(ctx.ptr, g0.data_ptr(), cols, a_rows, cols, rb, rb + o_rows, smax,
                                   f_scr[0].data_ptr(), cols, fin.data_ptr(), cols), ctx.ptr)
         torch.cuda.synchronize()
         hist = torch.bincount(fin.flatten().long(), minlength=256).cpu().numpy()
-        visits = 0
+        visits = ops = 0
         for k in range(3, smax + 1, 2):
             reach = int(hist[0]) + int(hist[k:].sum())  # finalised at >= k, or never
             visits += reach * k * k
+            ops = ops + reach * AMF_OPS[k] if (ops is not None and k in AMF_OPS) else None
         del fin
 
     # ---------------- e2e through the C ABI with pinned host buffers ----------------
@@ -594,18 +605,23 @@ def run_gpu(args, cfg, c):
             if w_issue:
                 issue["wiener"] = {k: w_issue[k] for k in ("achieved", "frac")}
 
-    # integer roofline of the AMF: algorithmic element visits / s vs the measured VIMNMX.U16x2 lane rate
+    # integer roofline of the AMF: algorithmic min/max lane operations / s vs the measured VIMNMX.U16x2
+    # lane rate (two 16-bit lanes per instruction)
     int_roof = None
     ip = int_peak()
-    if visits and ip:
-        ach = visits / (t_amf * 1e-3) / 1e9
+    if ops and ip:
+        ach = ops / (t_amf * 1e-3) / 1e9
         pk = ip["elem_per_s"] / 1e9
-        int_roof = {"bound": "integer issue (VIMNMX.U16x2)", "kernel": "amf (k3 + growth)",
-                    "achieved": round(ach, 1), "peak": round(pk, 1), "unit": "G window-element visits/s",
+        int_roof = {"bound": "integer ALU (VIMNMX.U16x2 lane min/max)", "kernel": "amf (k3 + growth)",
+                    "achieved": round(ach, 1), "peak": round(pk, 1), "unit": "G min/max lane-ops/s",
                     "frac": round(ach / pk, 4),
-                    "work_per_px": round(visits / px_local, 3),
-                    "work": "sum_k reach(k) * k^2 element visits per pixel (SURVEY.md 8(d)), from the "
-                            "finalized_at histogram of this input",
+                    "work_per_px": round(ops / px_local, 3),
+                    "work": "sum_k reach(k) * ops(k): min/max lane operations of a zmin/zmed/zmax selection "
+                            "network for every window size the pixel reaches (k = 3: shared 3-tall column "
+                            "sorts, 21 ops/px; k >= 5: the pruned Batcher networks of tools/gen_networks.py, "
+                            "214 / 608 / 1360 / 2178 ops at k = 5 / 7 / 9 / 11), reach(k) from the "
+                            "finalized_at histogram of this input; a 3-input min/max counts as 2 ops",
+                    "element_visits_per_px": round(visits / px_local, 3),
                     "peak_source": "profiles/int_peak.json (tools/int_peak.cu, " + ip.get("how", "") + ")"}
 
     cpu = None

@@ -109,6 +109,13 @@ int hyb_amf_batch_u8(hyb_ctx* ctx, const uint8_t* src, size_t src_pitch, size_t 
                      int n_slices, int rows, int cols, int smax, uint8_t* dst, size_t dst_pitch,
                      size_t dst_slice_stride);
 
+/* window_stats -- reference proj/src/adaptive_median.cpp:96-119 (proj/include/denoise/adaptive_median.hpp:16-24):
+ * per pixel the min, median (sorted index (k^2-1)/2) and max of its k x k window, edge replication.
+ * k odd >= 3 (HYB_EINVAL "window size must be an odd integer >= 3, got N").  The three output planes share
+ * out_pitch; any of them may be NULL (not computed). */
+int hyb_window_stats_u8(hyb_ctx* ctx, const uint8_t* src, size_t pitch, int rows, int cols, int k,
+                        uint8_t* zmin, uint8_t* zmed, uint8_t* zmax, size_t out_pitch);
+
 /* W1 local-Wiener noise statistics (replaces estimate_noise_variance, reference
  * proj/include/denoise/wiener.hpp:23, call site proj/src/pipeline.cpp:46-50).
  * Adds W = sum of V over rows [row_begin, row_end) of f to *noise_sum (host or device int64);

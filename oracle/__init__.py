@@ -31,6 +31,7 @@ def _load_oracle():
                                               P, c_size_t]
     lib.hyb_oracle_hybrid_u8.argtypes = [P, c_size_t, c_int, c_int, c_int, c_int, P, P, c_size_t, POINTER(c_int64)]
     lib.hyb_oracle_validate_smax.argtypes = [c_int]
+    lib.hyb_oracle_window_stats_u8.argtypes = [P, c_size_t, c_int, c_int, c_int, P, P, P, c_size_t]
     lib.hyb_oracle_contrast_stretch_u8.argtypes = [P, c_size_t, c_int, c_int, P, c_size_t]
     lib.oracle_make_phantom_u8.argtypes = [c_int, c_int, c_int, c_double, c_double, c_uint64, P, c_size_t]
     return lib
@@ -66,6 +67,7 @@ def ref():
         r.ref_amf_rows_u8.argtypes = [P, c_size_t, c_int, c_int, c_int, c_int, c_int, P, c_size_t, P, c_size_t]
         r.ref_amf_parallel_u8.argtypes = [P, c_size_t, c_int, c_int, c_int, c_int, c_int, c_int, P, c_size_t,
                                           POINTER(c_double)]
+        r.ref_window_stats_u8.argtypes = [P, c_size_t, c_int, c_int, c_int, P, P, P, c_size_t]
         r.ref_split_bands.argtypes = [c_int, c_int, c_int, c_int, POINTER(c_int)]
         r.ref_rng_uniform.argtypes = [c_uint64, c_int, POINTER(c_double)]
         r.ref_rng_normal.argtypes = [c_uint64, c_int, POINTER(c_double)]
@@ -97,6 +99,28 @@ def amf(img, smax, row_begin=0, row_end=None, finalized_at=False):
     if st:
         raise ValueError(f"oracle amf rejected smax={smax} range=[{row_begin},{row_end}) of {rows}")
     return (out, fin) if finalized_at else out
+
+
+def window_stats(img, k):
+    """(zmin, zmed, zmax) planes of the k x k windows (reference window_stats,
+    proj/src/adaptive_median.cpp:96-119)."""
+    img, p = _u8(img)
+    rows, cols = img.shape
+    out = [np.empty((rows, cols), np.uint8) for _ in range(3)]
+    st = lib().hyb_oracle_window_stats_u8(p, cols, rows, cols, k, *(o.ctypes.data for o in out), cols)
+    if st:
+        raise ValueError(f"window size must be an odd integer >= 3, got {k}")
+    return tuple(out)
+
+
+def ref_window_stats(img, k):
+    """The reference's own window_stats on k/255 doubles, mapped back to uint8."""
+    img, p = _u8(img)
+    rows, cols = img.shape
+    out = [np.empty((rows, cols), np.uint8) for _ in range(3)]
+    if ref().ref_window_stats_u8(p, cols, rows, cols, k, *(o.ctypes.data for o in out), cols):
+        raise ValueError(ref().ref_last_error().decode())
+    return tuple(out)
 
 
 def wiener_stats(f, win, row_begin=0, row_end=None):

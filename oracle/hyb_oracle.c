@@ -35,6 +35,39 @@ static int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v
 int hyb_oracle_validate_smax(int smax) { return (smax <= 1 || smax % 2 == 0) ? HYB_EINVAL : HYB_OK; }
 
 /*
+ * window_stats, reference proj/src/adaptive_median.cpp:96-119: per pixel the min, the median
+ * (sorted index (k*k-1)/2, :52-56 via median_of) and the max of the k x k window, coordinates
+ * clamped (edge replication, :20-41).  k odd >= 3 (:97-100).  Outputs nullable; one pitch.
+ * 256-bin counting per window, exact for uint8 samples.
+ */
+int hyb_oracle_window_stats_u8(const uint8_t* src, size_t spitch, int rows, int cols, int k,
+                               uint8_t* zmin, uint8_t* zmed, uint8_t* zmax, size_t opitch) {
+    if (k < 3 || k % 2 == 0 || rows < 1 || cols < 1) return HYB_EINVAL;
+    const int rk = k / 2, m = (k * k - 1) / 2;
+    uint32_t hist[256];
+    for (int r = 0; r < rows; ++r) {
+        for (int c = 0; c < cols; ++c) {
+            for (int i = 0; i < 256; ++i) hist[i] = 0;
+            for (int dr = -rk; dr <= rk; ++dr)
+                for (int dc = -rk; dc <= rk; ++dc)
+                    ++hist[src[(size_t)clampi(r + dr, 0, rows - 1) * spitch + (size_t)clampi(c + dc, 0, cols - 1)]];
+            int lo = 0, hi = 255, md = -1, acc = 0;
+            while (!hist[lo]) ++lo;
+            while (!hist[hi]) --hi;
+            for (int v = lo; v <= hi && md < 0; ++v) {
+                acc += (int)hist[v];
+                if (acc > m) md = v;
+            }
+            const size_t o = (size_t)r * opitch + (size_t)c;
+            if (zmin) zmin[o] = (uint8_t)lo;
+            if (zmed) zmed[o] = (uint8_t)md;
+            if (zmax) zmax[o] = (uint8_t)hi;
+        }
+    }
+    return HYB_OK;
+}
+
+/*
  * Adaptive median over rows [row_begin, row_end) of src (rows x cols, pitch
  * spitch).  Restates reference proj/src/adaptive_median.cpp:123-215:
  *   - windows k = 3, 5, ..., smax over the PRISTINE input (:40-50, stats never

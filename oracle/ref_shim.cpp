@@ -113,6 +113,17 @@ int ref_amf_parallel_u8(const uint8_t* src, size_t pitch, int rows, int cols, in
     });
 }
 
+// window_stats (reference proj/include/denoise/adaptive_median.hpp:24): zmin / zmed / zmax planes.
+int ref_window_stats_u8(const uint8_t* src, size_t pitch, int rows, int cols, int k, uint8_t* zmin,
+                        uint8_t* zmed, uint8_t* zmax, size_t opitch) {
+    return guarded([&] {
+        denoise::WindowStats ws = denoise::window_stats(to_image(src, pitch, rows, cols), k);
+        from_image(ws.zmin, zmin, opitch);
+        from_image(ws.zmed, zmed, opitch);
+        from_image(ws.zmax, zmax, opitch);
+    });
+}
+
 // split_bands geometry (reference proj/src/tiling.cpp:10-45): 4 ints per band.
 int ref_split_bands(int rows, int cols, int parts, int halo, int* out) {
     return guarded([&] {

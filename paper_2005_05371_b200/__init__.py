@@ -8,7 +8,7 @@ from .capi import CudaError, InvalidArgument, make_phantom  # noqa: F401
 from .denoise import (  # noqa: F401
     FilterConfig, HybridResult, adaptive_median_parallel, adaptive_median_rows,
     adaptive_median_serial, hybrid_denoise, hybrid_denoise_batch, split_bands, validate_config,
-    validate_smax, wiener_local,
+    validate_smax, wiener_local, window_stats, WindowStats,
 )
 
 from .configs import CONFIGS  # noqa: F401  (BASELINE.json configs)

@@ -25,7 +25,7 @@ EXPORTED = (
     "hyb_create", "hyb_create_multi", "hyb_context_devices", "hyb_destroy", "hyb_set_stream", "hyb_set_exclusive", "hyb_set_async", "hyb_synchronize", "hyb_last_error", "hyb_kernel_launches",
     "hyb_validate_smax", "hyb_validate_config", "hyb_amf_u8", "hyb_amf_batch_u8",
     "hyb_wiener_stats_u8", "hyb_wiener_gain_u8", "hyb_wiener_u8", "hyb_hybrid_u8",
-    "hyb_hybrid_batch_u8", "hyb_contrast_stretch_u8", "hyb_hybrid_stretch_u8",
+    "hyb_hybrid_batch_u8", "hyb_window_stats_u8", "hyb_contrast_stretch_u8", "hyb_hybrid_stretch_u8",
     "hyb_wiener_freq_f64", "hyb_contrast_stretch_f64", "hyb_noise_robust_f64", "hyb_noise_reference_f64", "hyb_make_phantom_u8",
 )
 
@@ -77,6 +77,7 @@ def _load():
         "hyb_wiener_u8": (c_int, [P, P, c_size_t, c_int, c_int, c_int, P, c_size_t, Pi64]),
         "hyb_hybrid_u8": (c_int, [P, P, c_size_t, c_int, c_int, c_int, c_int, c_int, P, c_size_t,
                                   POINTER(HybStats)]),
+        "hyb_window_stats_u8": (c_int, [P, P, c_size_t, c_int, c_int, c_int, P, P, P, c_size_t]),
         "hyb_hybrid_batch_u8": (c_int, [P, P, c_size_t, c_size_t, c_int, c_int, c_int, c_int, c_int, P,
                                         c_size_t, c_size_t, Pi64]),
         "hyb_contrast_stretch_u8": (c_int, [P, P, c_size_t, c_int, c_int, P, c_size_t]),

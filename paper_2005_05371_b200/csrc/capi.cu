@@ -1314,6 +1314,49 @@ int hyb_contrast_stretch_u8(hyb_ctx* ctx, const uint8_t* src, size_t pitch, int 
     return HYB_OK;
 }
 
+int hyb_window_stats_u8(hyb_ctx* ctx, const uint8_t* src, size_t pitch, int rows, int cols, int k, uint8_t* zmin,
+                        uint8_t* zmed, uint8_t* zmax, size_t out_pitch) {
+    if (!ctx) return HYB_EINVAL;
+    CtxScope scope_(ctx);
+    int st;
+    if (k < 3 || k % 2 == 0)  // proj/src/adaptive_median.cpp:97-100
+        return fail(ctx, HYB_EINVAL, "window size must be an odd integer >= 3, got " + std::to_string(k));
+    if ((st = check_dims(ctx, rows, cols)) || (st = check_pitch(ctx, pitch, cols, "src")) ||
+        (st = check_pitch(ctx, out_pitch, cols, "out")))
+        return st;
+    if (!src) return fail(ctx, HYB_EINVAL, "null image pointer");
+    HYB_CHECK(cudaSetDevice(ctx->device));
+    const size_t pp = round_pitch(cols);
+    const uint8_t* s = src;
+    size_t sp = pitch;
+    if (!is_device_ptr(src)) {
+        HYB_CHECK(ctx->in.ensure(pp * rows));
+        HYB_CHECK(copy2d(ctx, ctx->in.ptr, pp, src, pitch, cols, rows));
+        s = ctx->in.ptr;
+        sp = pp;
+    }
+    // device outputs are written in place; host ones go through three planes of ctx->out (pitch pp)
+    uint8_t* outs[3] = {zmin, zmed, zmax};
+    bool staged[3] = {false, false, false};
+    bool any_staged = false;
+    for (int i = 0; i < 3; ++i) staged[i] = outs[i] && !is_device_ptr(outs[i]), any_staged |= staged[i];
+    if (any_staged) HYB_CHECK(ctx->out.ensure(3 * pp * rows));
+    uint8_t* d[3];
+    size_t dp = out_pitch;
+    if (any_staged) dp = pp;
+    for (int i = 0; i < 3; ++i) d[i] = staged[i] ? ctx->out.ptr + (size_t)i * pp * rows : outs[i];
+    if (any_staged && dp != out_pitch) {
+        // one pitch per launch: with mixed host / device outputs, stage the device ones too
+        for (int i = 0; i < 3; ++i)
+            if (outs[i] && !staged[i]) staged[i] = true, d[i] = ctx->out.ptr + (size_t)i * pp * rows;
+    }
+    HYB_CHECK(hyb::launch_window_stats(s, sp, rows, cols, k, d[0], d[1], d[2], dp, ctx->stream));
+    for (int i = 0; i < 3; ++i)
+        if (staged[i]) HYB_CHECK(copy2d(ctx, outs[i], out_pitch, d[i], dp, cols, rows));
+    if (any_staged || s != src) HYB_CHECK(cudaStreamSynchronize(ctx->stream));
+    return HYB_OK;
+}
+
 int hyb_hybrid_stretch_u8(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int cols, int smax, int win,
                           int parts, uint8_t* y, size_t y_pitch, hyb_stats* stats) {
     if (!ctx) return HYB_EINVAL;

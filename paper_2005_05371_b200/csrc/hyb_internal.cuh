@@ -150,6 +150,10 @@ cudaError_t launch_small(const SmallPlan& pl, const SmallBufs& bufs, int rows, i
 cudaError_t launch_contrast_stretch(const uint8_t* src, size_t spitch, int rows, int cols, uint8_t* dst,
                                     size_t dpitch, unsigned* mm, cudaStream_t stream);
 
+// window_stats (wstats.cu): min / median / max planes of the k x k windows; outputs nullable.
+cudaError_t launch_window_stats(const uint8_t* src, size_t pitch, int rows, int cols, int k, uint8_t* zmin,
+                                uint8_t* zmed, uint8_t* zmax, size_t opitch, cudaStream_t stream);
+
 // Frequency-domain Wiener + noise estimates (freq.cu, doubles like the reference).
 struct FreqWork {
     unsigned long long plan_f = 0, plan_i = 0;  // cufftHandle

@@ -196,6 +196,29 @@ def adaptive_median_parallel(image, config: FilterConfig, ctx=None):
 
 # ---------------------------------------------------------------- W1 Wiener
 
+@dataclass
+class WindowStats:
+    """reference WindowStats (proj/include/denoise/adaptive_median.hpp:16-22): uint8 planes."""
+    zmin: object
+    zmax: object
+    zmed: object
+    k: int = 0
+
+
+def window_stats(image, k: int, ctx=None) -> WindowStats:
+    """window_stats -- reference proj/src/adaptive_median.cpp:96-119: per-pixel min / median / max of the
+    k x k window (edge replication), computed on the device (hyb_window_stats_u8)."""
+    if k < 3 or k % 2 == 0:
+        raise InvalidArgument(f"window size must be an odd integer >= 3, got {k}")
+    rows, cols = _shape(image)
+    outs = [_empty_like(image, rows, cols) for _ in range(3)]
+    sp, spitch = capi.buf(image)
+    ptrs = [capi.buf(o)[0] for o in outs]
+    c = _ctx(ctx, image, *outs)
+    check(lib.hyb_window_stats_u8(c, sp, spitch, rows, cols, k, ptrs[0], ptrs[1], ptrs[2], cols), c)
+    return WindowStats(zmin=outs[0], zmax=outs[2], zmed=outs[1], k=k)
+
+
 def wiener_local(f, win: int = 3, ctx=None):
     """W1 local-statistics Wiener on a whole image; returns (y, W) with W = sum of V."""
     rows, cols = _shape(f)

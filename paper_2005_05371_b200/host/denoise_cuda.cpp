@@ -168,6 +168,30 @@ void adaptive_median_rows(const Image& src, int smax, int row_begin, int row_end
 
 }  // namespace detail
 
+WindowStats window_stats(const Image& image, int k) {
+    if (k < 3 || k % 2 == 0)  // proj/src/adaptive_median.cpp:97-100
+        throw std::invalid_argument("window size must be an odd integer >= 3, got " + std::to_string(k));
+    const int rows = image.rows(), cols = image.cols();
+    const Coded in = encode_for_amf(image);  // order statistics commute with the rank coding
+    std::vector<uint8_t> planes(3 * (std::size_t)rows * cols);
+    uint8_t* zmin = planes.data();
+    uint8_t* zmed = zmin + (std::size_t)rows * cols;
+    uint8_t* zmax = zmed + (std::size_t)rows * cols;
+    hyb_ctx* ctx = context();
+    check(hyb_window_stats_u8(ctx, in.px.data(), cols, rows, cols, k, zmin, zmed, zmax, cols), ctx);
+    WindowStats ws;
+    ws.k = k;
+    ws.zmin = Image(rows, cols);
+    ws.zmed = Image(rows, cols);
+    ws.zmax = Image(rows, cols);
+    for (std::size_t i = 0; i < (std::size_t)rows * cols; ++i) {
+        ws.zmin.pixels()[i] = in.decode(zmin[i]);
+        ws.zmed.pixels()[i] = in.decode(zmed[i]);
+        ws.zmax.pixels()[i] = in.decode(zmax[i]);
+    }
+    return ws;
+}
+
 Image adaptive_median_serial(const Image& image, int smax) {
     validate_smax(smax);
     Image out;

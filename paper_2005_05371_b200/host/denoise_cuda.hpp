@@ -80,6 +80,16 @@ int default_device();
 /// validate_config -- proj/src/parallel.cpp:16-25.
 void validate_config(const FilterConfig& config);
 
+/// WindowStats / window_stats -- proj/include/denoise/adaptive_median.hpp:16-24: per-pixel min / median /
+/// max planes of the k x k window (edge replication), on the GPU (hyb_window_stats_u8).
+struct WindowStats {
+    Image zmin;
+    Image zmax;
+    Image zmed;
+    int k = 0;
+};
+WindowStats window_stats(const Image& image, int k);
+
 /// adaptive_median_serial -- proj/include/denoise/adaptive_median.hpp:35.
 Image adaptive_median_serial(const Image& image, int smax);
 

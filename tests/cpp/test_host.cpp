@@ -19,6 +19,7 @@ int hyb_make_phantom_u8(int, int, int, double, double, uint64_t, uint8_t*, size_
 int hyb_oracle_wiener_stats_u8(const uint8_t*, size_t, int, int, int, int, int, int64_t*);
 int hyb_oracle_wiener_gain_u8(const uint8_t*, size_t, int, int, int, int, int, int64_t, int64_t, uint8_t*, size_t);
 int hyb_oracle_contrast_stretch_u8(const uint8_t*, size_t, int, int, uint8_t*, size_t);
+int hyb_oracle_window_stats_u8(const uint8_t*, size_t, int, int, int, uint8_t*, uint8_t*, uint8_t*, size_t);
 }
 
 using namespace denoise_cuda;
@@ -78,6 +79,46 @@ int main() {
         CHECK(std::string(e.what()).find("odd integer > 1") != std::string::npos);
     }
 
+    // window_stats on a 3x3 ramp (proj/tests/test_adaptive_median.cpp:26-38): off-grid values, rank-coded
+    {
+        Image img = Image::from_pixels(3, 3, {0.1, 0.2, 0.3, 0.4, 0.5, 0.6, 0.7, 0.8, 0.9});
+        WindowStats ws = window_stats(img, 3);
+        CHECK(ws.k == 3);
+        CHECK(ws.zmin.at(1, 1) == 0.1);
+        CHECK(ws.zmed.at(1, 1) == 0.5);
+        CHECK(ws.zmax.at(1, 1) == 0.9);
+        CHECK(ws.zmin.at(0, 0) == 0.1);
+        CHECK(ws.zmed.at(0, 0) == 0.2);
+        CHECK(ws.zmax.at(0, 0) == 0.5);
+    }
+    // constants and invalid sizes (:40-48)
+    {
+        Image flat(6, 5, 0.25);
+        WindowStats ws = window_stats(flat, 5);
+        CHECK(ws.zmin == flat);
+        CHECK(ws.zmed == flat);
+        CHECK(ws.zmax == flat);
+        CHECK_THROWS_AS(window_stats(flat, 4), std::invalid_argument);
+        CHECK_THROWS_AS(window_stats(flat, 1), std::invalid_argument);
+    }
+    // ordering invariant on random data (:50-59), and the planes equal the oracle's
+    {
+        Image img = random_grid_image(21, 17, 99, 0.1);
+        std::vector<uint8_t> in = to_u8(img);
+        for (int k : {3, 5, 7, 9}) {
+            WindowStats ws = window_stats(img, k);
+            std::vector<uint8_t> o[3];
+            for (auto& v : o) v.resize(img.size());
+            hyb_oracle_window_stats_u8(in.data(), 17, 21, 17, k, o[0].data(), o[1].data(), o[2].data(), 17);
+            for (std::size_t i = 0; i < img.size(); ++i) {
+                CHECK(ws.zmin.pixels()[i] <= ws.zmed.pixels()[i]);
+                CHECK(ws.zmed.pixels()[i] <= ws.zmax.pixels()[i]);
+            }
+            CHECK(ws.zmin == from_u8(o[0].data(), 21, 17));
+            CHECK(ws.zmed == from_u8(o[1].data(), 21, 17));
+            CHECK(ws.zmax == from_u8(o[2].data(), 21, 17));
+        }
+    }
     // constants are a fixed point (:61-65)
     {
         Image flat(9, 9, 0.7);

@@ -9,7 +9,8 @@ reference's results.  The W1 Wiener has no reference implementation: wiener_kat.
 hand-checkable cases computed here with exact rational arithmetic (fractions.Fraction),
 independently of the C oracle.
 
-    python tests/golden/make_golden.py
+    python tests/golden/make_golden.py               (every fixture)
+    python tests/golden/make_golden.py window_stats  (window_stats_reference.npz only)
 """
 import json
 import os
@@ -136,6 +137,26 @@ def build_wiener():
     return cases
 
 
+def build_window_stats():
+    """window_stats planes from the reference (proj/src/adaptive_median.cpp:96-119): its unit-test images
+    (proj/tests/test_adaptive_median.cpp:26-59, rank-compressed / quantised) and random S&P images."""
+    cases = {}
+
+    def add(name, img, ks):
+        cases[f"{name}/input"] = img
+        for k in ks:
+            zmin, zmed, zmax = oracle.ref_window_stats(img, k)
+            cases[f"{name}/k{k}"] = np.stack([zmin, zmed, zmax])
+
+    add("kat_ramp3", np.arange(1, 10, dtype=np.uint8).reshape(3, 3), [3, 5])
+    add("kat_flat6x5", np.full((6, 5), 64, np.uint8), [5])
+    add("random_21x17_99", oracle.ref_random_image(21, 17, 99, 0.0, 100), [3, 5, 7])
+    for i, (rows, cols) in enumerate([(1, 1), (1, 40), (40, 1), (33, 70), (64, 48)]):
+        img = oracle.ref_random_image(rows, cols, 900 + i, 0.3, 950 + i)
+        add(f"sp_{rows}x{cols}", img, [3, 7, 11])
+    return cases
+
+
 def phantom_pins():
     """Reference Rng64 streams used by the BASELINE phantom generator (checked in test_phantom.py)."""
     return {
@@ -149,8 +170,13 @@ def phantom_pins():
 def main():
     if not oracle.ref_available():
         sys.exit("oracle/_ref/libref.so missing: run `make -C oracle` where /root/reference exists")
+    if sys.argv[1:] == ["window_stats"]:  # only the window_stats fixture
+        np.savez_compressed(os.path.join(HERE, "window_stats_reference.npz"), **build_window_stats())
+        print("wrote window_stats_reference.npz")
+        return
     amf = build_amf()
     np.savez_compressed(os.path.join(HERE, "amf_reference.npz"), **amf)
+    np.savez_compressed(os.path.join(HERE, "window_stats_reference.npz"), **build_window_stats())
     with open(os.path.join(HERE, "wiener_kat.json"), "w") as fh:
         json.dump(build_wiener(), fh)
     with open(os.path.join(HERE, "rng_pins.json"), "w") as fh:

@@ -222,3 +222,42 @@ def test_contrast_stretch_endpoints_order_and_rounding():
         assert np.max(np.abs(out - ref)) <= 0.5 + 1e-9
         exact = (510 * (img.astype(int) - lo) + (hi - lo)) // (2 * (hi - lo))
         np.testing.assert_array_equal(out, exact)
+
+
+# ---------------------------------------------------------------- window_stats
+
+def ws_cases():
+    gold = np.load(os.path.join(GOLD, "window_stats_reference.npz"))
+    for key in gold.files:
+        if "/k" in key:
+            name, k = key.split("/k")
+            yield name, gold[f"{name}/input"], int(k), gold[key]
+
+
+def test_oracle_window_stats_matches_reference_golden():
+    n = 0
+    for name, img, k, planes in ws_cases():
+        got = np.stack(oracle.window_stats(img, k))
+        np.testing.assert_array_equal(got, planes, err_msg=f"{name} k={k}")
+        n += 1
+    assert n >= 20
+
+
+def test_oracle_window_stats_kats():
+    # proj/tests/test_adaptive_median.cpp:26-48 (rank-compressed ramp), invalid sizes
+    zmin, zmed, zmax = oracle.window_stats(np.arange(1, 10, dtype=np.uint8).reshape(3, 3), 3)
+    assert (zmin[1, 1], zmed[1, 1], zmax[1, 1]) == (1, 5, 9)
+    assert (zmin[0, 0], zmed[0, 0], zmax[0, 0]) == (1, 2, 5)
+    for k in (4, 1):
+        with pytest.raises(ValueError):
+            oracle.window_stats(np.zeros((6, 5), np.uint8), k)
+
+
+@pytest.mark.skipif(not oracle.ref_available(), reason="oracle/_ref not built (no /root/reference)")
+@pytest.mark.parametrize("k", [3, 5, 9, 13])
+def test_oracle_window_stats_live_vs_reference(k):
+    rng = np.random.default_rng(k)
+    img = rng.integers(0, 256, size=(37, 45), dtype=np.uint8)
+    img[rng.random(img.shape) < 0.2] = 255
+    for a, b in zip(oracle.window_stats(img, k), oracle.ref_window_stats(img, k)):
+        np.testing.assert_array_equal(a, b)
