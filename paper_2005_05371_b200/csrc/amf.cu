@@ -338,10 +338,14 @@ __global__ void __launch_bounds__(GNT, C::MINB) amf_grow_kernel(const __grid_con
 // written once; no bitmap, no records, no second launch.  Batches are claimed from a global counter, so
 // SMs that meet cheap batches take more.  Tile geometry: R <= 16 (smax <= 33), so the k = 3 byte-tile
 // layout (CP = 16, BS = 160) is the growth tile's.
-template <int NETMAX_, int MINB_, int BT_, int NSET_>
+template <int NETMAX_, int MINB_, int BT_, int NSET_, int CAP_>
 struct FusedCfg {
     static constexpr int NETMAX = NETMAX_, MINB = MINB_, BT = BT_;
     static constexpr int NSET = NSET_;  // slot sets: 2 = the next batch's tiles load while this one computes
+    // growth queue capacity (entries per buffer); below BT * 4096 the k = 3 pass runs tile by tile and the
+    // growth runs whenever the queue could overflow on the next tile (and at the batch end)
+    static constexpr int CAP = CAP_;
+    static constexpr bool CAPPED = CAP_ < BT_ * TW * TH;
 };
 // Measured (config 2 / 3 / 4 AMF ms): one slot set with 3 / 4 tiles per batch 0.182 / 0.270 / 2.26; two sets
 // (the next batch's tiles load during this one) with 2 / 3 tiles 0.197 / 0.286 / 2.47 -- the growth pool size
@@ -355,10 +359,19 @@ struct FusedCfg {
 #ifndef HYB_FUSED_NSET
 #define HYB_FUSED_NSET 1
 #endif
-using FusedWide = FusedCfg<9, 2, HYB_FUSED_BT_WIDE, HYB_FUSED_NSET>;  // k = 9 network (~115 registers): 2 CTAs / SM
-using FusedLean = FusedCfg<7, 3, HYB_FUSED_BT_LEAN, HYB_FUSED_NSET>;  // networks to k = 7, radix above: 3 CTAs / SM
+#ifndef HYB_FUSED_CAP_WIDE
+#define HYB_FUSED_CAP_WIDE (HYB_FUSED_BT_WIDE * TW * TH)
+#endif
+#ifndef HYB_FUSED_CAP_LEAN
+#define HYB_FUSED_CAP_LEAN (HYB_FUSED_BT_LEAN * TW * TH)
+#endif
+// k = 9 network (~115 registers): 2 CTAs / SM
+using FusedWide = FusedCfg<9, 2, HYB_FUSED_BT_WIDE, HYB_FUSED_NSET, HYB_FUSED_CAP_WIDE>;
+// networks to k = 7, radix above: 3 CTAs / SM
+using FusedLean = FusedCfg<7, 3, HYB_FUSED_BT_LEAN, HYB_FUSED_NSET, HYB_FUSED_CAP_LEAN>;
 static_assert(FusedWide::BT * FusedWide::NSET <= 16 && FusedLean::BT * FusedLean::NSET <= 16, "header layout");
 static_assert(FusedWide::BT <= 8 && FusedLean::BT <= 8, "3-bit queue slots");
+static_assert(FusedWide::CAP >= TW * TH && FusedLean::CAP >= TW * TH, "one tile's failures fit the queue");
 
 constexpr int FHDR = 1024;  // mbarriers [16], tile info [16][4], level counters [128], batch claims [2]
 
@@ -376,8 +389,8 @@ struct FArgs {
 
 template <bool FIN, class C>
 inline size_t fused_smem(const GGeo& g) {  // header, tile sets, k = 3 staging (+ finalized_at), two queues
-    return FHDR + (size_t)C::NSET * C::BT * g.b_bytes + (size_t)NW * (FIN ? 2 : 1) * WPIX +
-           2 * (size_t)C::BT * (TW * TH) * 2 + 128;
+    return FHDR + (size_t)C::NSET * C::BT * g.b_bytes + (size_t)NW * (FIN ? 2 : 1) * WPIX + 2 * (size_t)C::CAP * 2 +
+           128;
 }
 
 template <bool FIN, class C>
@@ -394,7 +407,7 @@ __global__ void __launch_bounds__(NT, C::MINB) amf_fused_kernel(const __grid_con
     uint8_t* slots = smem + FHDR;                           // [NSET][BT][geo.b_bytes]
     uint8_t* stage = slots + (size_t)NSET * BT * geo.b_bytes;  // [NW][1 + FIN][WPIX] k = 3 output / finalized_at
     uint16_t* Q0 = reinterpret_cast<uint16_t*>(stage + NW * (FIN ? 2 : 1) * WPIX);
-    uint16_t* Q1 = Q0 + BT * TW * TH;
+    uint16_t* Q1 = Q0 + C::CAP;
     const int tid = threadIdx.x, warp = tid >> 5;
     const int per_slice = a.tiles_x * a.tiles_y;
     const int ntiles = per_slice * a.n_slices;
@@ -447,9 +460,15 @@ __global__ void __launch_bounds__(NT, C::MINB) amf_fused_kernel(const __grid_con
             replicate_edges<NT>(bufs + (size_t)i * geo.b_bytes, geo.BS, max(0, -sx0), min(geo.BS, a.cols - sx0),
                                 max(0, -sy0), min(geo.BH, a.rows - sy0), 0, geo.BH, geo.R);
         }
-        // ---- k = 3 on every pixel of the batch: f stored, level-A failures queued ----
-        for (int j = warp; j < nt * NW; j += NW) {
-            const int i = j / NW, sub = j % NW;
+        // ---- k = 3 on every pixel of the batch: f stored, level-A failures queued; growth k = 5..smax over
+        //      the pooled failures, from the resident tiles ----
+        auto out = [&](int sl, int pix, uint8_t v, int k) {
+            const int* ti = tset + 4 * sl;
+            const size_t row = (size_t)(ti[1] - a.row_begin + (pix >> 7));
+            a.dst[(size_t)ti[2] * a.dslice + row * a.dpitch + ti[0] + (pix & 127)] = v;
+            if (FIN) a.fin[(size_t)ti[2] * a.fslice + row * a.fpitch + ti[0] + (pix & 127)] = (uint8_t)k;
+        };
+        auto k3 = [&](int i, int sub) {
             const int* ti = tset + 4 * i;
             const int x0 = ti[0], y0 = ti[1], z = ti[2];
             const uint8_t* B = bufs + (size_t)i * geo.b_bytes + (size_t)(geo.R - 1) * geo.BS;  // row 0 = y0 - 1
@@ -457,21 +476,29 @@ __global__ void __launch_bounds__(NT, C::MINB) amf_fused_kernel(const __grid_con
                           a.dst + (size_t)z * a.dslice + (size_t)(y0 - a.row_begin) * a.dpitch + x0, a.dpitch,
                           FIN ? a.fin + (size_t)z * a.fslice + (size_t)(y0 - a.row_begin) * a.fpitch + x0 : nullptr,
                           a.fpitch, a.row_end - y0, a.cols - x0, grow ? Q0 : nullptr, qcount, (uint32_t)i << 12);
+        };
+        if constexpr (!C::CAPPED) {
+            for (int j = warp; j < nt * NW; j += NW) k3(j / NW, j % NW);
+            __syncthreads();
+            const int total = qcount[0];
+            if (grow && total > 0) grow_levels<FIN, NT, decltype(out), C::NETMAX>(bufs, geo, Q0, Q1, qcount, total, a.smax, out);
+            __syncthreads();
+            if (tid < MAX_LEVELS) qcount[tid] = 0;
+        } else {
+            // tile by tile (one strip per warp); the pooled growth runs when the next tile's failures might
+            // not fit, and at the batch end
+            for (int i = 0; i < nt; ++i) {
+                k3(i, warp);
+                __syncthreads();
+                const int total = qcount[0];
+                if (grow && total > 0 && (i == nt - 1 || total > C::CAP - TW * TH)) {
+                    grow_levels<FIN, NT, decltype(out), C::NETMAX>(bufs, geo, Q0, Q1, qcount, total, a.smax, out);
+                    if (tid < MAX_LEVELS) qcount[tid] = 0;
+                    __syncthreads();
+                }
+            }
+            if (!grow && tid == 0) qcount[0] = 0;
         }
-        __syncthreads();
-        // ---- growth k = 5..smax over the batch's pooled failures, from the resident tiles ----
-        const int total = qcount[0];
-        if (grow && total > 0) {
-            auto out = [&](int sl, int pix, uint8_t v, int k) {
-                const int* ti = tset + 4 * sl;
-                const size_t row = (size_t)(ti[1] - a.row_begin + (pix >> 7));
-                a.dst[(size_t)ti[2] * a.dslice + row * a.dpitch + ti[0] + (pix & 127)] = v;
-                if (FIN) a.fin[(size_t)ti[2] * a.fslice + row * a.fpitch + ti[0] + (pix & 127)] = (uint8_t)k;
-            };
-            grow_levels<FIN, NT, decltype(out), C::NETMAX>(bufs, geo, Q0, Q1, qcount, total, a.smax, out);
-        }
-        __syncthreads();
-        if (tid < MAX_LEVELS) qcount[tid] = 0;
     }
     // the last CTA resets the claim counter for the next launch
     if (tid == 0) {

@@ -67,6 +67,9 @@ struct hyb_ctx {
     DevBuf in, out, fin, f, wsum;      // staging / scratch
     DevBuf sbar;                       // fused small-image kernel: grid-barrier words (zeroed once), stamps
     DevBuf mm, ys;                     // contrast stretch: min / max scratch, staged hybrid output
+    DevBuf mmtot, mmparts;             // multi-device stretch: combined range, gathered partial ranges
+    unsigned* stretch_mm = nullptr;    // hyb_hybrid_stretch_u8 in progress: the gains fold y's range here
+    bool stretch_fused = false;        // ... and they did (else the stretch runs its own min / max pass)
     DevBuf fin64, fout64, fref64, fsc;  // frequency Wiener: staged doubles, scalar results
     hyb::FreqWork freq;
     bool small_used = false;           // the last hybrid call ran the fused kernel
@@ -102,7 +105,7 @@ struct hyb_ctx {
     DevBuf ain[2], aout[2];
     cudaEvent_t ev_in_free[2] = {}, ev_out_free[2] = {};
     cudaEvent_t ev_ah2d[2][16] = {}, ev_again[2][16] = {};
-    cudaEvent_t ev_stats = nullptr, ev_done = nullptr, ev_start = nullptr;
+    cudaEvent_t ev_stats = nullptr, ev_done = nullptr, ev_start = nullptr, ev_gainx = nullptr;
     static constexpr int kMaxChunks = 16;
     cudaEvent_t ev_h2d[kMaxChunks] = {}, ev_gain[kMaxChunks] = {};
 };
@@ -314,7 +317,9 @@ int hybrid_device(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int co
         if (timed) HYB_CHECK(cudaEventRecord(ctx->ev[1], ctx->stream));
         hyb::Plane w{ctx->f.ptr, fp, 0, y, ypitch, 0, rows, cols, 0, rows, 1};
         HYB_CHECK(hyb::launch_wiener_stats(w, win, W, ctx->stream));
-        HYB_CHECK(hyb::launch_wiener_gain(w, win, reinterpret_cast<const long long*>(W), P, ctx->stream));
+        HYB_CHECK(hyb::launch_wiener_gain(w, win, reinterpret_cast<const long long*>(W), P, ctx->stream,
+                                          ctx->stretch_mm));
+        ctx->stretch_fused = ctx->stretch_mm != nullptr;
     } else {
         // split_bands geometry (reference proj/src/tiling.cpp:23-32) with halo rA + rW
         const int h = rA + rW;
@@ -361,8 +366,9 @@ int hybrid_device(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int co
             hyb::Plane w{ctx->strip_f[i].ptr, sp, 0, y + (size_t)t.start * ypitch, ypitch, 0,
                          t.fa + t.core + t.fb, cols, t.fa, t.fa + t.core, 1};
             HYB_CHECK(hyb::launch_wiener_gain(w, win, reinterpret_cast<const long long*>(W), P,
-                                              ctx->stream));
+                                              ctx->stream, ctx->stretch_mm));
         }
+        ctx->stretch_fused = ctx->stretch_mm != nullptr;
     }
     if (timed) HYB_CHECK(cudaEventRecord(ctx->ev[2], ctx->stream));
     return HYB_OK;
@@ -469,8 +475,12 @@ int ptr_device(const void* p) {
 //      store to (its own, or a peer's over NVLink), else staged and copied out.
 // The caller's stream (ctx->stream, strip 0) orders the call: every strip starts after the work already
 // on it, and it waits for every strip's end.
+//   5. (stretch: hyb_hybrid_stretch_u8, reference proj/src/pipeline.cpp:55-57) every gain also folds the
+//      range of its rows into its device's partial (min, 255 - max); after all gains each device combines
+//      the partials over NVLink the same way and maps its own rows with the global range -- the contrast
+//      stretch's min / max fused into the gain plus one exchange.
 int hybrid_multi(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int cols, int smax, int win, int parts,
-                 uint8_t* y, size_t ypitch, hyb_stats* stats) {
+                 uint8_t* y, size_t ypitch, hyb_stats* stats, bool stretch = false) {
     int st;
     if ((st = check_smax(ctx, smax)) || (st = check_win(ctx, win)) || (st = check_dims(ctx, rows, cols)) ||
         (st = check_pitch(ctx, pitch, cols, "g")) || (st = check_pitch(ctx, ypitch, cols, "y")))
@@ -525,6 +535,12 @@ int hybrid_multi(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int col
             (st = chk(c->wtot.ensure(sizeof(long long)), "alloc")) ||
             (st = chk(c->wparts.ensure(sizeof(long long) * n), "alloc")))
             return st;
+        if (stretch &&
+            ((st = chk(c->mm.ensure(2 * sizeof(unsigned)), "alloc")) ||
+             (st = chk(c->mmtot.ensure(2 * sizeof(unsigned)), "alloc")) ||
+             (st = chk(c->mmparts.ensure(2 * sizeof(unsigned) * n), "alloc")) ||
+             (st = chk(cudaMemsetAsync(c->mm.ptr, 0xFF, 2 * sizeof(unsigned), c->stream), "memset"))))
+            return st;
         if ((st = chk(copy2d(c, c->strip_g[0].ptr, sp, g + (size_t)(t.start - t.hA) * pitch, pitch, cols, grows),
                       "strip halo copy")))
             return st;
@@ -544,6 +560,9 @@ int hybrid_multi(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int col
         HYB_CHECK(cudaEventRecord(ctx->ev[1], ctx->stream));
     }
     // 3-4: exact total W on every device, then the gain of its core rows
+    std::vector<uint8_t*> ydst(n);
+    std::vector<size_t> ydp(n);
+    std::vector<char> ydirect(n);
     for (int i = 0; i < n; ++i) {
         hyb_ctx* c = sub[i];
         const S& t = s[i];
@@ -581,9 +600,51 @@ int hybrid_multi(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows, int col
             yp = sp;
         }
         hyb::Plane w{c->strip_f[0].ptr, sp, 0, yd, yp, 0, t.fa + t.core + t.fb, cols, t.fa, t.fa + t.core, 1};
-        if ((st = chk(hyb::launch_wiener_gain(w, win, Wt, P, c->stream), "strip gain"))) return st;
+        if ((st = chk(hyb::launch_wiener_gain(w, win, Wt, P, c->stream,
+                                              stretch ? reinterpret_cast<unsigned*>(c->mm.ptr) : nullptr),
+                      "strip gain")))
+            return st;
+        ydst[i] = yd;
+        ydp[i] = yp;
+        ydirect[i] = direct;
+        if (stretch) {
+            if ((st = chk(cudaEventRecord(c->ev_gainx, c->stream), "event"))) return st;
+            continue;  // the map (step 5) comes first
+        }
         if (!direct &&
             (st = chk(copy2d(c, y + (size_t)t.start * ypitch, ypitch, yd, yp, cols, t.core), "strip output copy")))
+            return st;
+        if ((st = chk(cudaEventRecord(c->ev_done, c->stream), "event"))) return st;
+    }
+    // 5: the global range from every strip's partial on every device, then the map of its own rows
+    for (int i = 0; i < n && stretch; ++i) {
+        hyb_ctx* c = sub[i];
+        const S& t = s[i];
+        CtxScope scope(c);
+        if (cudaSetDevice(c->device) != cudaSuccess) return cuda_fail(ctx, cudaGetLastError(), "cudaSetDevice");
+        auto chk = [&](cudaError_t e, const char* what) { return e == cudaSuccess ? HYB_OK : cuda_fail(ctx, e, what); };
+        hyb::MmPartials pm{};
+        pm.n = n;
+        for (int j = 0; j < n; ++j) {
+            if (j != i && (st = chk(cudaStreamWaitEvent(c->stream, sub[j]->ev_gainx, 0), "wait gain"))) return st;
+            if (ctx->peer_ok[(size_t)i * n + j]) {
+                pm.p[j] = reinterpret_cast<const unsigned*>(sub[j]->mm.ptr);
+            } else {
+                unsigned* dst = reinterpret_cast<unsigned*>(c->mmparts.ptr) + 2 * j;
+                if ((st = chk(cudaMemcpyPeerAsync(dst, c->device, sub[j]->mm.ptr, sub[j]->device, 2 * sizeof(unsigned),
+                                                  c->stream),
+                              "partial range copy")))
+                    return st;
+                pm.p[j] = dst;
+            }
+        }
+        unsigned* mt = reinterpret_cast<unsigned*>(c->mmtot.ptr);
+        if ((st = chk(hyb::launch_min_partials(pm, mt, c->stream), "range reduction")) ||
+            (st = chk(hyb::launch_stretch_map(ydst[i], ydp[i], t.core, cols, ydst[i], ydp[i], mt, c->stream),
+                      "strip stretch")))
+            return st;
+        if (!ydirect[i] && (st = chk(copy2d(c, y + (size_t)t.start * ypitch, ypitch, ydst[i], ydp[i], cols, t.core),
+                                     "strip output copy")))
             return st;
         if ((st = chk(cudaEventRecord(c->ev_done, c->stream), "event"))) return st;
     }
@@ -727,6 +788,7 @@ hyb_ctx* hyb_create(int device, int* status) {
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->copy2, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_stats, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_done, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_gainx, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_start, cudaEventDisableTiming);
     for (int i = 0; i < hyb_ctx::kMaxChunks && e == cudaSuccess; ++i) {
         e = cudaEventCreateWithFlags(&ctx->ev_h2d[i], cudaEventDisableTiming);
@@ -780,7 +842,7 @@ int hyb_destroy(hyb_ctx* ctx) {
     ctx->mg_in.release();
     ctx->mg_out.release();
     if (ctx->host_w) cudaFreeHost(ctx->host_w);
-    for (cudaEvent_t ev : {ctx->ev_stats, ctx->ev_done, ctx->ev_start})
+    for (cudaEvent_t ev : {ctx->ev_stats, ctx->ev_done, ctx->ev_start, ctx->ev_gainx})
         if (ev) cudaEventDestroy(ev);
     for (auto& ev : ctx->ev)
         if (ev) cudaEventDestroy(ev);
@@ -1364,8 +1426,12 @@ int hyb_hybrid_stretch_u8(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows
     int st;
     if ((st = check_dims(ctx, rows, cols)) || (st = check_pitch(ctx, y_pitch, cols, "y"))) return st;
     if (!y) return fail(ctx, HYB_EINVAL, "null image pointer");
+    // multi-device: per-strip ranges fused into the gains, one exchange, per-strip maps (hybrid_multi 5.)
+    if (!ctx->peers.empty()) return hybrid_multi(ctx, g, pitch, rows, cols, smax, win, parts, y, y_pitch, stats, true);
     HYB_CHECK(cudaSetDevice(ctx->device));
-    // stages 1-2 into a device buffer, then the final stretch (in place when y is on the device)
+    // stages 1-2 into a device buffer, then the final stretch (in place when y is on the device).  The
+    // separate-kernel gains fold y's range into mm as they write it, leaving only the map; the fused
+    // small-image kernel does not, and then the stretch runs its own min / max pass first.
     const bool dy = is_device_ptr(y);
     const size_t pp = round_pitch(cols);
     uint8_t* d = y;
@@ -1375,10 +1441,18 @@ int hyb_hybrid_stretch_u8(hyb_ctx* ctx, const uint8_t* g, size_t pitch, int rows
         d = ctx->ys.ptr;
         dp = pp;
     }
-    if ((st = hyb_hybrid_u8(ctx, g, pitch, rows, cols, smax, win, parts, d, dp, stats))) return st;
     HYB_CHECK(ctx->mm.ensure(2 * sizeof(unsigned)));
-    HYB_CHECK(hyb::launch_contrast_stretch(d, dp, rows, cols, d, dp, reinterpret_cast<unsigned*>(ctx->mm.ptr),
-                                           ctx->stream));
+    unsigned* mm = reinterpret_cast<unsigned*>(ctx->mm.ptr);
+    HYB_CHECK(cudaMemsetAsync(mm, 0xFF, 2 * sizeof(unsigned), ctx->stream));
+    ctx->stretch_mm = mm;
+    ctx->stretch_fused = false;
+    st = hybrid_u8_impl(ctx, g, pitch, rows, cols, smax, win, parts, d, dp, stats, false);  // no graph replay
+    ctx->stretch_mm = nullptr;
+    if (st) return st;
+    if (ctx->stretch_fused)
+        HYB_CHECK(hyb::launch_stretch_map(d, dp, rows, cols, d, dp, mm, ctx->stream));
+    else
+        HYB_CHECK(hyb::launch_contrast_stretch(d, dp, rows, cols, d, dp, mm, ctx->stream));
     if (!dy) {
         HYB_CHECK(copy2d(ctx, y, y_pitch, d, dp, cols, rows));
         HYB_CHECK(cudaStreamSynchronize(ctx->stream));

@@ -119,9 +119,11 @@ cudaError_t launch_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, si
 // W1 statistics launch (wiener.cu): adds sum of V over the rows into noise_sum[slice].
 cudaError_t launch_wiener_stats(const Plane& p, int win, unsigned long long* noise_sum,
                                 cudaStream_t stream);
-// W1 gain launch: noise_sum[slice] read on the device; pixel_count per slice.
+// W1 gain launch: noise_sum[slice] read on the device; pixel_count per slice.  mm (nullable, device, 2 u32):
+// also fold the range of the y it writes into mm[0] = min, mm[1] = 255 - max (atomicMin; the caller
+// initialises both to 0xFFFFFFFF) -- contrast_stretch's min / max fused into the gain.
 cudaError_t launch_wiener_gain(const Plane& p, int win, const long long* noise_sum,
-                               long long pixel_count, cudaStream_t stream);
+                               long long pixel_count, cudaStream_t stream, unsigned* mm = nullptr);
 
 // Fused single-kernel hybrid step for small single images (small.cu): every CTA keeps its tiles
 // resident; two grid barriers (cooperative launch).  plan_small says whether it applies.
@@ -149,6 +151,18 @@ cudaError_t launch_small(const SmallPlan& pl, const SmallBufs& bufs, int rows, i
 // contrast_stretch (stretch.cu): mm = 2 u32 device scratch; src == dst allowed.
 cudaError_t launch_contrast_stretch(const uint8_t* src, size_t spitch, int rows, int cols, uint8_t* dst,
                                     size_t dpitch, unsigned* mm, cudaStream_t stream);
+// its two passes: fold src's range into mm (mm[0] = min, mm[1] = 255 - max, atomicMin: initialise both to
+// 0xFFFFFFFF first), and the exact LUT map with the range mm holds
+cudaError_t launch_stretch_minmax(const uint8_t* src, size_t spitch, int rows, int cols, unsigned* mm,
+                                  cudaStream_t stream);
+cudaError_t launch_stretch_map(const uint8_t* src, size_t spitch, int rows, int cols, uint8_t* dst, size_t dpitch,
+                               const unsigned* mm, cudaStream_t stream);
+// multi-device stretch: out[0..1] = the elementwise min of the n devices' mm pairs (peer reads)
+struct MmPartials {
+    const unsigned* p[kMaxDevices];
+    int n;
+};
+cudaError_t launch_min_partials(const MmPartials& parts, unsigned* out, cudaStream_t stream);
 
 // window_stats (wstats.cu): min / median / max planes of the k x k windows; outputs nullable.
 cudaError_t launch_window_stats(const uint8_t* src, size_t pitch, int rows, int cols, int k, uint8_t* zmin,

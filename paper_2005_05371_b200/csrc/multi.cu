@@ -17,7 +17,23 @@ __global__ void sum_partials_kernel(const Partials parts, long long* out) {
     }
 }
 
+__global__ void min_partials_kernel(const MmPartials parts, unsigned* out) {
+    if (threadIdx.x < 2) {
+        unsigned v = 0xFFFFFFFFu;
+        for (int i = 0; i < parts.n; ++i) v = min(v, ((volatile const unsigned*)parts.p[i])[threadIdx.x]);
+        out[threadIdx.x] = v;
+    }
+}
+
 }  // namespace
+
+// contrast_stretch over the strips: every device combines the per-strip ranges its gains folded
+// (mm[0] = min, mm[1] = 255 - max) the same way, so every strip maps with the same global range.
+cudaError_t launch_min_partials(const MmPartials& parts, unsigned* out, cudaStream_t stream) {
+    min_partials_kernel<<<1, 32, 0, stream>>>(parts, out);
+    count_launch();
+    return cudaGetLastError();
+}
 
 cudaError_t launch_sum_partials(const Partials& parts, long long* out, cudaStream_t stream) {
     sum_partials_kernel<<<1, 32, 0, stream>>>(parts, out);

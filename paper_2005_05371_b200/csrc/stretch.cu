@@ -91,21 +91,32 @@ __global__ void __launch_bounds__(XT) map_kernel(const uint8_t* __restrict__ src
 
 }  // namespace
 
-cudaError_t launch_contrast_stretch(const uint8_t* src, size_t spitch, int rows, int cols, uint8_t* dst,
-                                    size_t dpitch, unsigned* mm, cudaStream_t stream) {
-    const int sms = device_sms();
-    cudaError_t e = cudaMemsetAsync(mm, 0xFF, 2 * sizeof(unsigned), stream);  // lo = 255+, 255 - hi = 255+
-    if (e != cudaSuccess) return e;
+cudaError_t launch_stretch_minmax(const uint8_t* src, size_t spitch, int rows, int cols, unsigned* mm,
+                                  cudaStream_t stream) {
     const long long px = (long long)rows * cols;
-    const int grid = (int)std::max(1ll, std::min((long long)sms * 8, (px + XT * 16 - 1) / (XT * 16)));
-    e = launch_pdl(minmax_kernel, dim3(grid), dim3(XT), 0, stream, src, spitch, rows, cols, mm);
-    count_launch();
-    if (e != cudaSuccess) return e;
-    const int mgrid = (int)std::max(1ll, std::min((long long)sms * 8, (px + XT * 4 - 1) / (XT * 4)));
-    e = launch_pdl(map_kernel, dim3(mgrid), dim3(XT), 0, stream, src, spitch, rows, cols, dst, dpitch,
-                   (const unsigned*)mm);
+    const int grid = (int)std::max(1ll, std::min((long long)device_sms() * 8, (px + XT * 16 - 1) / (XT * 16)));
+    const cudaError_t e = launch_pdl(minmax_kernel, dim3(grid), dim3(XT), 0, stream, src, spitch, rows, cols, mm);
     count_launch();
     return e;
+}
+
+cudaError_t launch_stretch_map(const uint8_t* src, size_t spitch, int rows, int cols, uint8_t* dst, size_t dpitch,
+                               const unsigned* mm, cudaStream_t stream) {
+    const long long px = (long long)rows * cols;
+    const int mgrid = (int)std::max(1ll, std::min((long long)device_sms() * 8, (px + XT * 4 - 1) / (XT * 4)));
+    const cudaError_t e = launch_pdl(map_kernel, dim3(mgrid), dim3(XT), 0, stream, src, spitch, rows, cols, dst,
+                                     dpitch, mm);
+    count_launch();
+    return e;
+}
+
+cudaError_t launch_contrast_stretch(const uint8_t* src, size_t spitch, int rows, int cols, uint8_t* dst,
+                                    size_t dpitch, unsigned* mm, cudaStream_t stream) {
+    cudaError_t e = cudaMemsetAsync(mm, 0xFF, 2 * sizeof(unsigned), stream);  // lo = 255+, 255 - hi = 255+
+    if (e != cudaSuccess) return e;
+    e = launch_stretch_minmax(src, spitch, rows, cols, mm, stream);
+    if (e != cudaSuccess) return e;
+    return launch_stretch_map(src, spitch, rows, cols, dst, dpitch, mm, stream);
 }
 
 }  // namespace hyb

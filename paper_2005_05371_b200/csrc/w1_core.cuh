@@ -300,9 +300,12 @@ __device__ __forceinline__ uint32_t w1_gain4(const W1Gain& k, uint32_t own, cons
 
 // Gain of one tile: y for the tile's output pixels (rows < row_lim, columns < col_lim) through
 // dst_tile (image row y0, column x0).
-template <int RW, int FH>
+// MM: also fold the written y bytes into the byte-SIMD running minimum / maximum mn / mx (the contrast
+// stretch's image range, fused into the gain).
+template <int RW, int FH, bool MM = false>
 __device__ __forceinline__ void w1_tile_gain(const uint8_t* __restrict__ T, int x0, int col_lim, int row_lim,
-                                             const W1Gain& k, uint8_t* dst_tile, size_t dpitch) {
+                                             const W1Gain& k, uint8_t* dst_tile, size_t dpitch,
+                                             uint32_t* mn = nullptr, uint32_t* mx = nullptr) {
     constexpr int N = 2 * RW + 1;
     constexpr int NN = N * N;
     const int lane = threadIdx.x & 31;
@@ -336,6 +339,13 @@ __device__ __forceinline__ void w1_tile_gain(const uint8_t* __restrict__ T, int 
         const uint32_t own = *(base + (y + RW) * (FBS / 4) + 1);  // f of the 4 output pixels
         const uint32_t out = w1_gain4<NN>(k, own, s1, s2, inv_n);
         if (y < row_lim) {
+            if (MM) {
+                // bytes outside the image (ragged last tile) are neutral: 0xFF for the min, 0 for the max
+                const uint32_t keep = c + 4 <= col_lim ? 0xFFFFFFFFu
+                                                       : (c >= col_lim ? 0u : (1u << (8 * (col_lim - c))) - 1u);
+                *mn = __vminu4(*mn, out | ~keep);
+                *mx = __vmaxu4(*mx, out & keep);
+            }
             if (vec_store) {
                 *reinterpret_cast<uint32_t*>(drow) = out;
             } else {

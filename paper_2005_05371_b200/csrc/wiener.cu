@@ -232,12 +232,14 @@ struct FastArgs {
     size_t dpitch, dslice;
     int rows, cols, row_begin, row_end, n_slices;
     int tiles_x, tiles_y;
+    uint32_t mx, ms;           // ceil(2^32 / tiles_x), ceil(2^32 / per_slice): tile index -> coordinates
     unsigned long long* wsum;  // stats
     const long long* wread;    // gain
     long long pixel_count;
+    unsigned* mm;              // gain, MM: [0] = min y, [1] = 255 - max y (atomicMin; 0xFFFFFFFF when empty)
 };
 
-template <int RW, bool GAIN, int FH>
+template <int RW, bool GAIN, int FH, bool MM = false>
 __global__ void __launch_bounds__(FNW * 32, GAIN ? 4 : 3) wiener_fast_kernel(const __grid_constant__ CUtensorMap tm,
                                                                const __grid_constant__ FastArgs a) {
     constexpr int SROWS = FH + 2 * RW;
@@ -251,10 +253,19 @@ __global__ void __launch_bounds__(FNW * 32, GAIN ? 4 : 3) wiener_fast_kernel(con
     const int ntiles = per_slice * a.n_slices;
     const int gw = blockIdx.x * FNW + warp, nw = gridDim.x * FNW;  // global warp id / count
     if (gw >= ntiles) return;
+    // t / d as a multiply-high by m = min(ceil(2^32 / d), 2^32 - 1) plus a correction step each way
+    // (the estimate is off by at most one; d = 1 clamps m); the integer divisions were ~5 % of the W1
+    // passes' stall samples at config 4
+    auto fdiv = [](uint32_t t, uint32_t d, uint32_t m) {
+        uint32_t q = __umulhi(t, m);
+        if (q * d > t) --q;
+        if ((q + 1) * d <= t) ++q;
+        return q;
+    };
     auto coords = [&](int t, int& x0, int& y0, int& z) {
-        z = t / per_slice;
+        z = a.n_slices == 1 ? 0 : (int)fdiv((uint32_t)t, (uint32_t)per_slice, a.ms);
         const int rem = t - z * per_slice;
-        const int by = rem / a.tiles_x;
+        const int by = (int)fdiv((uint32_t)rem, (uint32_t)a.tiles_x, a.mx);
         x0 = (rem - by * a.tiles_x) * FW;
         y0 = a.row_begin + by * FH;
     };
@@ -276,6 +287,7 @@ __global__ void __launch_bounds__(FNW * 32, GAIN ? 4 : 3) wiener_fast_kernel(con
 
     W1Gain kg = {};
     unsigned long long vsum = 0;
+    uint32_t ymn = 0xFFFFFFFFu, ymx = 0u;  // MM: byte-SIMD range of the y written by this lane
     int zprev = -1;
     int it = 0;
     for (int t = gw; t < ntiles; t += nw, ++it) {
@@ -308,8 +320,9 @@ __global__ void __launch_bounds__(FNW * 32, GAIN ? 4 : 3) wiener_fast_kernel(con
         if (!GAIN) {
             vsum += (unsigned long long)w1_tile_stats<RW, FH>(T, x0, y0, a.rows, a.cols, a.row_begin, a.row_end);
         } else {
-            w1_tile_gain<RW, FH>(T, x0, col_lim, row_lim, kg,
-                                 a.dst + (size_t)z * a.dslice + (size_t)(y0 - a.row_begin) * a.dpitch + x0, a.dpitch);
+            w1_tile_gain<RW, FH, MM>(T, x0, col_lim, row_lim, kg,
+                                     a.dst + (size_t)z * a.dslice + (size_t)(y0 - a.row_begin) * a.dpitch + x0,
+                                     a.dpitch, &ymn, &ymx);
         }
         __syncwarp();
         // refill this slot with the warp's tile after next
@@ -323,16 +336,26 @@ __global__ void __launch_bounds__(FNW * 32, GAIN ? 4 : 3) wiener_fast_kernel(con
         for (int d = 16; d > 0; d >>= 1) vsum += __shfl_down_sync(0xFFFFFFFFu, vsum, d);
         if (lane == 0 && vsum) atomicAdd(a.wsum + zprev, vsum);
     }
+    if (MM) {  // the warp's y range -> the image range (one min atomic each for lo and 255 - hi)
+        uint32_t lo = min(min(ymn & 0xFFu, (ymn >> 8) & 0xFFu), min((ymn >> 16) & 0xFFu, ymn >> 24));
+        uint32_t hi = max(max(ymx & 0xFFu, (ymx >> 8) & 0xFFu), max((ymx >> 16) & 0xFFu, ymx >> 24));
+        lo = __reduce_min_sync(0xFFFFFFFFu, lo);
+        hi = __reduce_max_sync(0xFFFFFFFFu, hi);
+        if (lane == 0 && lo <= hi) {
+            atomicMin(&a.mm[0], lo);
+            atomicMin(&a.mm[1], 255u - hi);
+        }
+    }
 }
 
-template <int RW, bool GAIN, int FH>
+template <int RW, bool GAIN, int FH, bool MM = false>
 cudaError_t launch_fast(const Plane& p, unsigned long long* wsum, const long long* wread, long long pixel_count,
-                        cudaStream_t stream) {
+                        cudaStream_t stream, unsigned* mm = nullptr) {
     constexpr int SLOT = kFastSmemSlot(RW, FH);
     constexpr size_t smem = 128 + (size_t)FNW * 2 * SLOT + 128;
     static PerDevice attr, occ;
     {
-        const cudaError_t e = ensure_smem_attr(attr, (const void*)wiener_fast_kernel<RW, GAIN, FH>, smem);
+        const cudaError_t e = ensure_smem_attr(attr, (const void*)wiener_fast_kernel<RW, GAIN, FH, MM>, smem);
         if (e != cudaSuccess) return e;
     }
     CUtensorMap tm;
@@ -349,15 +372,23 @@ cudaError_t launch_fast(const Plane& p, unsigned long long* wsum, const long lon
     a.n_slices = p.n_slices;
     a.tiles_x = (p.cols + FW - 1) / FW;
     a.tiles_y = (p.row_end - p.row_begin + FH - 1) / FH;
+    {
+        auto magic = [](unsigned long long d) {
+            return (uint32_t)std::min<unsigned long long>(((1ull << 32) + d - 1) / d, 0xFFFFFFFFull);
+        };
+        a.mx = magic((unsigned long long)a.tiles_x);
+        a.ms = magic((unsigned long long)a.tiles_x * a.tiles_y);
+    }
     a.wsum = wsum;
     a.wread = wread;
     a.pixel_count = pixel_count;
-    const int per_sm = occupancy(occ, (const void*)wiener_fast_kernel<RW, GAIN, FH>, FNW * 32, smem);
+    a.mm = mm;
+    const int per_sm = occupancy(occ, (const void*)wiener_fast_kernel<RW, GAIN, FH, MM>, FNW * 32, smem);
     const long long ntiles = (long long)a.tiles_x * a.tiles_y * a.n_slices;
     const long long warps = std::min<long long>(ntiles, (long long)device_sms() * per_sm * FNW);
     const int grid = (int)((warps + FNW - 1) / FNW);
     const cudaError_t le =
-        launch_pdl(wiener_fast_kernel<RW, GAIN, FH>, dim3(grid), dim3(FNW * 32), smem, stream, tm, a);
+        launch_pdl(wiener_fast_kernel<RW, GAIN, FH, MM>, dim3(grid), dim3(FNW * 32), smem, stream, tm, a);
     if (le != cudaSuccess) return le;
     count_launch();
     return cudaGetLastError();
@@ -365,24 +396,32 @@ cudaError_t launch_fast(const Plane& p, unsigned long long* wsum, const long lon
 
 template <bool GAIN>
 cudaError_t dispatch(const Plane& p, int win, unsigned long long* wsum, const long long* wread,
-                     long long pixel_count, cudaStream_t stream) {
+                     long long pixel_count, cudaStream_t stream, unsigned* mm = nullptr) {
     if (tma_compatible(p.src, p.spitch, p.sslice)) {
         const long long px = (long long)(p.row_end - p.row_begin) * p.cols * p.n_slices;
         const bool small = px < (16ll << 20);
+        // small images: 8-row tiles, twice the warps in flight and half the per-warp chain
+#define HYB_FAST(RW)                                                                                          \
+    if (GAIN && mm)                                                                                          \
+        return small ? launch_fast<RW, GAIN, 8, true>(p, wsum, wread, pixel_count, stream, mm)                \
+                     : launch_fast<RW, GAIN, 16, true>(p, wsum, wread, pixel_count, stream, mm);              \
+    return small ? launch_fast<RW, GAIN, 8>(p, wsum, wread, pixel_count, stream)                              \
+                 : launch_fast<RW, GAIN, 16>(p, wsum, wread, pixel_count, stream);
         switch (win) {
-            // small images: 8-row tiles, twice the warps in flight and half the per-warp chain
-            case 1: return small ? launch_fast<0, GAIN, 8>(p, wsum, wread, pixel_count, stream)
-                                 : launch_fast<0, GAIN, 16>(p, wsum, wread, pixel_count, stream);
-            case 3: return small ? launch_fast<1, GAIN, 8>(p, wsum, wread, pixel_count, stream)
-                                 : launch_fast<1, GAIN, 16>(p, wsum, wread, pixel_count, stream);
-            case 5: return small ? launch_fast<2, GAIN, 8>(p, wsum, wread, pixel_count, stream)
-                                 : launch_fast<2, GAIN, 16>(p, wsum, wread, pixel_count, stream);
-            case 7: return small ? launch_fast<3, GAIN, 8>(p, wsum, wread, pixel_count, stream)
-                                 : launch_fast<3, GAIN, 16>(p, wsum, wread, pixel_count, stream);
+            case 1: HYB_FAST(0)
+            case 3: HYB_FAST(1)
+            case 5: HYB_FAST(2)
+            case 7: HYB_FAST(3)
             default: break;
         }
+#undef HYB_FAST
     }
-    return launch<GAIN>(p, win, wsum, wread, pixel_count, stream);
+    cudaError_t e = launch<GAIN>(p, win, wsum, wread, pixel_count, stream);
+    if (e != cudaSuccess || !GAIN || !mm) return e;
+    // generic gain: the range of the rows it wrote by a separate pass (same result, one more read)
+    for (int z = 0; z < p.n_slices && e == cudaSuccess; ++z)
+        e = launch_stretch_minmax(p.dst + (size_t)z * p.dslice, p.dpitch, p.row_end - p.row_begin, p.cols, mm, stream);
+    return e;
 }
 
 }  // namespace
@@ -393,8 +432,8 @@ cudaError_t launch_wiener_stats(const Plane& p, int win, unsigned long long* noi
 }
 
 cudaError_t launch_wiener_gain(const Plane& p, int win, const long long* noise_sum,
-                               long long pixel_count, cudaStream_t stream) {
-    return dispatch<true>(p, win, nullptr, noise_sum, pixel_count, stream);
+                               long long pixel_count, cudaStream_t stream, unsigned* mm) {
+    return dispatch<true>(p, win, nullptr, noise_sum, pixel_count, stream, mm);
 }
 
 }  // namespace hyb

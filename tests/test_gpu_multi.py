@@ -131,3 +131,29 @@ def test_estimate_mode_reference_and_stretches():
     res = denoise.hybrid_denoise(g, FilterConfig(smax=7, wiener_window=3, final_stretch=True), stretch_after_each=True)
     assert res.noise_sum == ws
     np.testing.assert_array_equal(res.image, oracle.contrast_stretch(ys))
+
+
+@pytest.mark.parametrize("devices", [None] + _device_sets()[:2])
+@pytest.mark.parametrize("shape,smax,win,parts", [((2053, 1500), 9, 5, 1), ((611, 997), 11, 7, 1),
+                                                  ((300, 400), 7, 9, 1), ((1100, 900), 7, 3, 3),
+                                                  ((64, 300), 5, 3, 1)])
+def test_hybrid_stretch_fused_range(ctx, devices, shape, smax, win, parts):
+    # stages 1-3 (reference proj/src/pipeline.cpp:23-57): the contrast stretch's min / max folded into the
+    # W1 gain (separate-kernel path; the generic gain for win 9 and the fused small-image kernel take a
+    # separate min / max pass), and across strips the per-device ranges combined over NVLink before each
+    # strip maps its own rows (multi-device contexts) -- all equal to the oracle's stretch of the oracle
+    g = _img(*shape, seed=shape[1] + smax)
+    g[:3, :5] = 0  # the full range present, and not: both map branches exercised across cases
+    if shape[0] == 64:
+        g[g > 200] = 200
+    ref_y, ref_w = oracle.hybrid_threaded(g, smax, win)
+    want = oracle.contrast_stretch(ref_y)
+    c = ctx if devices is None else capi.Context(devices=devices)
+    cfg = FilterConfig(smax=smax, wiener_window=win, parts=parts if devices is None else 1)
+    res = denoise.hybrid_denoise_stretched(torch.from_numpy(g).cuda(), cfg, ctx=c)
+    assert res.noise_sum == ref_w
+    np.testing.assert_array_equal(res.image.cpu().numpy(), want)
+    res = denoise.hybrid_denoise_stretched(g, cfg, ctx=c)  # host buffers
+    np.testing.assert_array_equal(res.image, want)
+    if devices is not None:
+        c.close()
