@@ -651,6 +651,9 @@ cudaError_t launch_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, si
     g.row_end = p.row_end;
     g.n_slices = p.n_slices;
     g.smax = smax;
+#ifdef HYB_EXP_GROW_SMAX_CAP  // timing experiment only: the growth stops at this window (output incomplete)
+    g.smax = std::min(smax, HYB_EXP_GROW_SMAX_CAP);
+#endif
     g.tiles_x = a.tiles_x;
     g.tiles_y = a.tiles_y;
     g.rec_ctr = a.rec_ctr;

@@ -225,6 +225,15 @@ cudaError_t launch(const Plane& p, int win, unsigned long long* wsum, const long
 // integer ops; statistics stay exact int32 per pixel.
 // ------------------------------------------------------------------------------------------
 constexpr int FNW = 8;           // warps per CTA
+// Tile rows for images >= 16 MPix (8 below): a tile pays N - 1 prologue rows of box sums, so taller tiles
+// amortise them, at the cost of shared memory per warp.  Measured (W1 ms, config 2 = 5x5 / config 4 = 7x7):
+// 16 rows 0.168 / 0.667, 24 rows 0.160 / 0.682, 32 rows 0.178 / 0.663.
+#ifndef HYB_W1_FH
+#define HYB_W1_FH(RW) ((RW) <= 2 ? 24 : 16)
+#endif
+#ifndef HYB_W1_GAIN_MINB
+#define HYB_W1_GAIN_MINB 3  // gain CTAs per SM (register budget; 4: config 4 W1 +1.4 %)
+#endif
 __host__ __device__ constexpr int kFastSmemSlot(int rw, int fh) { return ((FBS * (fh + 2 * rw)) + 127) / 128 * 128; }
 
 struct FastArgs {
@@ -240,7 +249,7 @@ struct FastArgs {
 };
 
 template <int RW, bool GAIN, int FH, bool MM = false>
-__global__ void __launch_bounds__(FNW * 32, GAIN ? 4 : 3) wiener_fast_kernel(const __grid_constant__ CUtensorMap tm,
+__global__ void __launch_bounds__(FNW * 32, GAIN ? HYB_W1_GAIN_MINB : 3) wiener_fast_kernel(const __grid_constant__ CUtensorMap tm,
                                                                const __grid_constant__ FastArgs a) {
     constexpr int SROWS = FH + 2 * RW;
     constexpr int SLOT = kFastSmemSlot(RW, FH);
@@ -404,9 +413,9 @@ cudaError_t dispatch(const Plane& p, int win, unsigned long long* wsum, const lo
 #define HYB_FAST(RW)                                                                                          \
     if (GAIN && mm)                                                                                          \
         return small ? launch_fast<RW, GAIN, 8, true>(p, wsum, wread, pixel_count, stream, mm)                \
-                     : launch_fast<RW, GAIN, 16, true>(p, wsum, wread, pixel_count, stream, mm);              \
+                     : launch_fast<RW, GAIN, HYB_W1_FH(RW), true>(p, wsum, wread, pixel_count, stream, mm);              \
     return small ? launch_fast<RW, GAIN, 8>(p, wsum, wread, pixel_count, stream)                              \
-                 : launch_fast<RW, GAIN, 16>(p, wsum, wread, pixel_count, stream);
+                 : launch_fast<RW, GAIN, HYB_W1_FH(RW)>(p, wsum, wread, pixel_count, stream);
         switch (win) {
             case 1: HYB_FAST(0)
             case 3: HYB_FAST(1)
