@@ -349,7 +349,7 @@ def hybrid_denoise_stretched(noisy, config: FilterConfig, ctx=None) -> HybridRes
     gp, gpitch = capi.buf(noisy)
     yp, ypitch = capi.buf(y)
     st = capi.HybStats()
-    c = _ctx(ctx, noisy, y)
+    c = _config_ctx(ctx, config, noisy, y)
     check(lib.hyb_hybrid_stretch_u8(c, gp, gpitch, rows, cols, config.smax, config.wiener_window, config.parts,
                                     yp, ypitch, ctypes.byref(st)), c)
     return HybridResult(y, st.sigma2, st.t_adaptive, st.t_wiener, 0.0, st.noise_sum, st.t_total)

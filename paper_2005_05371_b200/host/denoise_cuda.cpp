@@ -262,10 +262,11 @@ HybridResult hybrid_denoise(const Image& noisy, const FilterConfig& config, cons
     const long long P = (long long)rows * cols;
     const int win = config.wiener_window;
     if (config.estimate_mode == EstimateMode::robust && !stretch_after_each) {
-        // the hot path: AMF + W1 in one call (strips over every configured device)
+        // the hot path: AMF + W1 in one call (strips over every configured device); with final_stretch the
+        // stretch rides along (its min / max folded into the gain, the range reduced across the devices)
         hyb_stats st{};
-        check(hyb_hybrid_u8(ctx, g.data(), cols, rows, cols, config.smax, win, config.parts, y.data(), cols, &st),
-              ctx);
+        auto hybrid = config.final_stretch ? hyb_hybrid_stretch_u8 : hyb_hybrid_u8;
+        check(hybrid(ctx, g.data(), cols, rows, cols, config.smax, win, config.parts, y.data(), cols, &st), ctx);
         r.sigma2 = st.sigma2;
         r.t_adaptive = st.t_adaptive;
         r.t_wiener = st.t_wiener;
@@ -306,7 +307,8 @@ HybridResult hybrid_denoise(const Image& noisy, const FilterConfig& config, cons
         r.t_wiener = secs(t2, clock::now());
         r.noise_sum = config.estimate_mode == EstimateMode::reference ? 0 : W;
     }
-    if (config.final_stretch) {  // proj/src/pipeline.cpp:55-57
+    const bool stretched = config.estimate_mode == EstimateMode::robust && !stretch_after_each;
+    if (config.final_stretch && !stretched) {  // proj/src/pipeline.cpp:55-57
         const auto t = std::chrono::steady_clock::now();
         check(hyb_contrast_stretch_u8(ctx, y.data(), cols, rows, cols, y.data(), cols), ctx);
         r.t_stretch += std::chrono::duration<double>(std::chrono::steady_clock::now() - t).count();

@@ -269,6 +269,22 @@ int main() {
         hyb_oracle_contrast_stretch_u8(y.data(), cols, rows, cols, y.data(), cols);
         CHECK(h2.noise_sum == w2);
         CHECK(h2.image == from_u8(y.data(), rows, cols));
+        // final_stretch on the hot path: the stretch's range folded into the W1 gain (one device, and three
+        // strips as a multi-device context on repeated ids)
+        int64_t w3 = 0;
+        hyb_oracle_wiener_stats_u8(f.data(), cols, rows, cols, 0, rows, 3, &w3);
+        hyb_oracle_wiener_gain_u8(f.data(), cols, rows, cols, 0, rows, 3, w3, (int64_t)rows * cols, y.data(), cols);
+        hyb_oracle_contrast_stretch_u8(y.data(), cols, rows, cols, y.data(), cols);
+        for (int multi = 0; multi < 2; ++multi) {
+            FilterConfig c3;
+            c3.smax = 7;
+            c3.wiener_window = 3;
+            c3.final_stretch = true;
+            if (multi) c3.device_ids = {0, 0, 0};
+            const HybridResult h3 = hybrid_denoise(noisy, c3);
+            CHECK(h3.noise_sum == w3);
+            CHECK(h3.image == from_u8(y.data(), rows, cols));
+        }
     }
     // the reference's pipeline tail (proj/tests/test_pipeline.cpp:29-57, test_wiener.cpp:110-160)
     {

@@ -1,6 +1,6 @@
 """Per-launch DRAM bytes and warp instructions of each stage from an `ncu --set full` report ->
 profiles/ncu_counters.json (read by bench.py).  usage: ncu_counters.py <config> <file.ncu-rep>
-Stages: hybrid_small_kernel (fused), amf (k3 + growth), wiener (statistics + gain); launches of a
+Stages: hybrid_small_kernel (fused), amf (k3 + growth, or the fused per-batch AMF kernel), wiener (statistics + gain); launches of a
 stage are summed (one hybrid call)."""
 import csv
 import io
@@ -16,7 +16,7 @@ UNITS = {"byte": 1, "B": 1, "Kbyte": 1e3, "KB": 1e3, "Mbyte": 1e6, "MB": 1e6, "G
 def stage(name):
     if "hybrid_small" in name:
         return "hybrid_small_kernel"
-    if "amf_k3" in name or "amf_grow" in name:
+    if "amf_k3" in name or "amf_grow" in name or "amf_fused" in name:
         return "amf"
     if "wiener" in name:
         return "wiener"

@@ -1,0 +1,20 @@
+#!/bin/bash
+# Round-2 evidence (run on the GPU box): GPU tests, the default bench line (config 4), the reference arm,
+# per-config bench lines, the ncu launch list of the bench command, and ncu --set full captures of
+# configs 1-4.  usage: tools/profile_r2.sh <tag>   (outputs under gpurun_out/prof_<tag>/)
+tag=${1:-v}
+o=gpurun_out/prof_$tag
+mkdir -p $o
+nvidia-smi > $o/nvidia_smi.txt 2>&1
+timeout 900 python -m pytest tests -m gpu -q > $o/gpu_tests.txt 2>&1; echo "gpu tests rc=$?"; tail -1 $o/gpu_tests.txt
+timeout 900 python bench.py > $o/bench_config4.json 2> $o/bench.err; echo "bench rc=$?"; tail -c 300 $o/bench_config4.json
+timeout 900 python bench.py --impl reference > $o/bench_reference.json 2> $o/bench_ref.err; echo "ref rc=$?"; tail -c 300 $o/bench_reference.json
+for c in 0 1 2 3; do
+  timeout 600 python bench.py --config $c --no-cpu-baseline > $o/bench_config$c.json 2>> $o/bench.err; echo "bench config $c rc=$?"
+done
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file $o/launches_config4.csv \
+    python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $o/ncu_launch.log 2>&1; echo "launch list rc=$?"
+for c in 1 2 3 4; do
+  timeout 900 ncu --set full --import-source on --clock-control none -o $o/full_config$c \
+      python tools/hybrid_dev.py $c 1 > $o/ncu_full_$c.log 2>&1; echo "ncu full config $c rc=$?"
+done
