@@ -30,7 +30,7 @@ namespace {
 
 constexpr int BBYTES = (BS * BH + 127) / 128 * 128;  // ring slot (TMA destinations are 128-byte aligned)
 constexpr int NBUF = 4;          // TMA ring depth
-constexpr int HDR = 256;         // mbarriers, counters, tile coordinates
+constexpr int HDR = 384;         // mbarriers, counters, tile coordinates, per-strip failure counts
 constexpr int K3T = NT + 32;     // + one producer warp (tile claims and TMA loads)
 constexpr int WAREA = 2 * WPIX;  // per warp: output strip, finalized_at strip
 constexpr size_t SMEM = HDR + NBUF * BBYTES + NW * WAREA + 128;
@@ -84,9 +84,8 @@ __global__ void __launch_bounds__(K3T, 3)
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);        // [NBUF] tile landed (or: no tile)
     uint64_t* empty = reinterpret_cast<uint64_t*>(smem + 32);  // [NBUF] all strips of the slot done
     int* done_cnt = reinterpret_cast<int*>(smem + 64);           // [NBUF] strips finished
-    int* fcount = reinterpret_cast<int*>(smem + 80);             // [NBUF] level-A failures of the slot's tile
-    int* next_strip = reinterpret_cast<int*>(smem + 96);         // dynamic strip counter
     int* tinfo = reinterpret_cast<int*>(smem + 128);             // [NBUF][4]: x0, y0, z, tile (-1: none)
+    int* fcnt = reinterpret_cast<int*>(smem + 256);              // [NBUF][NW] level-A failures per strip
     uint8_t* bufs = smem + HDR;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
@@ -99,9 +98,7 @@ __global__ void __launch_bounds__(K3T, 3)
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], TH / WR);
             done_cnt[s] = 0;
-            fcount[s] = 0;
         }
-        *next_strip = 0;
         fence_mbar_init();
     }
     __syncthreads();
@@ -140,12 +137,12 @@ __global__ void __launch_bounds__(K3T, 3)
     uint8_t* O = bufs + NBUF * BBYTES + warp * WAREA;
     uint8_t* F = O + WPIX;
 
-    // Strips (4-row slices of this CTA's tiles, in ring order) are claimed dynamically by warps.
-    for (;;) {
-        int claim = 0;
-        if (lane == 0) claim = atomicAdd(next_strip, 1);
-        claim = __shfl_sync(0xFFFFFFFFu, claim, 0);
-        const int ti = claim >> 3, sub = claim & 7;
+    // Warp w takes strip w (rows 4w .. 4w + 3) of every tile of the ring: k = 3 costs the same on every
+    // strip, so a static split balances without a strip-claim atomic per strip (the dynamic claim's atomics
+    // held ~10 % of this kernel's stall samples, but the kernel is ALU-bound and measured the same time
+    // either way -- configs 3 / 4 AMF 0.241 / 2.136 ms; the static split is the simpler code).
+    const int sub = warp;
+    for (int ti = 0;; ++ti) {
         const int s = ti & (NBUF - 1);
         mbar_wait_warp(&full[s], (uint32_t)(ti / NBUF) & 1u);
         const int t = tinfo[4 * s + 3];
@@ -165,15 +162,17 @@ __global__ void __launch_bounds__(K3T, 3)
                                      FIN ? args.fin + (size_t)z * args.fslice + (size_t)(y0 - args.row_begin) * args.fpitch + x0
                                          : nullptr,
                                      args.fpitch, args.row_end - y0, cols - x0);
-        if (lane == 0 && nf) atomicAdd(&fcount[s], nf);
 
         // ---- release the slot; the tile's last strip publishes its failure record ----
         if (lane == 0) {
+            fcnt[s * NW + sub] = nf;
             __threadfence_block();
             if (atomicAdd(&done_cnt[s], 1) == TH / WR - 1) {
                 done_cnt[s] = 0;
-                const int c = fcount[s];
-                fcount[s] = 0;
+                __threadfence_block();  // the other strips' counts (written before their done_cnt adds)
+                int c = 0;
+#pragma unroll
+                for (int w = 0; w < NW; ++w) c += ((volatile int*)fcnt)[s * NW + w];
                 if (c) {
                     const unsigned long long old =
                         atomicAdd(args.rec_ctr, (1ull << REC_SHIFT) | (unsigned)(c + REC_W));
