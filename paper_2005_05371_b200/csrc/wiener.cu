@@ -411,9 +411,11 @@ cudaError_t dispatch(const Plane& p, int win, unsigned long long* wsum, const lo
         const bool small = px < (16ll << 20);
         // small images: 8-row tiles, twice the warps in flight and half the per-warp chain
 #define HYB_FAST(RW)                                                                                          \
-    if (GAIN && mm)                                                                                          \
-        return small ? launch_fast<RW, GAIN, 8, true>(p, wsum, wread, pixel_count, stream, mm)                \
-                     : launch_fast<RW, GAIN, HYB_W1_FH(RW), true>(p, wsum, wread, pixel_count, stream, mm);              \
+    if constexpr (GAIN) {                                                                                     \
+        if (mm)                                                                                               \
+            return small ? launch_fast<RW, true, 8, true>(p, wsum, wread, pixel_count, stream, mm)           \
+                         : launch_fast<RW, true, HYB_W1_FH(RW), true>(p, wsum, wread, pixel_count, stream, mm); \
+    }                                                                                                         \
     return small ? launch_fast<RW, GAIN, 8>(p, wsum, wread, pixel_count, stream)                              \
                  : launch_fast<RW, GAIN, HYB_W1_FH(RW)>(p, wsum, wread, pixel_count, stream);
         switch (win) {
