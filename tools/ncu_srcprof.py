@@ -1,6 +1,6 @@
 """Per-source-line profile from `ncu -i X --page source --csv --print-source cuda,sass`: stall samples,
 executed warp instructions and the stall-reason mix, summed over the SASS under each source line
-(inlined header code is attributed to its own file:line).  usage: ncu_srcprof.py <report> <kernel regex> [top]"""
+(inlined header code is attributed to its own file:line).  usage: ncu_srcprof.py <report> <kernel regex> [top] [launches to skip]"""
 import csv
 import io
 import subprocess
@@ -9,8 +9,10 @@ from collections import defaultdict
 
 rep, kern = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
+skip = sys.argv[4] if len(sys.argv) > 4 else "0"  # matching launches to skip (e.g. 1: the second W1 pass)
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name", "regex:" + kern,
-                      "--print-source", "cuda,sass"], capture_output=True, text=True).stdout
+                      "--launch-skip", skip, "--launch-count", "1", "--print-source", "cuda,sass"],
+                     capture_output=True, text=True).stdout
 def num(x):
     try:
         return float(x.replace(",", ""))
