@@ -104,3 +104,44 @@ def test_fuzz_hybrid_batch(ctx, n, rows, cols, smax, win, density, dev, seed):
         ry, rw = oracle.hybrid(stack[s], smax, win)
         assert ws[s] == rw, s
         np.testing.assert_array_equal(out[s], ry, err_msg=f"slice {s}")
+
+
+@settings(**dict(SETTINGS, max_examples=80))
+@given(rows=st.integers(1, 400), cols=st.integers(1, 600), win=odd(1, 15), lo=st.floats(0.0, 1.0),
+       hi=st.floats(0.0, 1.0), pad=st.sampled_from([0, 7, 32]), dev=st.booleans(), seed=st.integers(0, 10**6))
+def test_fuzz_wiener_row_ranges(ctx, rows, cols, win, lo, hi, pad, dev, seed):
+    # W1 statistics and gain on a row range of f (the strip form): W and y against the oracle
+    a, b = sorted((int(lo * rows), int(hi * rows)))
+    b = max(b, a + 1)
+    if b > rows:
+        a, b = rows - 1, rows
+    f = _img(rows, cols, seed, 0.0)
+    fb = _pitched(f, pad, dev)
+    w = np.zeros(1, np.int64)
+    capi.check(capi.lib.hyb_wiener_stats_u8(ctx.ptr, _ptr(fb), cols + pad, rows, cols, a, b, win, w.ctypes.data),
+               ctx.ptr)
+    rw = oracle.wiener_stats(f, win, a, b)
+    assert int(w[0]) == rw
+    yb = _pitched(np.zeros((b - a, cols), np.uint8), pad, dev)
+    capi.check(capi.lib.hyb_wiener_gain_u8(ctx.ptr, _ptr(fb), cols + pad, rows, cols, a, b, win, w.ctypes.data,
+                                           rows * cols, _ptr(yb), cols + pad), ctx.ptr)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(_np(yb)[:, :cols], oracle.wiener_gain(f, win, rw, rows * cols, a, b))
+
+
+@settings(**dict(SETTINGS, max_examples=60))
+@given(rows=st.integers(1, 300), cols=st.integers(1, 300), k=odd(3, 21), density=st.floats(0.0, 0.9),
+       dev=st.booleans(), seed=st.integers(0, 10**6))
+def test_fuzz_window_stats_and_stretch(ctx, rows, cols, k, density, dev, seed):
+    g = _img(rows, cols, seed, density)
+    gb = torch.from_numpy(g).cuda() if dev else g
+    outs = [torch.empty_like(gb) if dev else np.empty_like(g) for _ in range(3)]
+    capi.check(capi.lib.hyb_window_stats_u8(ctx.ptr, _ptr(gb), cols, rows, cols, k, *(_ptr(o) for o in outs), cols),
+               ctx.ptr)
+    torch.cuda.synchronize()
+    for got, want in zip(outs, oracle.window_stats(g, k)):
+        np.testing.assert_array_equal(_np(got), want)
+    y = torch.empty_like(gb) if dev else np.empty_like(g)
+    capi.check(capi.lib.hyb_contrast_stretch_u8(ctx.ptr, _ptr(gb), cols, rows, cols, _ptr(y), cols), ctx.ptr)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(_np(y), oracle.contrast_stretch(g))
