@@ -132,15 +132,14 @@ __device__ __forceinline__ int k3_strip(const uint8_t* __restrict__ B, uint8_t* 
             // median of 9 = med3(max lo, med mid, min hi)
             const uint32_t zmed = sub_fma(sub_fma(add_fma(add_fma(a, b), c), ml), mh);
             const uint32_t g = gm[j + 1];
-            // lane masks (values are v * 257): mA = level A holds, mB = zmin < g < zmax
-            const uint32_t mA =
-                lane_mask(fadd(__vimin3_u16x2(fsub(zmed, zmin), fsub(zmax, zmed), 0x01010101u), 0x7FFF7FFFu));
-            const uint32_t mB =
-                lane_mask(fadd(__vimin3_u16x2(fsub(g, zmin), fsub(zmax, g), 0x01010101u), 0x7FFF7FFFu));
-            const uint32_t sel = mA & ~mB;
+            // flags in bit 15 of each lane (values are v * 257): tA = level A holds, tB = zmin < g < zmax;
+            // one sign-replicating PRMT turns tA & ~tB into the lane select mask
+            const uint32_t tA = fadd(__vimin3_u16x2(fsub(zmed, zmin), fsub(zmax, zmed), 0x01010101u), 0x7FFF7FFFu);
+            const uint32_t tB = fadd(__vimin3_u16x2(fsub(g, zmin), fsub(zmax, g), 0x01010101u), 0x7FFF7FFFu);
+            const uint32_t sel = lane_mask(tA & ~tB);
             o[j] = (zmed & sel) | (g & ~sel);
-            if (FIN) fz[j] = mA & 0x00030003u;     // 3 where finalised at k = 3
-            failbits |= (~mA & 0x80008000u) >> j;  // lane 0 -> bit 15 - j, lane 1 -> bit 31 - j
+            if (FIN) fz[j] = lane_mask(tA) & 0x00030003u;  // 3 where finalised at k = 3
+            failbits |= (~tA & 0x80008000u) >> j;          // lane 0 -> bit 15 - j, lane 1 -> bit 31 - j
         }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
