@@ -250,7 +250,7 @@ struct GrowCfg {
 #define HYB_WIDE_CAP 8192  // pooled queue capacity
 #endif
 #ifndef HYB_WIDE_CHUNK
-#define HYB_WIDE_CHUNK 13  // log2 of a dynamic claim
+#define HYB_WIDE_CHUNK 15  // log2 of the static chunk (the guided claims take at most this many units)
 #endif
 using GrowWide = GrowCfg<9, HYB_WIDE_MINB, HYB_WIDE_SLOTS, HYB_WIDE_CAP, true, HYB_WIDE_CHUNK>;
 #ifndef HYB_LEAN_SLOTS
@@ -613,7 +613,8 @@ cudaError_t launch_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, si
     a.rec_ctr = reinterpret_cast<unsigned long long*>(work.counters);
     a.records = work.records;
     a.chunk_rec = work.chunk_rec;
-    a.chunk_shift = smax >= HYB_WIDE_MIN_SMAX ? GrowWide::CHUNK_SHIFT : GrowLean::CHUNK_SHIFT;  // the growth variant below
+    a.chunk_shift = smax >= HYB_WIDE_MIN_SMAX ? (HYB_GUIDED ? 11 : GrowWide::CHUNK_SHIFT)
+                                              : GrowLean::CHUNK_SHIFT;  // the growth variant below
     const int per_sm = occupancy(occ_k3, (const void*)amf_k3_kernel<false>, K3T, SMEM);
     const long long ntiles = (long long)a.tiles_x * a.tiles_y * a.n_slices;
     const int grid = (int)std::min<long long>(ntiles, (long long)num_sms * per_sm);

@@ -571,6 +571,15 @@ __device__ __forceinline__ long long rec_off(const unsigned long long* rec, long
 // row * 128 + column of a 128 x 32 tile whose window bytes start at slot(slot), laid out as geo).  CTA-wide
 // (NTHR threads, every thread calls it; qcount[1..] zero on entry); level k resolves what it can through
 // out(slot, pixel, value, k) and re-queues the rest for k + 2.  Ends with __syncthreads.
+#ifndef HYB_GUIDED
+#define HYB_GUIDED 1  // guided (shrinking) dynamic growth claims; needs the k = 3 chunk table at 2048 units
+#endif
+#ifndef HYB_STATIC_Q
+#define HYB_STATIC_Q 3  // quarters of the growth work split statically (the rest claimed dynamically)
+#endif
+#ifndef HYB_GUIDED_DIV
+#define HYB_GUIDED_DIV 2  // a guided claim takes remaining / (HYB_GUIDED_DIV * CTAs) units
+#endif
 #ifndef HYB_GROW_NETMAX
 #define HYB_GROW_NETMAX 9  // largest window grown with a selection network (k <= 9); radix above
 #endif
@@ -782,7 +791,7 @@ __device__ __forceinline__ void grow_range(const CUtensorMap* tm, const GGeo& ge
     // static split sees (config 4: static-only CTAs finished 1.70 .. 2.22 ms; with the dynamic quarter
     // 2.03 .. 2.17 ms and a 3 % shorter step).  Without DYN everything is static (configs 2 / 3, where
     // the failures are shallow and a claimed chunk's half-filled batches cost more than the tail).
-    const long long nchunks = (T + CHUNK - 1) / CHUNK, nstatic = DYN ? nchunks * 3 / 4 : nchunks;
+    const long long nchunks = (T + CHUNK - 1) / CHUNK, nstatic = DYN ? nchunks * HYB_STATIC_Q / 4 : nchunks;
     __syncthreads();
 
     // One warp chooses the next batch (lane l: record cur + l) into sinfo_n / ctl_n and bulk-copies its
@@ -818,6 +827,41 @@ __device__ __forceinline__ void grow_range(const CUtensorMap* tm, const GGeo& ge
                 }
                 __syncwarp();
             }
+#if HYB_GUIDED
+            if (!have && DYN) {
+                // guided dynamic claims: k table units of 2048 (the k = 3 kernel's chunk table granularity),
+                // k = remaining units / (2 x CTAs) clamped to [1, CHUNK / 2048] -- big claims first, single units
+                // at the end, so the CTAs' finishing times close up (config 4 AMF 2.127 -> 2.096 ms with CHUNK 2^15;
+                // 4 x CTAs: 2.134, 1 x: 2.116 at CHUNK 2^13; half the work static: 2.170; strips of N = 4 / 8:
+                // 790 -> 764 / 440 -> 423 us)
+                constexpr long long U = 2048;
+                const long long Ts = min(T, nstatic * CHUNK), nu = (T - Ts + U - 1) / U;
+                long long c = 0, k = 1;
+                if (lane == 0) {
+                    const long long rem = nu - (long long)*(volatile int*)chunk_ctr;
+                    const long long d = (long long)HYB_GUIDED_DIV * gridDim.x;
+                    k = min(max((rem + d - 1) / d, 1ll), CHUNK / U);
+                    c = atomicAdd(chunk_ctr, (int)k);
+                }
+                c = __shfl_sync(0xFFFFFFFFu, c, 0);
+                k = __shfl_sync(0xFFFFFFFFu, k, 0);
+                if (c >= nu) {
+                    if (lane == 0) {
+                        sm.ctl_n[0] = 0;
+                        sm.ctl_n[1] = 0;
+                        sm.ctl_n[2] = 0;  // no more work
+                    }
+                    __syncwarp();
+                    return;
+                }
+                if (lane == 0) {
+                    cur[0] = __ldcg(chunk_rec + ((Ts + c * U) >> 11));
+                    cur[1] = Ts + c * U;
+                    cur[2] = min(Ts + (c + k) * U, T);
+                }
+                __syncwarp();
+            } else
+#endif
             if (!have) {
                 long long ch = nchunks;  // without DYN: no dynamic chunks
                 if (DYN) {
