@@ -259,7 +259,10 @@ using GrowWide = GrowCfg<9, HYB_WIDE_MINB, HYB_WIDE_SLOTS, HYB_WIDE_CAP, true, H
 #ifndef HYB_WIDE_MIN_SMAX
 #define HYB_WIDE_MIN_SMAX 11  // smallest smax grown by the wide variant
 #endif
-using GrowLean = GrowCfg<7, 3, HYB_LEAN_SLOTS, 4096, HYB_LEAN_DYN != 0, 11>;
+#ifndef HYB_LEAN_CHUNK
+#define HYB_LEAN_CHUNK 11
+#endif
+using GrowLean = GrowCfg<7, 3, HYB_LEAN_SLOTS, 4096, HYB_LEAN_DYN != 0, HYB_LEAN_CHUNK>;
 static_assert(GrowWide::SLOTS <= 8 && GrowLean::SLOTS <= 8, "header layout");
 static_assert(GrowWide::SLOTS <= GNT / 32 && GrowLean::SLOTS <= GNT / 32, "queue build: one warp per slot");
 static_assert(GrowWide::CHUNK_SHIFT >= 11 && GrowLean::CHUNK_SHIFT >= 11, "chunk table sized for chunks >= 2048");
@@ -613,8 +616,8 @@ cudaError_t launch_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, si
     a.rec_ctr = reinterpret_cast<unsigned long long*>(work.counters);
     a.records = work.records;
     a.chunk_rec = work.chunk_rec;
-    a.chunk_shift = smax >= HYB_WIDE_MIN_SMAX ? (HYB_GUIDED ? 11 : GrowWide::CHUNK_SHIFT)
-                                              : GrowLean::CHUNK_SHIFT;  // the growth variant below
+    // the chunk table of the growth variant below: 2048-unit entries for guided claims
+    a.chunk_shift = HYB_GUIDED ? 11 : smax >= HYB_WIDE_MIN_SMAX ? GrowWide::CHUNK_SHIFT : GrowLean::CHUNK_SHIFT;
     const int per_sm = occupancy(occ_k3, (const void*)amf_k3_kernel<false>, K3T, SMEM);
     const long long ntiles = (long long)a.tiles_x * a.tiles_y * a.n_slices;
     const int grid = (int)std::min<long long>(ntiles, (long long)num_sms * per_sm);
