@@ -28,7 +28,11 @@
 namespace hyb {
 namespace {
 
-constexpr int BBYTES = (BS * BH + 127) / 128 * 128;  // ring slot (TMA destinations are 128-byte aligned)
+#ifndef HYB_COMPACT_T_DEF
+#define HYB_COMPACT_T_DEF 32  // strips with at most this many level-A failures use compact growth entries
+#endif
+constexpr int KHMAX = 3;         // largest k = 3 tile halo (3 rows: compact growth windows, amf_core.cuh CompactOut)
+constexpr int BBYTES = (BS * (TH + 2 * KHMAX) + 127) / 128 * 128;  // ring slot (TMA destinations 128-byte aligned)
 constexpr int NBUF = 4;          // TMA ring depth
 constexpr int HDR = 384;         // mbarriers, counters, tile coordinates, per-strip failure counts
 constexpr int K3T = NT + 32;     // + one producer warp (tile claims and TMA loads)
@@ -57,13 +61,18 @@ struct K3Args {
     unsigned long long* records;  // [record] = (weighted offset << 24) | tile
     int* chunk_rec;               // [chunk] = record holding weighted position chunk << chunk_shift
     int chunk_shift;              // log2 of the growth chunk (the growth variant's queue capacity)
+    int halo;                     // tile rows loaded above / below: 1, or 3 with compact windows
+    uint4* cq;                    // compact growth entries (nullptr: bitmaps only)
+    int* cq_ctr;
+    int cq_cap, cq_thresh;
+    int out_rows;
 };
 
 
 __device__ __forceinline__ void issue_tile_load(const CUtensorMap* tm, uint8_t* Bbuf, uint64_t* bar, int x0, int y0,
-                                                int z) {
-    mbar_expect_tx(bar, BS * BH);
-    tma_load_3d(Bbuf, tm, bar, x0 - CP, y0 - 1, z);
+                                                int z, int halo) {
+    mbar_expect_tx(bar, BS * (TH + 2 * halo));
+    tma_load_3d(Bbuf, tm, bar, x0 - CP, y0 - halo, z);
 }
 
 __device__ __forceinline__ void tile_coords(const K3Args& a, int t, int* info) {
@@ -124,7 +133,7 @@ __global__ void __launch_bounds__(K3T, 3)
                 tinfo[4 * s + 3] = t;
                 fence_proxy_async_smem();
                 issue_tile_load(&tm_src, bufs + s * BBYTES, &full[s], tinfo[4 * s], tinfo[4 * s + 1],
-                                tinfo[4 * s + 2]);
+                                tinfo[4 * s + 2], args.halo);
             }
             __threadfence();
             if (args.dynamic && atomicAdd(args.done, 1) == (int)gridDim.x - 1) {  // every CTA stopped claiming
@@ -148,20 +157,33 @@ __global__ void __launch_bounds__(K3T, 3)
         const int t = tinfo[4 * s + 3];
         if (t < 0) break;
         const int x0 = tinfo[4 * s], y0 = tinfo[4 * s + 1], z = tinfo[4 * s + 2];
-        uint8_t* B = bufs + s * BBYTES;
+        const int H = args.halo;
+        uint8_t* Bfull = bufs + s * BBYTES;  // row 0 = image row y0 - H
+        uint8_t* B = Bfull + (H - 1) * BS;   // row 0 = image row y0 - 1
 
-        // ---- border tiles: edge replication (this strip's rows) in place of TMA's zero fill ----
-        const int sx0 = x0 - CP, sy0 = y0 - 1;
-        if (sx0 < 0 || sx0 + BS > cols || sy0 < 0 || sy0 + BH > rows)
-            replicate_edges<32>(B, BS, max(0, -sx0), min(BS, cols - sx0), max(0, -sy0), min(BH, rows - sy0),
-                                sub * WR, sub * WR + WR + 2, 1);
+        // ---- border tiles: edge replication (this strip's rows, reach H) in place of TMA's zero fill ----
+        const int sx0 = x0 - CP, sy0 = y0 - H, bh = TH + 2 * H;
+        if (sx0 < 0 || sx0 + BS > cols || sy0 < 0 || sy0 + bh > rows)
+            replicate_edges<32>(Bfull, BS, max(0, -sx0), min(BS, cols - sx0), max(0, -sy0), min(bh, rows - sy0),
+                                sub * WR, sub * WR + WR + 2 * H, H);
 
+        CompactOut co;
+        if (args.cq) {
+            co.ent = args.cq;
+            co.ctr = args.cq_ctr;
+            co.cap = args.cq_cap;
+            co.thresh = args.cq_thresh;
+            co.B = Bfull;
+            co.x0 = (uint32_t)x0;
+            co.key0 = (uint32_t)(z * args.out_rows + (y0 - args.row_begin));
+        }
         const int nf = k3_strip<FIN>(B, O, F, sub, args.grow ? args.bitmap + (size_t)t * 512 : nullptr,
                                      args.dst + (size_t)z * args.dslice + (size_t)(y0 - args.row_begin) * args.dpitch + x0,
                                      args.dpitch,
                                      FIN ? args.fin + (size_t)z * args.fslice + (size_t)(y0 - args.row_begin) * args.fpitch + x0
                                          : nullptr,
-                                     args.fpitch, args.row_end - y0, cols - x0);
+                                     args.fpitch, args.row_end - y0, cols - x0, nullptr, nullptr, 0,
+                                     args.cq ? &co : nullptr);
 
         // ---- release the slot; the tile's last strip publishes its failure record ----
         if (lane == 0) {
@@ -217,6 +239,10 @@ struct GArgs {
     const int* chunk_rec;               // [chunk] = record holding its first weighted position
     int* chunk_ctr;                     // growth chunk claims; reset here by the last CTA
     int* done;
+    const uint4* cq;                    // compact entries of the sparse strips (nullptr: none)
+    int* cq_ctr;                        // their count (may exceed cq_cap); reset here by the last CTA
+    int* cq_claim;                      // compact chunk claims; reset here by the last CTA
+    int cq_cap, out_rows;
 };
 
 
@@ -291,11 +317,14 @@ __global__ void __launch_bounds__(GNT, C::MINB) amf_grow_kernel(const __grid_con
     int* ctl_n = reinterpret_cast<int*>(smem + 1280);              // [4]
     uint64_t* bmbar = reinterpret_cast<uint64_t*>(smem + 1344);    // next batch's bitmap copies
     uint32_t* bms = reinterpret_cast<uint32_t*>(Q1 + C::CAP);      // [SLOTS][128]
+    uint64_t* cbar = reinterpret_cast<uint64_t*>(smem + 1416);     // [2] compact entry staging
     const int tid = threadIdx.x;
     const int per_slice = args.tiles_x * args.tiles_y;
     if (tid == 0) {
         for (int i = 0; i < C::SLOTS; ++i) mbar_init(&bar[i], 1);
         mbar_init(bmbar, 1);
+        mbar_init(&cbar[0], 1);
+        mbar_init(&cbar[1], 1);
         prefetch_tmap(&tm);
         fence_mbar_init();
     }
@@ -309,11 +338,97 @@ __global__ void __launch_bounds__(GNT, C::MINB) amf_grow_kernel(const __grid_con
         args.dst[(size_t)si[2] * args.dslice + row * args.dpitch + si[0] + (pix & 127)] = v;
         if (FIN) args.fin[(size_t)si[2] * args.fslice + row * args.fpitch + si[0] + (pix & 127)] = (uint8_t)k;
     };
+    // tile records first: the CTAs that have some join the compact chunk claims below late
     grow_range<FIN, GNT, decltype(out), C::SLOTS, C::CAP, C::NETMAX, C::DYN, 1ll << C::CHUNK_SHIFT>(&tm, geo, sm, args.bitmap, args.records, R, T,
                                                                      args.chunk_rec, args.chunk_ctr, per_slice,
                                                                      args.tiles_x,
                                                                      args.row_begin, args.rows, args.cols, args.smax,
                                                                      phases, out);
+    if (args.cq) {
+        // The sparse strips' failures (compact entries): chunks of ch entries claimed from a global counter
+        // (so CTAs busy with tile records above take fewer), bulk-copied into the tile slots, double-buffered;
+        // k = 5 from shared memory, two entries per thread.  The entries still open are listed in shared
+        // memory (Q0 / Q1 as int scratch) and get k = 7 from global memory on full warps afterwards (inline
+        // when the list is full).
+        __syncthreads();  // the slots and queues are free
+        const int nc = min(__ldcg(args.cq_ctr), args.cq_cap);
+        const uint4* cq = args.cq;
+        int* sc = reinterpret_cast<int*>(smem + 1408);
+        int* cclaim = reinterpret_cast<int*>(smem + 1432);  // [2] chunk in each staging buffer
+        int* open7 = reinterpret_cast<int*>(Q0);
+        constexpr int OCAP = C::CAP;  // 2 * CAP u16 = CAP ints
+        const int ch = min((C::SLOTS * geo.b_bytes / 128) & ~1, 512);  // entries per staging buffer
+        const int ntot = (nc + ch - 1) / ch;
+        uint4* stg = reinterpret_cast<uint4*>(bufs);  // [2][ch] entries
+        auto claim_issue = [&](int b) {
+            const int c = atomicAdd(args.cq_claim, 1);
+            cclaim[b] = c;
+            if (c < ntot) {
+                const int n = min(ch, nc - c * ch);
+                mbar_expect_tx(&cbar[b], (uint32_t)n * 64);
+                bulk_g2s(stg + (size_t)b * ch * 4, cq + (size_t)c * ch * 4, (uint32_t)n * 64, &cbar[b]);
+            }
+        };
+        if (tid == 0) {
+            *sc = 0;
+            fence_proxy_async_smem();
+            claim_issue(0);
+            claim_issue(1);
+        }
+        __syncthreads();
+        auto cout = [&](int k) {
+            return [&, k](uint32_t x, uint32_t key, uint32_t v) {
+                const uint32_t z = key / (uint32_t)args.out_rows, row = key - z * (uint32_t)args.out_rows;
+                args.dst[(size_t)z * args.dslice + (size_t)row * args.dpitch + x] = (uint8_t)v;
+                if (FIN) args.fin[(size_t)z * args.fslice + (size_t)row * args.fpitch + x] = (uint8_t)k;
+            };
+        };
+        const int lane = tid & 31;
+        for (int it = 0;; ++it) {
+            const int b = it & 1, c = cclaim[b];
+            if (c >= ntot) break;
+            mbar_wait(&cbar[b], (uint32_t)(it >> 1) & 1u);
+            const int n = min(ch, nc - c * ch);
+            const uint4* sb = stg + (size_t)b * ch * 4;
+            for (int p0 = 0; 2 * p0 < n; p0 += GNT) {
+                const int pi = p0 + tid;
+                uint32_t pend = 0;
+                int ia = 2 * pi, ib = 2 * pi + 1;
+                if (ia < n) {
+                    const bool hasb = ib < n;
+                    if (!hasb) ib = ia;
+                    pend = (sb[ia * 4 + 3].z != CQ_NONE ? 1u : 0u) | (hasb && sb[ib * 4 + 3].z != CQ_NONE ? 2u : 0u);
+                    if (pend) pend = compact_level<5>(sb + ia * 4, sb + ib * 4, pend, cout(5));
+                }
+                if (args.smax >= 7) {
+                    const uint32_t balA = __ballot_sync(0xFFFFFFFFu, pend & 1u);
+                    const uint32_t balB = __ballot_sync(0xFFFFFFFFu, pend & 2u);
+                    const int tot = __popc(balA) + __popc(balB);
+                    int base = 0;
+                    if (lane == 0 && tot) base = atomicAdd(sc, tot);
+                    base = __shfl_sync(0xFFFFFFFFu, base, 0);
+                    const uint32_t below = (1u << lane) - 1u;
+                    const int pa = base + __popc(balA & below), pb = base + __popc(balA) + __popc(balB & below);
+                    const int ga = c * ch + ia, gb = c * ch + ib;
+                    if (base + tot <= OCAP) {
+                        if (pend & 1u) open7[pa] = ga;
+                        if (pend & 2u) open7[pb] = gb;
+                    } else if (pend) {
+                        compact_level<7>(cq + (size_t)ga * 4, cq + (size_t)gb * 4, pend, cout(7));
+                    }
+                }
+            }
+            fence_proxy_async_smem();  // this buffer's generic reads before its next bulk copy
+            __syncthreads();           // (also publishes the claims made after the previous barrier)
+            if (tid == 0) claim_issue(b);
+        }
+        __syncthreads();
+        const int n7 = min(*sc, OCAP);
+        for (int j = tid; 2 * j < n7; j += GNT) {
+            const int ia = open7[2 * j], ib = 2 * j + 1 < n7 ? open7[2 * j + 1] : ia;
+            compact_level<7>(cq + (size_t)ia * 4, cq + (size_t)ib * 4, 2 * j + 1 < n7 ? 3u : 1u, cout(7));
+        }
+    }
     TRACE(1, 15);
     // the last CTA resets the record counter for the next k = 3 launch
     if (tid == 0) {
@@ -321,6 +436,10 @@ __global__ void __launch_bounds__(GNT, C::MINB) amf_grow_kernel(const __grid_con
         if (atomicAdd(args.done, 1) == (int)gridDim.x - 1) {
             *args.rec_ctr = 0;
             *args.chunk_ctr = 0;
+            if (args.cq) {
+                *args.cq_ctr = 0;
+                *args.cq_claim = 0;
+            }
             *args.done = 0;
         }
     }
@@ -552,10 +671,20 @@ cudaError_t launch_fused_amf(const Plane& p, int smax, uint8_t* fin, size_t fpit
 
 }  // namespace
 
+// Compact growth entries: one per 128 image pixels (at least 1024, at most 2^21 = 128 MiB); strips that
+// find the list full fall back to their tile's bitmap.
+inline int compact_cap(const Plane& p) {
+    static const int forced = getenv("HYB_COMPACT_CAP") ? atoi(getenv("HYB_COMPACT_CAP")) : 0;  // tests: overflow
+    if (forced > 0) return forced;
+    const long long npix = (long long)p.cols * (p.row_end - p.row_begin) * p.n_slices;
+    return (int)std::min<long long>(std::max<long long>(npix / 128, 1024), 1ll << 21);
+}
+
 size_t amf_work_bytes(const Plane& p) {
     const size_t tiles = (size_t)((p.cols + TW - 1) / TW) * ((p.row_end - p.row_begin + TH - 1) / TH) * p.n_slices;
     // chunk table: weighted total <= tiles * (TW * TH + REC_W) over chunks of >= 2048 -> <= 2.07 tiles + 1
-    return 64 + (tiles * 8 + 63) / 64 * 64 + tiles * 512 + (tiles * 3 + 16) * sizeof(int);
+    const size_t head = 64 + (tiles * 8 + 63) / 64 * 64 + tiles * 512 + (tiles * 3 + 16) * sizeof(int);
+    return (head + 127) / 128 * 128 + (size_t)compact_cap(p) * 64;
 }
 
 AmfWork amf_work(uint8_t* base, const Plane& p) {
@@ -565,6 +694,9 @@ AmfWork amf_work(uint8_t* base, const Plane& p) {
     w.records = reinterpret_cast<unsigned long long*>(base + 64);
     w.bitmap = base + 64 + (tiles * 8 + 63) / 64 * 64;
     w.chunk_rec = reinterpret_cast<int*>(w.bitmap + tiles * 512);
+    const size_t head = 64 + (tiles * 8 + 63) / 64 * 64 + tiles * 512 + (tiles * 3 + 16) * sizeof(int);
+    w.cq = reinterpret_cast<uint4*>(base + (head + 127) / 128 * 128);
+    w.cq_cap = compact_cap(p);
     return w;
 }
 
@@ -592,8 +724,14 @@ cudaError_t launch_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, si
     const int num_sms = device_sms();
     const int out_rows = p.row_end - p.row_begin;
     const bool grow = smax >= 5;
+    // compact growth windows for sparse strips (smax <= 7: 7 x 7 windows; key = slice * out_rows + row
+    // must fit 32 bits).  HYB_COMPACT_T = per-strip failure threshold (0: off; A/B).
+    static const int cq_thresh = getenv("HYB_COMPACT_T") ? atoi(getenv("HYB_COMPACT_T")) : HYB_COMPACT_T_DEF;
+    const bool compact = grow && smax <= 7 && cq_thresh > 0 && (long long)p.n_slices * out_rows < (1ll << 31) &&
+                         p.cols < (1 << 30);
+    const int halo = compact ? 3 : 1;
     CUtensorMap tm_src;
-    e = make_tmap_u8(&tm_src, p.src, p.cols, p.rows, p.n_slices, p.spitch, p.sslice, BS, BH);
+    e = make_tmap_u8(&tm_src, p.src, p.cols, p.rows, p.n_slices, p.spitch, p.sslice, BS, TH + 2 * halo);
     if (e != cudaSuccess) return e;
     K3Args a;
     a.dst = p.dst;
@@ -618,6 +756,12 @@ cudaError_t launch_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, si
     a.chunk_rec = work.chunk_rec;
     // the chunk table of the growth variant below: 2048-unit entries for guided claims
     a.chunk_shift = HYB_GUIDED ? 11 : smax >= HYB_WIDE_MIN_SMAX ? GrowWide::CHUNK_SHIFT : GrowLean::CHUNK_SHIFT;
+    a.halo = halo;
+    a.cq = compact ? work.cq : nullptr;
+    a.cq_ctr = work.counters + 6;
+    a.cq_cap = work.cq_cap;
+    a.cq_thresh = std::min(cq_thresh, 32);
+    a.out_rows = out_rows;
     const int per_sm = occupancy(occ_k3, (const void*)amf_k3_kernel<false>, K3T, SMEM);
     const long long ntiles = (long long)a.tiles_x * a.tiles_y * a.n_slices;
     const int grid = (int)std::min<long long>(ntiles, (long long)num_sms * per_sm);
@@ -664,6 +808,11 @@ cudaError_t launch_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, si
     g.chunk_rec = work.chunk_rec;
     g.chunk_ctr = work.counters + 5;
     g.done = work.counters + 4;
+    g.cq = a.cq;
+    g.cq_ctr = a.cq_ctr;
+    g.cq_claim = work.counters + 7;
+    g.cq_cap = a.cq_cap;
+    g.out_rows = out_rows;
     const int gper_sm = occupancy(gocc[vi], (const void*)kern, GNT, gsm);
     // every resident CTA slot busy; each CTA takes a contiguous run of tiles
     const int ggrid = (int)std::min<long long>(ntiles, (long long)num_sms * gper_sm);

@@ -60,6 +60,41 @@ __device__ __forceinline__ int zero_bytes(uint32_t x, uint32_t v80) {
     return __popc(~(t | x) & v80);
 }
 
+// Compact growth windows (sparse strips, smax <= 7): a strip with at most `thresh` level-A failures
+// writes each failure's whole 7 x 7 window (clamped to the source bounds) with its coordinates as one
+// 64-byte entry instead of setting bitmap bits, so the growth never reloads its tile: words 2r, 2r + 1
+// = window row r (bytes 0..6 = columns x - 3 .. x + 3), word 14 = x (0xFFFFFFFF: no entry), word 15 =
+// slice * out_rows + output row.  B: the tile buffer with a 3-row halo (row 0 = image row y0 - 3).
+struct CompactOut {
+    uint4* ent;
+    int* ctr;
+    int cap, thresh;
+    const uint8_t* B;
+    uint32_t x0, key0;  // tile column, slice * out_rows + tile output row
+};
+constexpr uint32_t CQ_NONE = 0xFFFFFFFFu;
+#ifndef HYB_COMPACT_COOP
+#define HYB_COMPACT_COOP 0  // 1: warp-cooperative entry writes (measured slower: config 3 k = 3 kernel 236 vs 213 us)
+#endif
+
+__device__ __forceinline__ void compact_emit(const CompactOut& co, int tr, int tc, int pos) {
+    const int start = CP + tc - 3;
+    const uint32_t* wp = reinterpret_cast<const uint32_t*>(co.B + tr * BS + (start & ~3));
+    const int sh = 8 * (start & 3);
+    uint32_t w[16];
+#pragma unroll
+    for (int r = 0; r < 7; ++r) {
+        const uint32_t a = wp[r * (BS / 4)], b = wp[r * (BS / 4) + 1], c = wp[r * (BS / 4) + 2];
+        w[2 * r] = __funnelshift_r(a, b, sh);
+        w[2 * r + 1] = __funnelshift_r(b, c, sh);
+    }
+    w[14] = co.x0 + (uint32_t)tc;
+    w[15] = co.key0 + (uint32_t)tr;
+    uint4* e = co.ent + (size_t)pos * 4;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) e[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+}
+
 // k = 3 for one 4-row strip of a 128 x 32 tile (one warp).  B: the tile's byte rows at stride BS,
 // row 0 = image row y0 - 1, column CP = image column x0 (edges already replicated).  Writes the
 // strip's output rows through dst_tile / fin_tile (image row y0, column x0; rows >= tile_row_lim or
@@ -72,7 +107,7 @@ template <bool FIN>
 __device__ __forceinline__ int k3_strip(const uint8_t* __restrict__ B, uint8_t* O, uint8_t* F, int sub,
                                         uint8_t* bm_tile, uint8_t* dst_tile, size_t dpitch, uint8_t* fin_tile,
                                         size_t fpitch, int tile_row_lim, int col_lim, uint16_t* q = nullptr,
-                                        int* qctr = nullptr, uint32_t qslot = 0) {
+                                        int* qctr = nullptr, uint32_t qslot = 0, const CompactOut* co = nullptr) {
     const int lane = threadIdx.x & 31;
     // ---- k = 3: lane = rows (r0, r0+1) x columns c0..c0+7, u16x2 lanes = the two rows ----
     const int lr = 2 * (lane >> 4);  // local row within the strip
@@ -168,6 +203,66 @@ __device__ __forceinline__ int k3_strip(const uint8_t* __restrict__ B, uint8_t* 
         if (c0 + 8 > col_lim) {
             const uint32_t cm = col_lim <= c0 ? 0u : ((1u << (col_lim - c0)) - 1u);
             m &= cm | (cm << 8);
+        }
+        if (co) {  // sparse strip: windows to the compact list (all or none of the strip's failures)
+            const int cl = __popc(m);
+            const int nfw = __reduce_add_sync(0xFFFFFFFFu, cl);
+            if (nfw > 0 && nfw <= co->thresh) {
+                int base = 0;
+                if (lane == 0) base = atomicAdd(co->ctr, nfw);
+                base = __shfl_sync(0xFFFFFFFFu, base, 0);
+                if (base + nfw <= co->cap) {
+#if HYB_COMPACT_COOP
+                    // warp-cooperative: one failure at a time, lanes 0..6 copy its window rows, lane 7 the
+                    // coordinates -- one coalesced 64-byte store per failure
+                    uint32_t act = __ballot_sync(0xFFFFFFFFu, m != 0);
+                    int pos = base;
+                    const uint32_t* rowp = nullptr;
+                    int sh = 0;
+                    while (act) {
+                        const int src = __ffs(act) - 1;
+                        act &= act - 1;
+                        uint32_t mm = __shfl_sync(0xFFFFFFFFu, m, src);
+                        const int tr0 = sub * WR + 2 * (src >> 4), tc0 = 8 * (src & 15);
+                        while (mm) {
+                            const int b = __ffs(mm) - 1;
+                            mm &= mm - 1;
+                            const int tr = tr0 + (b >> 3), tc = tc0 + (b & 7);
+                            if (lane < 8) {
+                                uint2 val;
+                                if (lane < 7) {
+                                    const int start = CP + tc - 3;
+                                    rowp = reinterpret_cast<const uint32_t*>(co->B + (tr + lane) * BS + (start & ~3));
+                                    sh = 8 * (start & 3);
+                                    const uint32_t x = rowp[0], y = rowp[1], z = rowp[2];
+                                    val = make_uint2(__funnelshift_r(x, y, sh), __funnelshift_r(y, z, sh));
+                                } else {
+                                    val = make_uint2(co->x0 + (uint32_t)tc, co->key0 + (uint32_t)tr);
+                                }
+                                reinterpret_cast<uint2*>(co->ent + (size_t)pos * 4)[lane] = val;
+                            }
+                            ++pos;
+                        }
+                    }
+                    m = 0;
+#else
+                    int incl = cl;
+#pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const int v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+                        if (lane >= d) incl += v;
+                    }
+                    int pos = base + incl - cl;
+                    while (m) {
+                        const int b = __ffs(m) - 1;
+                        m &= m - 1;
+                        compact_emit(*co, sub * WR + lr + (b >> 3), c0 + (b & 7), pos++);
+                    }
+#endif
+                } else if (lane < co->cap - base) {  // reservation straddles the end: void its entries
+                    co->ent[(size_t)(base + lane) * 4 + 3].z = CQ_NONE;
+                }
+            }
         }
         if (bm_tile) {
             uint8_t* bm = bm_tile + (sub * WR + lr) * 16 + (c0 >> 3);
@@ -348,6 +443,46 @@ __device__ __forceinline__ void level_pair2(const uint8_t* __restrict__ BA, cons
             outw |= ((zn < gl && gl < zx) ? gl : zd) << (8 * l);
         }
     }
+}
+
+// Level k = K (5 or 7) of two compact entries (CompactOut; in shared or global memory) in the u16x2
+// lanes of one thread: the k = 5 window is the entry's centre 5 x 5, k = 7 its whole window.  `pend` bit l: entry l still open (and
+// valid); out(x, key, value) stores a resolved pixel.  Returns the entries still open after level K
+// (unresolved pixels keep the input the k = 3 pass wrote).
+template <int K, class Out>
+__device__ __forceinline__ uint32_t compact_level(const uint4* __restrict__ ea, const uint4* __restrict__ eb,
+                                                  uint32_t pend, Out out) {
+    const uint4 ca = ea[3], cb = eb[3];  // row 6 + coordinates
+    constexpr int O = (7 - K) / 2;                          // window offset in the 7 x 7 entry
+    uint32_t v[K * K];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        if (2 * q + 1 < O || 2 * q >= O + K) continue;
+        const uint4 x = q < 3 ? ea[q] : ca, y = q < 3 ? eb[q] : cb;
+        const uint32_t A[4] = {x.x, x.y, x.z, x.w}, Bw[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {  // entry row 2q + h = words 4q + 2h, 4q + 2h + 1
+            const int r = 2 * q + h - O;
+            if (r >= 0 && r < K) {
+#pragma unroll
+                for (int e = 0; e < K; ++e)
+                    v[r * K + e] = pairw_rt(A[2 * h + ((e + O) >> 2)], Bw[2 * h + ((e + O) >> 2)], (e + O) & 3);
+            }
+        }
+    }
+    const uint32_t g = v[(K * K) / 2];
+    uint32_t zmin, zmed, zmax;
+    select_net<K>(v, zmin, zmed, zmax);
+#pragma unroll
+    for (int l = 0; l < 2; ++l) {
+        const uint32_t zn = (zmin >> (16 * l)) & 0xFFu, zd = (zmed >> (16 * l)) & 0xFFu;
+        const uint32_t zx = (zmax >> (16 * l)) & 0xFFu, gl = (g >> (16 * l)) & 0xFFu;
+        if ((pend >> l & 1u) && zn < zd && zd < zx) {
+            out(l ? cb.z : ca.z, l ? cb.w : ca.w, (zn < gl && gl < zx) ? gl : zd);
+            pend &= ~(1u << l);
+        }
+    }
+    return pend;
 }
 
 // Count of window values equal to v (SWAR over the aligned window words).

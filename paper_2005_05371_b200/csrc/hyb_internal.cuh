@@ -85,10 +85,12 @@ struct Plane {
 // level-A failures, and the per-tile failure bitmap (512 bytes per 128 x 32 tile).
 struct AmfWork {
     int* counters;                 // [0..1] record counter (u64), [2] tile claims, [3] / [4] CTAs done,
-                                   // [5] growth chunk claims
+                                   // [5] growth chunk claims, [6] compact growth entries, [7] their chunk claims
     unsigned long long* records;   // (failure offset << 24) | tile
     uint8_t* bitmap;
     int* chunk_rec;                // [chunk]: the record holding weighted position chunk * CHUNK
+    uint4* cq;                     // compact growth entries (64 bytes each), counter = counters[6]
+    int cq_cap;
 };
 size_t amf_work_bytes(const Plane& p);
 AmfWork amf_work(uint8_t* base, const Plane& p);

@@ -106,6 +106,14 @@ __device__ __forceinline__ void replicate_edges(uint8_t* T, int width, int c_lo,
     else __syncthreads();
 }
 
+// Bulk copy global -> shared (cp.async.bulk, 16-byte aligned, bytes a multiple of 16), completing on bar.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
 // 3-D tiled TMA load (x = column, y = row, z = slice); out-of-bounds elements read as zero.
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y,
                                             int z) {
