@@ -223,7 +223,6 @@ constexpr int GNT = HYB_GNT;     // threads per growth CTA
 
 constexpr int GHDR = 1536;       // mbarriers, tile coordinates, level counters, scan scratch
 
-inline size_t grow_smem(const GGeo& g);
 
 struct GArgs {
     GGeo geo;
@@ -243,6 +242,7 @@ struct GArgs {
     int* cq_ctr;                        // their count (may exceed cq_cap); reset here by the last CTA
     int* cq_claim;                      // compact chunk claims; reset here by the last CTA
     int cq_cap, out_rows;
+    int fast;                           // plane words per slot of the fast growth levels (0: plain levels)
 };
 
 
@@ -293,9 +293,13 @@ static_assert(GrowWide::SLOTS <= 8 && GrowLean::SLOTS <= 8, "header layout");
 static_assert(GrowWide::SLOTS <= GNT / 32 && GrowLean::SLOTS <= GNT / 32, "queue build: one warp per slot");
 static_assert(GrowWide::CHUNK_SHIFT >= 11 && GrowLean::CHUNK_SHIFT >= 11, "chunk table sized for chunks >= 2048");
 
+// plane words (uint2) per slot of the fast growth levels: one per 32 tile bytes, one of padding, 16-byte multiple
+inline int plane_stride(const GGeo& g) { return (g.BH * (g.BS >> 5) + 2) & ~1; }
+
 template <class C>
-inline size_t grow_smem(const GGeo& g) {
-    return GHDR + (size_t)C::SLOTS * g.b_bytes + 2 * C::CAP * 2 + (size_t)C::SLOTS * 512 + 128;
+inline size_t grow_smem(const GGeo& g, bool fast = false) {
+    return GHDR + (size_t)C::SLOTS * g.b_bytes + 2 * C::CAP * 2 + (size_t)C::SLOTS * 512 + 128 +
+           (fast ? (size_t)C::SLOTS * plane_stride(g) * 8 : 0);
 }
 
 
@@ -332,7 +336,11 @@ __global__ void __launch_bounds__(GNT, C::MINB) amf_grow_kernel(const __grid_con
     const unsigned long long ctr = __ldcg(args.rec_ctr);
     const long long R = (long long)(ctr >> REC_SHIFT), T = (long long)(ctr & REC_MASK);
     uint32_t phases = 0;
-    const GrowSmem sm{bar, sinfo, cur, ctl, qcount, bufs, Q0, Q1, sinfo_n, ctl_n, bms, bmbar};
+    GrowSmem sm{bar, sinfo, cur, ctl, qcount, bufs, Q0, Q1, sinfo_n, ctl_n, bms, bmbar};
+    if (args.fast) {  // zero / 255 bit planes behind the bitmaps (16-byte aligned)
+        sm.planes = reinterpret_cast<uint2*>(bms + C::SLOTS * 128);
+        sm.pstride = args.fast;
+    }
     auto out = [&](const int* si, int pix, uint8_t v, int k) {
         const size_t row = (size_t)(si[1] - args.row_begin + (pix >> 7));
         args.dst[(size_t)si[2] * args.dslice + row * args.dpitch + si[0] + (pix & 127)] = v;
@@ -773,7 +781,10 @@ cudaError_t launch_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, si
     // ---- growth: one batched launch for every window size k = 5..smax ----
     const GGeo geo = make_ggeo(smax);
     const bool wide = smax >= HYB_WIDE_MIN_SMAX;
-    const size_t gsm = wide ? grow_smem<GrowWide>(geo) : grow_smem<GrowLean>(geo);
+    // zero / 255 bit-plane levels (amf_core.cuh grow_levels_fast) for the wide variant; HYB_GROW_FAST=0: plain levels (A/B)
+    static const bool fast_env = !(getenv("HYB_GROW_FAST") && atoi(getenv("HYB_GROW_FAST")) == 0);
+    const bool fast = wide && fast_env && (smax - 1) / 2 <= 16;
+    const size_t gsm = wide ? grow_smem<GrowWide>(geo, fast) : grow_smem<GrowLean>(geo);
     auto kern = wide ? (fin ? amf_grow_kernel<true, GrowWide> : amf_grow_kernel<false, GrowWide>)
                      : (fin ? amf_grow_kernel<true, GrowLean> : amf_grow_kernel<false, GrowLean>);
     const int vi = (fin ? 1 : 0) + (wide ? 2 : 0);
@@ -813,6 +824,7 @@ cudaError_t launch_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, si
     g.cq_claim = work.counters + 7;
     g.cq_cap = a.cq_cap;
     g.out_rows = out_rows;
+    g.fast = fast ? plane_stride(geo) : 0;
     const int gper_sm = occupancy(gocc[vi], (const void*)kern, GNT, gsm);
     // every resident CTA slot busy; each CTA takes a contiguous run of tiles
     const int ggrid = (int)std::min<long long>(ntiles, (long long)num_sms * gper_sm);

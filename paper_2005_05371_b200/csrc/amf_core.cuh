@@ -861,6 +861,357 @@ __device__ __forceinline__ void grow_levels(const uint8_t* bufs, const GGeo& geo
     grow_levels_at<FIN, NTHR, decltype(slot), Out, NETMAX>(slot, geo, Q0, Q1, qcount, n, smax, out);
 }
 
+// ------------------------------------------------------------------------------------------
+// Fast growth levels: zero / 255 bit planes
+// ------------------------------------------------------------------------------------------
+//
+// Under heavy salt & pepper nearly every window of a growing pixel holds both a 0 and a 255, so
+// zmin = 0 and zmax = 255 are known without looking at the values, level A (zmin < zmed < zmax) is
+// #(v == 0) <= m and #(v == 255) <= m, and level B keeps g unless g is 0 or 255 -- the window median
+// is needed only at the level where A passes, and only for an impulse centre.  The counts come from
+// two bit planes of the staged tile (bit = byte is 0 / byte is 255; build_planes), a few funnel
+// shifts and one POPC per 32 window bits instead of a selection network per level.  Windows are
+// nested, so a pixel whose 5 x 5 window lacks a 0 or a 255 is the only kind the shortcut cannot
+// decide: it is flagged (entry bit 15) and takes the generic zmin / zmed / zmax test at every level,
+// sharing the median pass with the flagged-free entries.
+
+// Bit planes of `ns` staged tiles: planes[sl][row * PW + w] = (zero bits, 255 bits) of the 32 tile
+// bytes at 32 (row * PW + w) (BS = 32 PW, so plane words and tile bytes are both linear).
+template <int NTHR>
+__device__ __forceinline__ void build_planes(const uint8_t* bufs, const GGeo& geo, uint2* planes, int pstride, int ns) {
+    const int per = geo.BH * (geo.BS >> 5);
+    for (int t = threadIdx.x; t < ns * per; t += NTHR) {
+        const int sl = t / per, q = t - sl * per;
+        const uint4* src = reinterpret_cast<const uint4*>(bufs + (size_t)sl * geo.b_bytes + 32 * q);
+        const uint4 lo = src[0], hi = src[1];
+        const uint32_t x[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+        uint32_t e0 = 0, e1 = 0;
+#pragma unroll
+        for (int j = 7; j >= 0; --j) {
+            const uint32_t t7 = x[j] & 0x7F7F7F7Fu;
+            const uint32_t z = ~((t7 + 0x7F7F7F7Fu) | x[j]) & 0x80808080u;  // byte MSB: byte == 0
+            const uint32_t f = (t7 + 0x01010101u) & x[j] & 0x80808080u;      // byte MSB: byte == 255
+            // the four MSBs gathered into the top nibble by one multiply, shifted into the plane word
+            e0 = __funnelshift_l(z * 0x00204081u, e0, 4);
+            e1 = __funnelshift_l(f * 0x00204081u, e1, 4);
+        }
+        planes[(size_t)sl * pstride + q] = make_uint2(e0, e1);
+    }
+}
+
+// #(v == 0) and #(v == 255) of the K x K window around tile pixel (ty, tx), from the tile's planes.
+template <int K>
+__device__ __forceinline__ void plane_counts(const uint2* __restrict__ P, const GGeo& geo, int ty, int tx, int& c0,
+                                             int& c255) {
+    constexpr int RK = K / 2, RPW = 32 / K;  // window rows packed per 32-bit word
+    constexpr uint32_t MASK = (1u << K) - 1u;
+    const int PW = geo.BS >> 5, cs = tx + geo.CP - RK, sh = cs & 31;
+    const uint2* row = P + (size_t)(ty + geo.R - RK) * PW + (cs >> 5);
+    uint32_t a0 = 0, a1 = 0;
+    c0 = 0;
+    c255 = 0;
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+        const uint2 lo = row[r * PW], hi = row[r * PW + 1];  // (the plane is padded by one word)
+        a0 = a0 * (1u << K) + (__funnelshift_r(lo.x, hi.x, sh) & MASK);
+        a1 = a1 * (1u << K) + (__funnelshift_r(lo.y, hi.y, sh) & MASK);
+        if ((r + 1) % RPW == 0 || r == K - 1) {
+            c0 += __popc(a0);
+            c255 += __popc(a1);
+            a0 = a1 = 0;
+        }
+    }
+}
+
+// Bit-sliced box counts of one plane for one tile row: e[i][j] = plane word j (of 5) of window row i (of
+// 5).  For every column, le12 / any = the 5 x 5 window holds <= 12 / >= 1 set bits.  Vertical sums as
+// 3-bit numbers (two full adders per word), five horizontally shifted copies added by carry-save adders:
+// ~45 LOP3 / SHF per 32 pixels, against one selection network per pixel.
+__device__ __forceinline__ uint32_t xor3(uint32_t a, uint32_t b, uint32_t c) { return a ^ b ^ c; }
+__device__ __forceinline__ uint32_t maj3(uint32_t a, uint32_t b, uint32_t c) { return (a & b) | (c & (a | b)); }
+
+__device__ __forceinline__ void box5_counts(const uint32_t (&e)[5][5], uint32_t (&le12)[5], uint32_t (&any)[5]) {
+    uint32_t v[3][7];  // vertical sums, bit b of word j at v[b][j + 1]; zero words either side
+#pragma unroll
+    for (int b = 0; b < 3; ++b) v[b][0] = v[b][6] = 0u;
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+        const uint32_t s1 = xor3(e[0][j], e[1][j], e[2][j]), c1 = maj3(e[0][j], e[1][j], e[2][j]);
+        v[0][j + 1] = xor3(s1, e[3][j], e[4][j]);
+        const uint32_t c2 = maj3(s1, e[3][j], e[4][j]);
+        v[1][j + 1] = c1 ^ c2;
+        v[2][j + 1] = c1 & c2;
+    }
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+        uint32_t t[3], c[3], d[3];
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+            const uint32_t A = __funnelshift_l(v[b][j], v[b][j + 1], 2);      // column - 2
+            const uint32_t B = __funnelshift_l(v[b][j], v[b][j + 1], 1);      // column - 1
+            const uint32_t C = v[b][j + 1];
+            const uint32_t D = __funnelshift_r(v[b][j + 1], v[b][j + 2], 1);  // column + 1
+            const uint32_t E = __funnelshift_r(v[b][j + 1], v[b][j + 2], 2);  // column + 2
+            const uint32_t s = xor3(A, B, C);
+            c[b] = maj3(A, B, C);
+            t[b] = xor3(s, D, E);
+            d[b] = maj3(s, D, E);
+        }
+        // t[b] weighs 2^b, c[b] and d[b] 2^(b+1)
+        const uint32_t r0 = t[0];
+        const uint32_t r1 = xor3(t[1], c[0], d[0]), k1 = maj3(t[1], c[0], d[0]);
+        const uint32_t u = xor3(t[2], c[1], d[1]), ku = maj3(t[2], c[1], d[1]);
+        const uint32_t r2 = u ^ k1, kv = u & k1;
+        const uint32_t w = xor3(c[2], d[2], ku), kw = maj3(c[2], d[2], ku);
+        const uint32_t r3 = w ^ kv, kx = w & kv;
+        const uint32_t r4 = kw | kx;
+        le12[j] = ~(r4 | (r3 & r2 & (r1 | r0)));  // count < 13
+        any[j] = r0 | r1 | r2 | r3 | r4;
+    }
+}
+
+// Level k = 5 for whole tiles at once (thread = one row of one staged tile; geo.CP == 16, BS == 160).
+// f3m[sl][128] holds the slot's level-A failures of k = 3 (bitmap words 4 row + q) on entry; on return
+// the pixels whose k = 5 median is needed (impulse centres that pass level A, and every pixel whose
+// window lacks a 0 or a 255 -- the generic test decides those), bs7[sl][128] the pixels still open.
+// Pixels that pass with a non-impulse centre keep g, which f already holds (FIN: they go through the
+// median pass so finalized_at gets its 5).
+template <int NTHR, bool FIN>
+__device__ __forceinline__ void dense_level5(const uint2* planes, int pstride, const GGeo& geo, int ns, uint32_t* f3m,
+                                             uint32_t* bs7) {
+    for (int t = threadIdx.x; t < ns * TH; t += NTHR) {
+        const int sl = t / TH, row = t - sl * TH;
+        const uint2* P = planes + (size_t)sl * pstride + (row + geo.R - 2) * 5;
+        uint32_t e0[5][5], e1[5][5];
+#pragma unroll
+        for (int i = 0; i < 5; ++i)
+#pragma unroll
+            for (int j = 0; j < 5; ++j) {
+                const uint2 w = P[i * 5 + j];
+                e0[i][j] = w.x;
+                e1[i][j] = w.y;
+            }
+        uint32_t le0[5], any0[5], le1[5], any1[5], dm[5], ds[5];
+        box5_counts(e0, le0, any0);
+        box5_counts(e1, le1, any1);
+#pragma unroll
+        for (int j = 0; j < 5; ++j) {
+            const uint32_t pass = le0[j] & le1[j], elig = any0[j] & any1[j], ext = e0[2][j] | e1[2][j];
+            dm[j] = FIN ? (~elig | pass) : (~elig | (pass & ext));
+            ds[j] = elig & ~pass;
+        }
+        uint4* fm = reinterpret_cast<uint4*>(f3m + sl * 128 + 4 * row);
+        const uint4 f = *fm;
+        // plane bit 16 + c = tile column c
+        *fm = make_uint4(f.x & __funnelshift_r(dm[0], dm[1], 16), f.y & __funnelshift_r(dm[1], dm[2], 16),
+                         f.z & __funnelshift_r(dm[2], dm[3], 16), f.w & __funnelshift_r(dm[3], dm[4], 16));
+        *reinterpret_cast<uint4*>(bs7 + sl * 128 + 4 * row) =
+            make_uint4(f.x & __funnelshift_r(ds[0], ds[1], 16), f.y & __funnelshift_r(ds[1], ds[2], 16),
+                       f.z & __funnelshift_r(ds[2], ds[3], 16), f.w & __funnelshift_r(ds[3], ds[4], 16));
+    }
+}
+
+// Queues of the fast levels.  Level index l <-> k = 5 + 2 l; |S_k| = qcount[2 l], |M_k| = qcount[2 l + 1].
+// S_k (open pixels, unflagged, plane-testable) sits at the front of a buffer, M_k (pixels whose level-k
+// median is needed: impulse centres that passed A, and every flagged pixel) at its tail, growing down.
+constexpr int FAST_FLAG = 0x8000;
+
+// Pass A of level K: plane test of S_K = X[0, nS) -> S_K+2 (front of Y), M_K (tail of Y), or the pixel keeps g.
+template <bool FIN, int NTHR, int CAP, int K, class Slot, class PlaneOf, class Out>
+__device__ __forceinline__ void fast_pass_a(Slot slot, PlaneOf plane, const GGeo& geo, const uint16_t* X, uint16_t* Y,
+                                            int nS, int* cSn, int* cM, bool last, int wrot, Out out) {
+    constexpr int NWARP = NTHR / 32;
+    const int lane = threadIdx.x & 31, warp = ((threadIdx.x >> 5) + NWARP - wrot) % NWARP;
+    const uint32_t below = (1u << lane) - 1u;
+    constexpr int M = (K * K - 1) / 2;
+    for (int base = warp * 32; base < nS; base += NTHR) {
+        const int i = base + lane;
+        int cls = 0, e = 0;  // 1: still open, 2: median needed
+        if (i < nS) {
+            e = X[i];
+            const int sl = e >> 12, pix = e & 4095, ty = pix >> 7, tx = pix & 127;
+            if (K <= 11) {
+                int c0, c255;
+                plane_counts<(K <= 11 ? K : 11)>(plane(sl), geo, ty, tx, c0, c255);
+                if (c0 > M || c255 > M) {
+                    cls = last ? 0 : 1;
+                } else {
+                    const uint32_t g = slot(sl)[(size_t)(ty + geo.R) * geo.BS + tx + geo.CP];
+                    if (g != 0u && g != 255u) {
+                        if (FIN) out(sl, pix, (uint8_t)g, K);  // f already holds g (the k = 3 pass wrote it)
+                    } else {
+                        cls = 2;
+                    }
+                }
+            } else {
+                cls = 2;  // beyond the plane tests: the generic level decides
+            }
+        }
+        const uint32_t balS = __ballot_sync(0xFFFFFFFFu, cls == 1);
+        const uint32_t balM = __ballot_sync(0xFFFFFFFFu, cls == 2);
+        if (balS) {
+            int qb = 0;
+            if (lane == 0) qb = atomicAdd(cSn, __popc(balS));
+            qb = __shfl_sync(0xFFFFFFFFu, qb, 0);
+            if (cls == 1) Y[qb + __popc(balS & below)] = (uint16_t)e;
+        }
+        if (balM) {
+            int qb = 0;
+            if (lane == 0) qb = atomicAdd(cM, __popc(balM));
+            qb = __shfl_sync(0xFFFFFFFFu, qb, 0);
+            if (cls == 2) Y[CAP - 1 - (qb + __popc(balM & below))] = (uint16_t)e;
+        }
+    }
+}
+
+// Pass B of level K: the median pass over M_K = tail of X, nM entries; flagged pixels that fail the
+// generic level A move to M_K+2 (tail of Y, flagged).
+template <bool FIN, int NTHR, int CAP, int K, int NETMAX, class Slot, class Out>
+__device__ __forceinline__ void fast_pass_b(Slot slot, const GGeo& geo, const uint16_t* X, uint16_t* Y, int nM, int* cMn,
+                                            bool last, Out out) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t below = (1u << lane) - 1u;
+    const uint16_t* Mq = X + CAP - 1;  // entry j at Mq[-j]
+    if constexpr (K <= NETMAX && K <= 9) {
+        const int npairs = (nM + 1) >> 1;
+        for (int base = warp * 32; base < npairs; base += NTHR) {
+            const int i = base + lane;
+            uint32_t keep = 0;
+            int ea = 0, eb = 0;
+            if (i < npairs) {
+                ea = Mq[-2 * i];
+                const bool hasb = 2 * i + 1 < nM;
+                eb = hasb ? Mq[-(2 * i + 1)] : ea;
+                const int sa = (ea >> 12) & 7, pa = ea & 4095, sb = (eb >> 12) & 7, pb = eb & 4095;
+                uint32_t done, outw;
+                level_pair2<K>(slot(sa), slot(sb), geo, pa, pb, done, outw);
+                if (done & 1u) out(sa, pa, (uint8_t)outw, K);
+                else keep |= 1u;
+                if (hasb) {
+                    if (done & 2u) out(sb, pb, (uint8_t)(outw >> 8), K);
+                    else keep |= 2u;
+                }
+            }
+            if (!last) {  // only pixels whose windows lack a 0 or a 255 can fail here
+                const uint32_t balA = __ballot_sync(0xFFFFFFFFu, keep & 1u);
+                const uint32_t balB = __ballot_sync(0xFFFFFFFFu, keep & 2u);
+                const int c = __popc(balA) + __popc(balB);
+                if (c) {
+                    int qb = 0;
+                    if (lane == 0) qb = atomicAdd(cMn, c);
+                    qb = __shfl_sync(0xFFFFFFFFu, qb, 0);
+                    if (keep & 1u) Y[CAP - 1 - (qb + __popc(balA & below))] = (uint16_t)(ea | FAST_FLAG);
+                    if (keep & 2u) Y[CAP - 1 - (qb + __popc(balA) + __popc(balB & below))] = (uint16_t)(eb | FAST_FLAG);
+                }
+            }
+        }
+    } else {
+        for (int base = warp * 32; base < nM; base += NTHR) {
+            const int i = base + lane;
+            bool keep = false;
+            int e = 0;
+            if (i < nM) {
+                e = Mq[-i];
+                const int sl = (e >> 12) & 7, pix = e & 4095, ty = pix >> 7, tx = pix & 127;
+                const uint8_t* B = slot(sl);
+                uint8_t o = 0;
+                if constexpr (K == 9 || K == 11) {
+                    int st = 2;  // unflagged: level A passed and g is an impulse -> the median
+                    if (e & FAST_FLAG) st = level_radix_test<K>(B, geo, ty, tx, &o);
+                    if (st == 2) o = level_radix_median<K>(B, geo, ty, tx);
+                    if (st) out(sl, pix, o, K);
+                    keep = st == 0;
+                } else {
+                    keep = true;  // generic levels: fast_pass_generic
+                }
+            }
+            if (!last) {
+                const uint32_t bal = __ballot_sync(0xFFFFFFFFu, keep);
+                if (bal) {
+                    int qb = 0;
+                    if (lane == 0) qb = atomicAdd(cMn, __popc(bal));
+                    qb = __shfl_sync(0xFFFFFFFFu, qb, 0);
+                    if (keep) Y[CAP - 1 - (qb + __popc(bal & below))] = (uint16_t)(e | FAST_FLAG);
+                }
+            }
+        }
+    }
+}
+
+// Levels k >= 13 (beyond the plane tests and the unrolled selects): every entry of S_k (front of X) and
+// M_k (tail of X) takes the generic level; failures move to M_k+2 (tail of Y).
+template <int NTHR, int CAP, class Slot, class Out>
+__device__ __forceinline__ void fast_pass_generic(Slot slot, const GGeo& geo, const uint16_t* X, uint16_t* Y, int nS, int nM,
+                                                  int* cMn, int k, bool last, Out out) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t below = (1u << lane) - 1u;
+    for (int base = warp * 32; base < nS + nM; base += NTHR) {
+        const int i = base + lane;
+        bool keep = false;
+        int e = 0;
+        if (i < nS + nM) {
+            e = i < nS ? X[i] : X[CAP - 1 - (i - nS)];
+            const int sl = (e >> 12) & 7, pix = e & 4095;
+            uint8_t o = 0;
+            if (level_generic(slot(sl), geo, pix >> 7, pix & 127, k, &o)) out(sl, pix, o, k);
+            else keep = true;
+        }
+        if (!last) {
+            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, keep);
+            if (bal) {
+                int qb = 0;
+                if (lane == 0) qb = atomicAdd(cMn, __popc(bal));
+                qb = __shfl_sync(0xFFFFFFFFu, qb, 0);
+                if (keep) Y[CAP - 1 - (qb + __popc(bal & below))] = (uint16_t)(e | FAST_FLAG);
+            }
+        }
+    }
+}
+
+// Growth levels with the plane shortcut, after dense_level5 and the queue build: Q0 holds S_7 at its
+// front (qcount[2] entries) and M_5 at its tail (qcount[1]); qcount[3..] zero.  Interval i runs pass B of
+// level kB = 5 + 2 i and pass A of level kB + 2 between two barriers (both read one buffer and write
+// the other; the selection network of one level and the plane test of the next share the instruction
+// cache, and the short tests fill the median pass's tail).  CTA-wide; ends with __syncthreads.
+template <bool FIN, int NTHR, int CAP, class Slot, class PlaneOf, class Out, int NETMAX = HYB_GROW_NETMAX>
+__device__ __forceinline__ void grow_levels_fast(Slot slot, PlaneOf plane, const GGeo& geo, uint16_t* Q0, uint16_t* Q1,
+                                                 int* qcount, int smax, Out out) {
+    constexpr int NWARP = NTHR / 32;
+    for (int i = 0;; ++i) {
+        const int kB = 5 + 2 * i, kA = kB + 2;
+        if (kB > smax) break;
+        const uint16_t* X = (i & 1) ? Q1 : Q0;
+        uint16_t* Y = (i & 1) ? Q0 : Q1;
+        const int nM = qcount[2 * i + 1], nS = kA <= smax ? qcount[2 * i + 2] : 0;
+        int* cMn = &qcount[2 * i + 3];  // |M_kA|
+        int* cSn = &qcount[2 * i + 4];  // |S_kA+2|
+        const bool lastB = kB + 2 > smax, lastA = kA + 2 > smax;
+        if (kB > 11) {
+            // S_kB is empty unless this is the first generic level (pass A below routes everything to M)
+            fast_pass_generic<NTHR, CAP>(slot, geo, X, Y, 0, nM, cMn, kB, lastB, out);
+        } else if (kB == 5) {
+            fast_pass_b<FIN, NTHR, CAP, 5, NETMAX>(slot, geo, X, Y, nM, cMn, lastB, out);
+        } else if (kB == 7) {
+            fast_pass_b<FIN, NTHR, CAP, 7, NETMAX>(slot, geo, X, Y, nM, cMn, lastB, out);
+        } else if (kB == 9) {
+            fast_pass_b<FIN, NTHR, CAP, 9, NETMAX>(slot, geo, X, Y, nM, cMn, lastB, out);
+        } else {
+            fast_pass_b<FIN, NTHR, CAP, 11, NETMAX>(slot, geo, X, Y, nM, cMn, lastB, out);
+        }
+        // the warps with one median round fewer start the tests
+        const int per = (kB <= NETMAX && kB <= 9) ? 64 : 32;
+        const int wrot = ((nM + per - 1) / per) % NWARP;
+        if (nS > 0) {
+            if (kA == 7) fast_pass_a<FIN, NTHR, CAP, 7>(slot, plane, geo, X, Y, nS, cSn, cMn, lastA, wrot, out);
+            else if (kA == 9) fast_pass_a<FIN, NTHR, CAP, 9>(slot, plane, geo, X, Y, nS, cSn, cMn, lastA, wrot, out);
+            else if (kA == 11) fast_pass_a<FIN, NTHR, CAP, 11>(slot, plane, geo, X, Y, nS, cSn, cMn, lastA, wrot, out);
+            else fast_pass_a<FIN, NTHR, CAP, 13>(slot, plane, geo, X, Y, nS, cSn, cMn, lastA, wrot, out);
+        }
+        __syncthreads();
+        if (*cMn == 0 && (lastA || *cSn == 0)) break;
+    }
+}
+
 // Growth over the failure range [gbeg, gend) of the weighted record order (records: (offset << 24) |
 // tile, offsets increasing; record r spans REC_W units for its tile load, then its failures): batches
 // of up to GSLOTS tile segments / GCAP failures; each segment's tile (+ R halo) is TMA-loaded into
@@ -881,6 +1232,8 @@ struct GrowSmem {
     int* ctl_n;      // [4]
     uint32_t* bms;   // [SLOTS][128] the next batch's failure bitmaps (bulk-copied ahead)
     uint64_t* bmbar; // [1] their mbarrier (initialised by the caller)
+    uint2* planes = nullptr;  // [SLOTS][pstride] zero / 255 bit planes (nullptr: plain grow_levels)
+    int pstride = 0;          // plane words per slot (>= BH * BS / 32 + 1)
 };
 
 template <bool FIN, int NTHR, class Out, int SLOTS = GSLOTS, int CAP = GCAP, int NETMAX = HYB_GROW_NETMAX,
@@ -1108,6 +1461,39 @@ __device__ __forceinline__ void grow_range(const CUtensorMap* tm, const GGeo& ge
         }
         GTRACE(1);
         // ---- 2. queue: warp w collects slot w's failures with in-tile rank in [lo, hi) ----
+        if (sm.planes) {
+            // fast levels: the segment's failure bits, as a bitmap (Q1 is free until the levels run)
+            if (warp < ns) {
+                mbar_wait_warp(sm.bmbar, bmphase);
+                const int* si = sinfo + 8 * warp;
+                const uint4 w4 = reinterpret_cast<const uint4*>(sm.bms + 128 * warp)[lane];
+                uint32_t wb[4] = {w4.x, w4.y, w4.z, w4.w};
+                const int nf = __popc(w4.x) + __popc(w4.y) + __popc(w4.z) + __popc(w4.w);
+                int incl = nf;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const int v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+                    if (lane >= d) incl += v;
+                }
+                int rank = incl - nf;
+                const int lo = si[4], hi = si[5];
+                if (rank < lo || incl > hi) {  // the segment boundary crosses this lane's row
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        uint32_t bits = wb[j], keepw = 0;
+                        while (bits) {
+                            const uint32_t low = bits & (0u - bits);
+                            if (rank >= lo && rank < hi) keepw |= low;
+                            bits ^= low;
+                            ++rank;
+                        }
+                        wb[j] = keepw;
+                    }
+                }
+                reinterpret_cast<uint4*>(reinterpret_cast<uint32_t*>(Q1) + 128 * warp)[lane] =
+                    make_uint4(wb[0], wb[1], wb[2], wb[3]);
+            }
+        } else
         if (warp < ns) {
             mbar_wait_warp(sm.bmbar, bmphase);
             const int* si = sinfo + 8 * warp;
@@ -1157,7 +1543,61 @@ __device__ __forceinline__ void grow_range(const CUtensorMap* tm, const GGeo& ge
         // ---- 4. levels, pooled over the batch ----
         int n = ctl[1];
         auto slot_out = [&](int sl, int pix, uint8_t v, int k) { out(sinfo + 8 * sl, pix, v, k); };
-        grow_levels<FIN, NTHR, decltype(slot_out), NETMAX>(bufs, geo, Q0, Q1, qcount, n, smax, slot_out);
+        if (sm.planes) {
+            uint32_t* f3m = reinterpret_cast<uint32_t*>(Q1);  // [SLOTS][128] failures -> k = 5 medians needed
+            uint32_t* bs7 = f3m + SLOTS * 128;                // [SLOTS][128] still open after k = 5
+            build_planes<NTHR>(bufs, geo, sm.planes, sm.pstride, ns);
+            __syncthreads();
+            dense_level5<NTHR, FIN>(sm.planes, sm.pstride, geo, ns, f3m, bs7);
+            __syncthreads();
+            // queues from the two bitmaps: S_7 at the front of Q0, M_5 at its tail (slot order as the warps arrive)
+            if (warp < ns) {
+                const uint4 m4 = reinterpret_cast<const uint4*>(f3m + 128 * warp)[lane];
+                const uint4 s4 = reinterpret_cast<const uint4*>(bs7 + 128 * warp)[lane];
+                const uint32_t mb[4] = {m4.x, m4.y, m4.z, m4.w}, sb[4] = {s4.x, s4.y, s4.z, s4.w};
+                const int mine = (__popc(s4.x) + __popc(s4.y) + __popc(s4.z) + __popc(s4.w)) |
+                                 ((__popc(m4.x) + __popc(m4.y) + __popc(m4.z) + __popc(m4.w)) << 16);
+                int incl = mine;  // open count | medians << 16 (each <= 4096)
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const int v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+                    if (lane >= d) incl += v;
+                }
+                const int tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+                int bS = 0, bM = 0;
+                if (lane == 0) {
+                    bS = atomicAdd(&qcount[2], tot & 0xFFFF);
+                    bM = atomicAdd(&qcount[1], tot >> 16);
+                }
+                bS = __shfl_sync(0xFFFFFFFFu, bS, 0);
+                bM = __shfl_sync(0xFFFFFFFFu, bM, 0);
+                int rs = bS + ((incl - mine) & 0xFFFF), rm = CAP - 1 - (bM + ((incl - mine) >> 16));
+                const uint32_t sbase = ((uint32_t)warp << 12) | (uint32_t)(lane * TW);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    uint32_t bits = sb[j];
+                    while (bits) {
+                        const int b = __ffs(bits) - 1;
+                        bits &= bits - 1;
+                        Q0[rs++] = (uint16_t)(sbase + 32 * j + b);
+                    }
+                    bits = mb[j];
+                    while (bits) {
+                        const int b = __ffs(bits) - 1;
+                        bits &= bits - 1;
+                        Q0[rm--] = (uint16_t)(sbase + 32 * j + b);
+                    }
+                }
+            }
+            __syncthreads();
+            GTRACE(14);
+            auto slot = [&](int sl) { return bufs + (size_t)sl * geo.b_bytes; };
+            auto plane = [&](int sl) { return sm.planes + (size_t)sl * sm.pstride; };
+            grow_levels_fast<FIN, NTHR, CAP, decltype(slot), decltype(plane), decltype(slot_out), NETMAX>(
+                slot, plane, geo, Q0, Q1, qcount, smax, slot_out);
+        } else {
+            grow_levels<FIN, NTHR, decltype(slot_out), NETMAX>(bufs, geo, Q0, Q1, qcount, n, smax, slot_out);
+        }
         __syncthreads();  // slots, queues and counters are reused by the next batch
 #ifdef HYB_TRACE
         if (tid == 0 && blockIdx.x < 1024) g_trace[(1024 + blockIdx.x) * 16 + 4] += 1;
