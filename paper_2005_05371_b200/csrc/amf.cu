@@ -257,9 +257,10 @@ struct GArgs {
 // 2 CTAs/SM, batches of 8 tiles / 8192 failures) pays off when the k = 9 level is dense (BASELINE
 // config 4: smax 11, S&P 0.5); "lean" (networks up to k = 7, radix above, <= 80 registers, 3 CTAs/SM,
 // batches of 8 tiles / 4096 failures) when it is sparse or absent (config 2: 6 % faster step).
-template <int NETMAX_, int MINB_, int SLOTS_, int CAP_, bool DYN_, int CHUNK_SHIFT_>
+template <int NETMAX_, int MINB_, int SLOTS_, int CAP_, bool DYN_, int CHUNK_SHIFT_, int NT_ = GNT>
 struct GrowCfg {
     static constexpr int NETMAX = NETMAX_, MINB = MINB_, SLOTS = SLOTS_, CAP = CAP_;
+    static constexpr int NT = NT_;     // threads per CTA
     static constexpr bool DYN = DYN_;  // dynamic last quarter of the work (amf_core.cuh grow_range)
     static constexpr int CHUNK_SHIFT = CHUNK_SHIFT_;  // log2 of a claim, in weighted units
 };
@@ -278,7 +279,17 @@ struct GrowCfg {
 #ifndef HYB_WIDE_CHUNK
 #define HYB_WIDE_CHUNK 15  // log2 of the static chunk (the guided claims take at most this many units)
 #endif
-using GrowWide = GrowCfg<9, HYB_WIDE_MINB, HYB_WIDE_SLOTS, HYB_WIDE_CAP, true, HYB_WIDE_CHUNK>;
+// With the bit-plane levels (amf_core.cuh grow_levels_fast) the k = 9 medians are few (config 4: ~270 per batch), so
+// the wide variant keeps networks to k = 7 (80 registers) and spends the registers on 12 warps per CTA instead:
+// measured config 4 AMF 1.864 ms (k = 9 network, 256 threads) / 1.860 (radix, 256) / 1.813 (radix, 384); 3 CTAs / SM of
+// 5- or 6-tile batches 2.04 / 2.11 ms -- the pool size matters more than the warps.
+#ifndef HYB_WIDE_NETMAX
+#define HYB_WIDE_NETMAX 7  // largest window the wide variant grows with a selection network
+#endif
+#ifndef HYB_WIDE_NT
+#define HYB_WIDE_NT 384
+#endif
+using GrowWide = GrowCfg<HYB_WIDE_NETMAX, HYB_WIDE_MINB, HYB_WIDE_SLOTS, HYB_WIDE_CAP, true, HYB_WIDE_CHUNK, HYB_WIDE_NT>;
 #ifndef HYB_LEAN_SLOTS
 #define HYB_LEAN_SLOTS 8
 #endif
@@ -290,7 +301,7 @@ using GrowWide = GrowCfg<9, HYB_WIDE_MINB, HYB_WIDE_SLOTS, HYB_WIDE_CAP, true, H
 #endif
 using GrowLean = GrowCfg<7, 3, HYB_LEAN_SLOTS, 4096, HYB_LEAN_DYN != 0, HYB_LEAN_CHUNK>;
 static_assert(GrowWide::SLOTS <= 8 && GrowLean::SLOTS <= 8, "header layout");
-static_assert(GrowWide::SLOTS <= GNT / 32 && GrowLean::SLOTS <= GNT / 32, "queue build: one warp per slot");
+static_assert(GrowWide::SLOTS <= GrowWide::NT / 32 && GrowLean::SLOTS <= GrowLean::NT / 32, "queue build: one warp per slot");
 static_assert(GrowWide::CHUNK_SHIFT >= 11 && GrowLean::CHUNK_SHIFT >= 11, "chunk table sized for chunks >= 2048");
 
 // plane words (uint2) per slot of the fast growth levels: one per 32 tile bytes, one of padding, 16-byte multiple
@@ -304,7 +315,7 @@ inline size_t grow_smem(const GGeo& g, bool fast = false) {
 
 
 template <bool FIN, class C>
-__global__ void __launch_bounds__(GNT, C::MINB) amf_grow_kernel(const __grid_constant__ CUtensorMap tm,
+__global__ void __launch_bounds__(C::NT, C::MINB) amf_grow_kernel(const __grid_constant__ CUtensorMap tm,
                                                       const __grid_constant__ GArgs args) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
@@ -347,7 +358,7 @@ __global__ void __launch_bounds__(GNT, C::MINB) amf_grow_kernel(const __grid_con
         if (FIN) args.fin[(size_t)si[2] * args.fslice + row * args.fpitch + si[0] + (pix & 127)] = (uint8_t)k;
     };
     // tile records first: the CTAs that have some join the compact chunk claims below late
-    grow_range<FIN, GNT, decltype(out), C::SLOTS, C::CAP, C::NETMAX, C::DYN, 1ll << C::CHUNK_SHIFT>(&tm, geo, sm, args.bitmap, args.records, R, T,
+    grow_range<FIN, C::NT, decltype(out), C::SLOTS, C::CAP, C::NETMAX, C::DYN, 1ll << C::CHUNK_SHIFT>(&tm, geo, sm, args.bitmap, args.records, R, T,
                                                                      args.chunk_rec, args.chunk_ctr, per_slice,
                                                                      args.tiles_x,
                                                                      args.row_begin, args.rows, args.cols, args.smax,
@@ -398,7 +409,7 @@ __global__ void __launch_bounds__(GNT, C::MINB) amf_grow_kernel(const __grid_con
             mbar_wait(&cbar[b], (uint32_t)(it >> 1) & 1u);
             const int n = min(ch, nc - c * ch);
             const uint4* sb = stg + (size_t)b * ch * 4;
-            for (int p0 = 0; 2 * p0 < n; p0 += GNT) {
+            for (int p0 = 0; 2 * p0 < n; p0 += C::NT) {
                 const int pi = p0 + tid;
                 uint32_t pend = 0;
                 int ia = 2 * pi, ib = 2 * pi + 1;
@@ -432,7 +443,7 @@ __global__ void __launch_bounds__(GNT, C::MINB) amf_grow_kernel(const __grid_con
         }
         __syncthreads();
         const int n7 = min(*sc, OCAP);
-        for (int j = tid; 2 * j < n7; j += GNT) {
+        for (int j = tid; 2 * j < n7; j += C::NT) {
             const int ia = open7[2 * j], ib = 2 * j + 1 < n7 ? open7[2 * j + 1] : ia;
             compact_level<7>(cq + (size_t)ia * 4, cq + (size_t)ib * 4, 2 * j + 1 < n7 ? 3u : 1u, cout(7));
         }
@@ -825,10 +836,11 @@ cudaError_t launch_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, si
     g.cq_cap = a.cq_cap;
     g.out_rows = out_rows;
     g.fast = fast ? plane_stride(geo) : 0;
-    const int gper_sm = occupancy(gocc[vi], (const void*)kern, GNT, gsm);
+    const int gnt = wide ? GrowWide::NT : GrowLean::NT;
+    const int gper_sm = occupancy(gocc[vi], (const void*)kern, gnt, gsm);
     // every resident CTA slot busy; each CTA takes a contiguous run of tiles
     const int ggrid = (int)std::min<long long>(ntiles, (long long)num_sms * gper_sm);
-    e = launch_pdl(kern, dim3(ggrid), dim3(GNT), gsm, stream, tm_g, g);
+    e = launch_pdl(kern, dim3(ggrid), dim3(gnt), gsm, stream, tm_g, g);
     count_launch();
     return e;
 }

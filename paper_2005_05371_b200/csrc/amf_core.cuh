@@ -885,17 +885,23 @@ __device__ __forceinline__ void build_planes(const uint8_t* bufs, const GGeo& ge
         const uint4* src = reinterpret_cast<const uint4*>(bufs + (size_t)sl * geo.b_bytes + 32 * q);
         const uint4 lo = src[0], hi = src[1];
         const uint32_t x[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-        uint32_t e0 = 0, e1 = 0;
+        // the four byte MSBs are gathered into the top nibble by one multiply (bits 24..27 of the product stay
+        // zero) and shifted into the plane word; even and odd words in separate chains (half the dependent depth)
+        uint32_t a0 = 0, b0 = 0, a1 = 0, b1 = 0;
 #pragma unroll
         for (int j = 7; j >= 0; --j) {
             const uint32_t t7 = x[j] & 0x7F7F7F7Fu;
             const uint32_t z = ~((t7 + 0x7F7F7F7Fu) | x[j]) & 0x80808080u;  // byte MSB: byte == 0
             const uint32_t f = (t7 + 0x01010101u) & x[j] & 0x80808080u;      // byte MSB: byte == 255
-            // the four MSBs gathered into the top nibble by one multiply, shifted into the plane word
-            e0 = __funnelshift_l(z * 0x00204081u, e0, 4);
-            e1 = __funnelshift_l(f * 0x00204081u, e1, 4);
+            if (j & 1) {
+                a0 = __funnelshift_l(z * 0x00204081u, a0, 8);
+                a1 = __funnelshift_l(f * 0x00204081u, a1, 8);
+            } else {
+                b0 = __funnelshift_l(z * 0x00204081u, b0, 8);
+                b1 = __funnelshift_l(f * 0x00204081u, b1, 8);
+            }
         }
-        planes[(size_t)sl * pstride + q] = make_uint2(e0, e1);
+        planes[(size_t)sl * pstride + q] = make_uint2(a0 | (b0 >> 4), a1 | (b1 >> 4));
     }
 }
 
@@ -1180,6 +1186,10 @@ __device__ __forceinline__ void grow_levels_fast(Slot slot, PlaneOf plane, const
     for (int i = 0;; ++i) {
         const int kB = 5 + 2 * i, kA = kB + 2;
         if (kB > smax) break;
+#ifdef HYB_TRACE
+        unsigned long long t_iv = 0;
+        if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_iv));
+#endif
         const uint16_t* X = (i & 1) ? Q1 : Q0;
         uint16_t* Y = (i & 1) ? Q0 : Q1;
         const int nM = qcount[2 * i + 1], nS = kA <= smax ? qcount[2 * i + 2] : 0;
@@ -1208,6 +1218,14 @@ __device__ __forceinline__ void grow_levels_fast(Slot slot, PlaneOf plane, const
             else fast_pass_a<FIN, NTHR, CAP, 13>(slot, plane, geo, X, Y, nS, cSn, cMn, lastA, wrot, out);
         }
         __syncthreads();
+#ifdef HYB_TRACE
+        // fast-level profile (kernel id 1): slots 5 + i += interval time (pass B of k = 5 + 2 i, pass A of k + 2)
+        if (threadIdx.x == 0 && blockIdx.x < 1024 && i < 4) {
+            unsigned long long t1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            g_trace[(1024 + blockIdx.x) * 16 + 5 + i] += t1 - t_iv;
+        }
+#endif
         if (*cMn == 0 && (lastA || *cSn == 0)) break;
     }
 }
@@ -1548,8 +1566,10 @@ __device__ __forceinline__ void grow_range(const CUtensorMap* tm, const GGeo& ge
             uint32_t* bs7 = f3m + SLOTS * 128;                // [SLOTS][128] still open after k = 5
             build_planes<NTHR>(bufs, geo, sm.planes, sm.pstride, ns);
             __syncthreads();
+            GTRACE(9);
             dense_level5<NTHR, FIN>(sm.planes, sm.pstride, geo, ns, f3m, bs7);
             __syncthreads();
+            GTRACE(10);
             // queues from the two bitmaps: S_7 at the front of Q0, M_5 at its tail (slot order as the warps arrive)
             if (warp < ns) {
                 const uint4 m4 = reinterpret_cast<const uint4*>(f3m + 128 * warp)[lane];
@@ -1590,7 +1610,7 @@ __device__ __forceinline__ void grow_range(const CUtensorMap* tm, const GGeo& ge
                 }
             }
             __syncthreads();
-            GTRACE(14);
+            GTRACE(11);
             auto slot = [&](int sl) { return bufs + (size_t)sl * geo.b_bytes; };
             auto plane = [&](int sl) { return sm.planes + (size_t)sl * sm.pstride; };
             grow_levels_fast<FIN, NTHR, CAP, decltype(slot), decltype(plane), decltype(slot_out), NETMAX>(

@@ -60,6 +60,71 @@ __device__ __forceinline__ uint32_t hsum1(uint32_t w0, uint32_t w1, uint32_t w2)
     return __dp4a(bytes4<S + 4>(w0, w1, w2), hw, __dp4a(bytes4<S>(w0, w1, w2), 0x01010101u, 0u));
 }
 
+// Horizontal window sums of the lane's 4 pixels at once.  5 x 5 and 7 x 7 windows: the sums of the two
+// pixels whose windows are made of whole words (plus masked neighbour words) come from dp4a, the other two
+// follow by adding the byte that enters and subtracting the byte that leaves (squares on the FMA pipe):
+// 6 (7 x 7) / 2 (5 x 5) dp4a per row instead of 16 -- the dp4a issue rate bounded the gain pass.
+__device__ __forceinline__ uint32_t byte_of(uint32_t w, int i) { return (w >> (8 * i)) & 0xFFu; }
+
+template <int RW>
+__device__ __forceinline__ void hsums4(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t (&h1)[4], uint32_t (&h2)[4]) {
+    if constexpr (RW == 3) {
+        // windows: bytes 1..7, 2..8, 3..9, 4..10 of [w0 w1 w2]
+        const uint32_t l = w0 & 0xFFFFFF00u, r = w2 & 0x00FFFFFFu;
+        const uint32_t m1 = __dp4a(w1, 0x01010101u, 0u), m2 = __dp4a(w1, w1, 0u);
+        h1[0] = __dp4a(l, 0x01010101u, m1);
+        h1[3] = __dp4a(r, 0x01010101u, m1);
+        h2[0] = __dp4a(l, l, m2);
+        h2[3] = __dp4a(r, r, m2);
+        const uint32_t b1 = byte_of(w0, 1), b3 = byte_of(w0, 3), b8 = byte_of(w2, 0), b10 = byte_of(w2, 2);
+        h1[1] = h1[0] - b1 + b8;
+        h1[2] = h1[3] + b3 - b10;
+        h2[1] = h2[0] - b1 * b1 + b8 * b8;
+        h2[2] = h2[3] + b3 * b3 - b10 * b10;
+    } else if constexpr (RW == 2) {
+        // windows: bytes 2..6, 3..7, 4..8, 5..9
+        const uint32_t m1 = __dp4a(w1, 0x01010101u, 0u), m2 = __dp4a(w1, w1, 0u);
+        const uint32_t b2 = byte_of(w0, 2), b3 = byte_of(w0, 3), b4 = byte_of(w1, 0), b7 = byte_of(w1, 3);
+        const uint32_t b8 = byte_of(w2, 0), b9 = byte_of(w2, 1);
+        h1[1] = m1 + b3;
+        h1[2] = m1 + b8;
+        h1[0] = h1[1] + b2 - b7;
+        h1[3] = h1[2] + b9 - b4;
+        h2[1] = m2 + b3 * b3;
+        h2[2] = m2 + b8 * b8;
+        h2[0] = h2[1] + b2 * b2 - b7 * b7;
+        h2[3] = h2[2] + b9 * b9 - b4 * b4;
+    } else {
+        hsums<RW, 0>(w0, w1, w2, h1[0], h2[0]);
+        hsums<RW, 1>(w0, w1, w2, h1[1], h2[1]);
+        hsums<RW, 2>(w0, w1, w2, h1[2], h2[2]);
+        hsums<RW, 3>(w0, w1, w2, h1[3], h2[3]);
+    }
+}
+
+// The same for the sums of f only (statistics pass).
+template <int RW>
+__device__ __forceinline__ void hsum1x4(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t (&h)[4]) {
+    if constexpr (RW == 3) {
+        const uint32_t m1 = __dp4a(w1, 0x01010101u, 0u);
+        h[0] = __dp4a(w0 & 0xFFFFFF00u, 0x01010101u, m1);
+        h[3] = __dp4a(w2 & 0x00FFFFFFu, 0x01010101u, m1);
+        h[1] = h[0] - byte_of(w0, 1) + byte_of(w2, 0);
+        h[2] = h[3] + byte_of(w0, 3) - byte_of(w2, 2);
+    } else if constexpr (RW == 2) {
+        const uint32_t m1 = __dp4a(w1, 0x01010101u, 0u);
+        h[1] = m1 + byte_of(w0, 3);
+        h[2] = m1 + byte_of(w2, 0);
+        h[0] = h[1] + byte_of(w0, 2) - byte_of(w1, 3);
+        h[3] = h[2] + byte_of(w2, 1) - byte_of(w1, 0);
+    } else {
+        h[0] = hsum1<RW, 0>(w0, w1, w2);
+        h[1] = hsum1<RW, 1>(w0, w1, w2);
+        h[2] = hsum1<RW, 2>(w0, w1, w2);
+        h[3] = hsum1<RW, 3>(w0, w1, w2);
+    }
+}
+
 // Number of (output position p in [lo, hi), offset d in [-RW, RW]) pairs whose clamped coordinate
 // clamp(p + d, 0, n - 1) equals r: how many output windows cover row (or column) r.
 __device__ __forceinline__ int win_count(int r, int lo, int hi, int n, int RW) {
@@ -135,10 +200,7 @@ __device__ __forceinline__ long long w1_tile_stats_body(const uint8_t* __restric
     auto take_row = [&](int rr, uint32_t (&h)[4]) {
         const uint32_t* rp = base + rr * (FBS / 4);
         const uint32_t w0 = rp[0], w1 = rp[1], w2 = rp[2];
-        h[0] = hsum1<RW, 0>(w0, w1, w2);
-        h[1] = hsum1<RW, 1>(w0, w1, w2);
-        h[2] = hsum1<RW, 2>(w0, w1, w2);
-        h[3] = hsum1<RW, 3>(w0, w1, w2);
+        hsum1x4<RW>(w0, w1, w2, h);
         if constexpr (FAST) {
             if (rr >= RW && rr < RW + FH) sq32 = __dp4a(w1, w1, sq32);
         } else {
@@ -319,10 +381,7 @@ __device__ __forceinline__ void w1_tile_gain(const uint8_t* __restrict__ T, int 
         const uint32_t* rp = base + rr * (FBS / 4);
         const uint32_t w0 = rp[0], w1 = rp[1], w2 = rp[2];
         uint32_t h1[4], h2[4];
-        hsums<RW, 0>(w0, w1, w2, h1[0], h2[0]);
-        hsums<RW, 1>(w0, w1, w2, h1[1], h2[1]);
-        hsums<RW, 2>(w0, w1, w2, h1[2], h2[2]);
-        hsums<RW, 3>(w0, w1, w2, h1[3], h2[3]);
+        hsums4<RW>(w0, w1, w2, h1, h2);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             s1[i] = sub ? s1[i] - h1[i] : s1[i] + h1[i];
@@ -375,10 +434,7 @@ __device__ __forceinline__ long long w1_tile_sums3(const uint8_t* __restrict__ T
         const uint32_t* rp = base + rr * (FBS / 4);
         const uint32_t w0 = rp[0], w1 = rp[1], w2 = rp[2];
         uint32_t h1[4], h2[4];
-        hsums<RW, 0>(w0, w1, w2, h1[0], h2[0]);
-        hsums<RW, 1>(w0, w1, w2, h1[1], h2[1]);
-        hsums<RW, 2>(w0, w1, w2, h1[2], h2[2]);
-        hsums<RW, 3>(w0, w1, w2, h1[3], h2[3]);
+        hsums4<RW>(w0, w1, w2, h1, h2);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             s1[i] = sub ? s1[i] - h1[i] : s1[i] + h1[i];
