@@ -310,7 +310,7 @@ inline int plane_stride(const GGeo& g) { return (g.BH * (g.BS >> 5) + 2) & ~1; }
 template <class C>
 inline size_t grow_smem(const GGeo& g, bool fast = false) {
     return GHDR + (size_t)C::SLOTS * g.b_bytes + 2 * C::CAP * 2 + (size_t)C::SLOTS * 512 + 128 +
-           (fast ? (size_t)C::SLOTS * plane_stride(g) * 8 : 0);
+           (fast ? (size_t)C::SLOTS * (plane_stride(g) * 8 + 512) : 0);  // planes + the second bitmap buffer
 }
 
 
@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB) amf_grow_kernel(const __grid_c
     uint16_t* Q1 = Q0 + C::CAP;
     int* sinfo_n = reinterpret_cast<int*>(smem + 1024);            // [SLOTS][8] next batch
     int* ctl_n = reinterpret_cast<int*>(smem + 1280);              // [4]
-    uint64_t* bmbar = reinterpret_cast<uint64_t*>(smem + 1344);    // next batch's bitmap copies
+    uint64_t* bmbar = reinterpret_cast<uint64_t*>(smem + 1344);    // [2] next batch's bitmap copies
     uint32_t* bms = reinterpret_cast<uint32_t*>(Q1 + C::CAP);      // [SLOTS][128]
     uint64_t* cbar = reinterpret_cast<uint64_t*>(smem + 1416);     // [2] compact entry staging
     const int tid = threadIdx.x;
@@ -338,6 +338,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB) amf_grow_kernel(const __grid_c
     if (tid == 0) {
         for (int i = 0; i < C::SLOTS; ++i) mbar_init(&bar[i], 1);
         mbar_init(bmbar, 1);
+        mbar_init(bmbar + 1, 1);
         mbar_init(&cbar[0], 1);
         mbar_init(&cbar[1], 1);
         prefetch_tmap(&tm);
@@ -349,7 +350,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB) amf_grow_kernel(const __grid_c
     uint32_t phases = 0;
     GrowSmem sm{bar, sinfo, cur, ctl, qcount, bufs, Q0, Q1, sinfo_n, ctl_n, bms, bmbar};
     if (args.fast) {  // zero / 255 bit planes behind the bitmaps (16-byte aligned)
-        sm.planes = reinterpret_cast<uint2*>(bms + C::SLOTS * 128);
+        sm.planes = reinterpret_cast<uint2*>(bms + 2 * C::SLOTS * 128);
         sm.pstride = args.fast;
     }
     auto out = [&](const int* si, int pix, uint8_t v, int k) {

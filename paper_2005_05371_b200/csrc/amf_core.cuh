@@ -977,16 +977,47 @@ __device__ __forceinline__ void box5_counts(const uint32_t (&e)[5][5], uint32_t 
 }
 
 // Level k = 5 for whole tiles at once (thread = one row of one staged tile; geo.CP == 16, BS == 160).
-// f3m[sl][128] holds the slot's level-A failures of k = 3 (bitmap words 4 row + q) on entry; on return
+// bm[sl][128] holds the slot's level-A failures of k = 3 (bitmap words 4 row + q), sinfo[8 sl + 4 / 5] the
+// in-tile rank range of the segment this batch grows; f3m[sl][128] receives
 // the pixels whose k = 5 median is needed (impulse centres that pass level A, and every pixel whose
 // window lacks a 0 or a 255 -- the generic test decides those), bs7[sl][128] the pixels still open.
 // Pixels that pass with a non-impulse centre keep g, which f already holds (FIN: they go through the
 // median pass so finalized_at gets its 5).
 template <int NTHR, bool FIN>
-__device__ __forceinline__ void dense_level5(const uint2* planes, int pstride, const GGeo& geo, int ns, uint32_t* f3m,
+__device__ __forceinline__ void dense_level5(const uint2* planes, int pstride, const GGeo& geo, int ns,
+                                             const uint32_t* __restrict__ bm, const int* sinfo, uint32_t* f3m,
                                              uint32_t* bs7) {
+    static_assert(TH == 32, "one warp = the rows of one tile");
     for (int t = threadIdx.x; t < ns * TH; t += NTHR) {
         const int sl = t / TH, row = t - sl * TH;
+        // the slot's k = 3 failures (bitmap words 4 row + q) whose in-tile rank lies in the segment [lo, hi)
+        uint4 f = reinterpret_cast<const uint4*>(bm + sl * 128)[row];
+        {
+            const int nf = __popc(f.x) + __popc(f.y) + __popc(f.z) + __popc(f.w);
+            int incl = nf;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+                if (row >= d) incl += v;
+            }
+            int rank = incl - nf;
+            const int lo = sinfo[8 * sl + 4], hi = sinfo[8 * sl + 5];
+            if (rank < lo || incl > hi) {  // the segment boundary crosses this row
+                uint32_t wb[4] = {f.x, f.y, f.z, f.w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    uint32_t bits = wb[j], keepw = 0;
+                    while (bits) {
+                        const uint32_t low = bits & (0u - bits);
+                        if (rank >= lo && rank < hi) keepw |= low;
+                        bits ^= low;
+                        ++rank;
+                    }
+                    wb[j] = keepw;
+                }
+                f = make_uint4(wb[0], wb[1], wb[2], wb[3]);
+            }
+        }
         const uint2* P = planes + (size_t)sl * pstride + (row + geo.R - 2) * 5;
         uint32_t e0[5][5], e1[5][5];
 #pragma unroll
@@ -1007,7 +1038,6 @@ __device__ __forceinline__ void dense_level5(const uint2* planes, int pstride, c
             ds[j] = elig & ~pass;
         }
         uint4* fm = reinterpret_cast<uint4*>(f3m + sl * 128 + 4 * row);
-        const uint4 f = *fm;
         // plane bit 16 + c = tile column c
         *fm = make_uint4(f.x & __funnelshift_r(dm[0], dm[1], 16), f.y & __funnelshift_r(dm[1], dm[2], 16),
                          f.z & __funnelshift_r(dm[2], dm[3], 16), f.w & __funnelshift_r(dm[3], dm[4], 16));
@@ -1250,7 +1280,8 @@ struct GrowSmem {
     int* ctl_n;      // [4]
     uint32_t* bms;   // [SLOTS][128] the next batch's failure bitmaps (bulk-copied ahead)
     uint64_t* bmbar; // [1] their mbarrier (initialised by the caller)
-    uint2* planes = nullptr;  // [SLOTS][pstride] zero / 255 bit planes (nullptr: plain grow_levels)
+    uint2* planes = nullptr;  // [SLOTS][pstride] zero / 255 bit planes (nullptr: plain grow_levels); with planes,
+                              // bms is [2][SLOTS][128] and bmbar [2]: the bitmaps stay until the dense k = 5 pass
     int pstride = 0;          // plane words per slot (>= BH * BS / 32 + 1)
 };
 
@@ -1305,7 +1336,10 @@ __device__ __forceinline__ void grow_range(const CUtensorMap* tm, const GGeo& ge
     // for its tile load, then its failures.  Work is claimed in chunks of CHUNK weighted units from a
     // global counter (chunk_rec gives each chunk's first record), so CTAs that meet cheap failures take
     // more chunks -- the cost of a failure depends on how deep it grows, which no static split sees.
-    auto choose = [&]() {
+    const bool dbl = sm.planes != nullptr;  // two bitmap buffers
+    auto choose = [&](int nbuf) {
+        uint32_t* bms_n = sm.bms + nbuf * SLOTS * 128;
+        uint64_t* bmbar_n = sm.bmbar + nbuf;
         if (cur[1] >= cur[2]) {  // range exhausted: the static run, then chunks from the counter
             bool have = false;
             if (!cur[3]) {
@@ -1421,7 +1455,7 @@ __device__ __forceinline__ void grow_range(const CUtensorMap* tm, const GGeo& ge
         const uint32_t segs = __ballot_sync(0xFFFFFFFFu, mine > 0);
         const uint32_t inside = __ballot_sync(0xFFFFFFFFu, within);  // lanes 0..k (lane 0 always)
         const int ns = __popc(segs);
-        if (lane == 0 && ns) mbar_expect_tx(sm.bmbar, (uint32_t)(ns * 512));
+        if (lane == 0 && ns) mbar_expect_tx(bmbar_n, (uint32_t)(ns * 512));
         __syncwarp();
         if (mine > 0) {
             const int sl = __popc(segs & ((1u << lane) - 1u));
@@ -1439,8 +1473,8 @@ __device__ __forceinline__ void grow_range(const CUtensorMap* tm, const GGeo& ge
             fence_proxy_async_smem();  // the previous batch's generic reads of bms before the async write
             asm volatile(
                 "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 512, [%2];" ::"r"(
-                    smem_u32(sm.bms + 128 * sl)),
-                "l"(bitmap + (size_t)tile * 512), "r"(smem_u32(sm.bmbar))
+                    smem_u32(bms_n + 128 * sl)),
+                "l"(bitmap + (size_t)tile * 512), "r"(smem_u32(bmbar_n))
                 : "memory");
         }
         const int last = 31 - __clz(inside);
@@ -1454,11 +1488,12 @@ __device__ __forceinline__ void grow_range(const CUtensorMap* tm, const GGeo& ge
         }
         __syncwarp();
     };
-    if (warp == 0) choose();
+    if (warp == 0) choose(0);
     __syncthreads();
     GTRACE(13);
 
-    while (true) {
+    for (int it = 0;; ++it) {
+        const int cb = dbl ? (it & 1) : 0, nbuf = dbl ? ((it + 1) & 1) : 0;  // this batch's / the next batch's bitmaps
         // ---- 1. promote the chosen batch; warp 0 issues its tile loads ----
         if (tid < MAX_LEVELS) qcount[tid] = 0;
         if (tid < 8 * SLOTS) sinfo[tid] = sm.sinfo_n[tid];
@@ -1468,7 +1503,7 @@ __device__ __forceinline__ void grow_range(const CUtensorMap* tm, const GGeo& ge
         const bool more = ctl[2] != 0;
         if (ns == 0) {  // only tile-load weight in this stretch of the range
             if (!more) break;
-            if (warp == 0) choose();
+            if (warp == 0) choose(nbuf);
             __syncthreads();
             continue;
         }
@@ -1478,40 +1513,9 @@ __device__ __forceinline__ void grow_range(const CUtensorMap* tm, const GGeo& ge
             grow_tile_load(tm, geo, bufs + (size_t)lane * geo.b_bytes, &bar[lane], si[0], si[1], si[2]);
         }
         GTRACE(1);
-        // ---- 2. queue: warp w collects slot w's failures with in-tile rank in [lo, hi) ----
-        if (sm.planes) {
-            // fast levels: the segment's failure bits, as a bitmap (Q1 is free until the levels run)
-            if (warp < ns) {
-                mbar_wait_warp(sm.bmbar, bmphase);
-                const int* si = sinfo + 8 * warp;
-                const uint4 w4 = reinterpret_cast<const uint4*>(sm.bms + 128 * warp)[lane];
-                uint32_t wb[4] = {w4.x, w4.y, w4.z, w4.w};
-                const int nf = __popc(w4.x) + __popc(w4.y) + __popc(w4.z) + __popc(w4.w);
-                int incl = nf;
-#pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    const int v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
-                    if (lane >= d) incl += v;
-                }
-                int rank = incl - nf;
-                const int lo = si[4], hi = si[5];
-                if (rank < lo || incl > hi) {  // the segment boundary crosses this lane's row
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        uint32_t bits = wb[j], keepw = 0;
-                        while (bits) {
-                            const uint32_t low = bits & (0u - bits);
-                            if (rank >= lo && rank < hi) keepw |= low;
-                            bits ^= low;
-                            ++rank;
-                        }
-                        wb[j] = keepw;
-                    }
-                }
-                reinterpret_cast<uint4*>(reinterpret_cast<uint32_t*>(Q1) + 128 * warp)[lane] =
-                    make_uint4(wb[0], wb[1], wb[2], wb[3]);
-            }
-        } else
+        // ---- 2. queue: warp w collects slot w's failures with in-tile rank in [lo, hi) (with planes: after
+        //      the dense k = 5 pass below, from its bitmaps) ----
+        if (!dbl) {
         if (warp < ns) {
             mbar_wait_warp(sm.bmbar, bmphase);
             const int* si = sinfo + 8 * warp;
@@ -1544,19 +1548,22 @@ __device__ __forceinline__ void grow_range(const CUtensorMap* tm, const GGeo& ge
         }
         bmphase ^= 1u;
         __syncthreads();  // bms consumed
+        }
         GTRACE(2);
         // ---- 3. the last warp chooses the next batch (its record loads and bitmap copies overlap the
         //      tile wait and the levels); tiles landed; border tiles get edge replication ----
-        if (warp == NWARP - 1) choose();
+        if (warp == NWARP - 1) choose(nbuf);
         for (int sl = 0; sl < ns; ++sl) mbar_wait(&bar[sl], (phases >> sl) & 1u);
         phases ^= (1u << ns) - 1u;
+        bool anyb = false;
         for (int sl = 0; sl < ns; ++sl) {
             if (!sinfo[8 * sl + 7]) continue;  // uniform
+            anyb = true;
             const int sx0 = sinfo[8 * sl] - geo.CP, sy0 = sinfo[8 * sl + 1] - geo.R;
             replicate_edges<NTHR>(bufs + (size_t)sl * geo.b_bytes, geo.BS, max(0, -sx0), min(geo.BS, cols - sx0),
                                   max(0, -sy0), min(geo.BH, rows - sy0), 0, geo.BH, geo.R);
         }
-        __syncthreads();
+        if (anyb || !dbl) __syncthreads();  // (every thread waited for the tiles itself)
         GTRACE(3);
         // ---- 4. levels, pooled over the batch ----
         int n = ctl[1];
@@ -1567,7 +1574,9 @@ __device__ __forceinline__ void grow_range(const CUtensorMap* tm, const GGeo& ge
             build_planes<NTHR>(bufs, geo, sm.planes, sm.pstride, ns);
             __syncthreads();
             GTRACE(9);
-            dense_level5<NTHR, FIN>(sm.planes, sm.pstride, geo, ns, f3m, bs7);
+            if (warp < ns) mbar_wait_warp(sm.bmbar + cb, (bmphase >> cb) & 1u);
+            bmphase ^= 1u << cb;
+            dense_level5<NTHR, FIN>(sm.planes, sm.pstride, geo, ns, sm.bms + cb * SLOTS * 128, sinfo, f3m, bs7);
             __syncthreads();
             GTRACE(10);
             // queues from the two bitmaps: S_7 at the front of Q0, M_5 at its tail (slot order as the warps arrive)

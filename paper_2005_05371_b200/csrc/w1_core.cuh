@@ -65,18 +65,29 @@ __device__ __forceinline__ uint32_t hsum1(uint32_t w0, uint32_t w1, uint32_t w2)
 // follow by adding the byte that enters and subtracting the byte that leaves (squares on the FMA pipe):
 // 6 (7 x 7) / 2 (5 x 5) dp4a per row instead of 16 -- the dp4a issue rate bounded the gain pass.
 __device__ __forceinline__ uint32_t byte_of(uint32_t w, int i) { return (w >> (8 * i)) & 0xFFu; }
+#ifndef HYB_W1_LOWDP
+#define HYB_W1_LOWDP 0  // 1: 7 x 7 edge sums from single bytes too (2 dp4a per row): measured slower, config 4 W1 0.618 vs 0.594 ms
+#endif
 
 template <int RW>
 __device__ __forceinline__ void hsums4(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t (&h1)[4], uint32_t (&h2)[4]) {
     if constexpr (RW == 3) {
         // windows: bytes 1..7, 2..8, 3..9, 4..10 of [w0 w1 w2]
-        const uint32_t l = w0 & 0xFFFFFF00u, r = w2 & 0x00FFFFFFu;
         const uint32_t m1 = __dp4a(w1, 0x01010101u, 0u), m2 = __dp4a(w1, w1, 0u);
+        const uint32_t b1 = byte_of(w0, 1), b3 = byte_of(w0, 3), b8 = byte_of(w2, 0), b10 = byte_of(w2, 2);
+#if HYB_W1_LOWDP
+        const uint32_t b2 = byte_of(w0, 2), b9 = byte_of(w2, 1);
+        h1[0] = m1 + b1 + b2 + b3;
+        h1[3] = m1 + b8 + b9 + b10;
+        h2[0] = m2 + b1 * b1 + b2 * b2 + b3 * b3;
+        h2[3] = m2 + b8 * b8 + b9 * b9 + b10 * b10;
+#else
+        const uint32_t l = w0 & 0xFFFFFF00u, r = w2 & 0x00FFFFFFu;
         h1[0] = __dp4a(l, 0x01010101u, m1);
         h1[3] = __dp4a(r, 0x01010101u, m1);
         h2[0] = __dp4a(l, l, m2);
         h2[3] = __dp4a(r, r, m2);
-        const uint32_t b1 = byte_of(w0, 1), b3 = byte_of(w0, 3), b8 = byte_of(w2, 0), b10 = byte_of(w2, 2);
+#endif
         h1[1] = h1[0] - b1 + b8;
         h1[2] = h1[3] + b3 - b10;
         h2[1] = h2[0] - b1 * b1 + b8 * b8;
