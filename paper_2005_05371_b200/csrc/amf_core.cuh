@@ -54,10 +54,19 @@ __device__ __forceinline__ uint32_t pairw_rt(uint32_t a, uint32_t b, int j) {
     return __byte_perm(a, b, j | (j << 4) | ((4 + j) << 8) | ((4 + j) << 12));
 }
 
-// Number of zero bytes of x among the byte lanes flagged (0x80) in v80.
-__device__ __forceinline__ int zero_bytes(uint32_t x, uint32_t v80) {
+// 128 x the number of zero bytes of x among the byte lanes flagged (0x80) in v80, added to acc.  The flag
+// bytes are summed by dp4a: a POPC per window word (XU pipe, a quarter of the ALU rate) bounded the radix
+// selects once the plane tests left them as the deep levels' only work.
+#ifndef HYB_ZB_POPC
+#define HYB_ZB_POPC 0  // 1: the POPC form (A/B)
+#endif
+__device__ __forceinline__ uint32_t zero_bytes_acc(uint32_t x, uint32_t v80, uint32_t acc) {
     const uint32_t t = (x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu;
-    return __popc(~(t | x) & v80);
+#if HYB_ZB_POPC
+    return acc + 128u * (uint32_t)__popc(~(t | x) & v80);
+#else
+    return __dp4a(~(t | x) & v80, 0x01010101u, acc);
+#endif
 }
 
 // Compact growth windows (sparse strips, smax <= 7): a strip with at most `thresh` level-A failures
@@ -489,12 +498,12 @@ __device__ __forceinline__ uint32_t compact_level(const uint4* __restrict__ ea, 
 template <int K>
 __device__ __forceinline__ int count_eq(const uint32_t (&w)[K][Win<K>::AW], uint32_t v) {
     const uint32_t P = v * 0x01010101u;
-    int c = 0;
+    uint32_t c = 0;
 #pragma unroll
     for (int r = 0; r < K; ++r)
 #pragma unroll
-        for (int j = 0; j < Win<K>::AW; ++j) c += zero_bytes(w[r][j] ^ P, Win<K>::v80(j));
-    return c;
+        for (int j = 0; j < Win<K>::AW; ++j) c = zero_bytes_acc(w[r][j] ^ P, Win<K>::v80(j), c);
+    return (int)(c >> 7);
 }
 
 // Element of rank `rank` (0-based): bitwise radix select.  All values lie in [lo, hi], so the
@@ -508,11 +517,12 @@ __device__ __forceinline__ uint32_t select_rank(const uint32_t (&w)[K][Win<K>::A
     for (int b = hb; b >= 0; --b) {
         const uint32_t M = ((0xFFu << b) & 0xFFu) * 0x01010101u;
         const uint32_t P = prefix * 0x01010101u;
-        int c = 0;
+        uint32_t c128 = 0;
 #pragma unroll
         for (int r = 0; r < K; ++r)
 #pragma unroll
-            for (int j = 0; j < Win<K>::AW; ++j) c += zero_bytes((w[r][j] ^ P) & M, Win<K>::v80(j));
+            for (int j = 0; j < Win<K>::AW; ++j) c128 = zero_bytes_acc((w[r][j] ^ P) & M, Win<K>::v80(j), c128);
+        const int c = (int)(c128 >> 7);
         if (below + c <= rank) {
             below += c;
             prefix |= 1u << b;
@@ -976,75 +986,76 @@ __device__ __forceinline__ void box5_counts(const uint32_t (&e)[5][5], uint32_t 
     }
 }
 
-// Level k = 5 for whole tiles at once (thread = one row of one staged tile; geo.CP == 16, BS == 160).
-// bm[sl][128] holds the slot's level-A failures of k = 3 (bitmap words 4 row + q), sinfo[8 sl + 4 / 5] the
-// in-tile rank range of the segment this batch grows; f3m[sl][128] receives
-// the pixels whose k = 5 median is needed (impulse centres that pass level A, and every pixel whose
-// window lacks a 0 or a 255 -- the generic test decides those), bs7[sl][128] the pixels still open.
-// Pixels that pass with a non-impulse centre keep g, which f already holds (FIN: they go through the
-// median pass so finalized_at gets its 5).
-template <int NTHR, bool FIN>
-__device__ __forceinline__ void dense_level5(const uint2* planes, int pstride, const GGeo& geo, int ns,
-                                             const uint32_t* __restrict__ bm, const int* sinfo, uint32_t* f3m,
-                                             uint32_t* bs7) {
+// Level k = 5 for a whole tile at once, one warp per staged tile, lane = tile row (geo.CP == 16, BS == 160).
+// bm[128] holds the tile's level-A failures of k = 3 (bitmap words 4 row + q), [lo, hi) the in-tile rank
+// range of the segment this batch grows.  Returns, for the lane's row, m = the pixels whose k = 5 median
+// is needed (impulse centres that pass level A, and every pixel whose window lacks a 0 or a 255 -- the
+// generic test decides those) and s = the pixels still open.  Pixels that pass with a non-impulse centre
+// keep g, which f already holds (FIN: they go through the median pass so finalized_at gets its 5).
+template <bool FIN>
+__device__ __forceinline__ void dense_level5(const uint2* P0, const GGeo& geo, const uint32_t* __restrict__ bm, int lo,
+                                             int hi, uint4& m, uint4& s) {
     static_assert(TH == 32, "one warp = the rows of one tile");
-    for (int t = threadIdx.x; t < ns * TH; t += NTHR) {
-        const int sl = t / TH, row = t - sl * TH;
-        // the slot's k = 3 failures (bitmap words 4 row + q) whose in-tile rank lies in the segment [lo, hi)
-        uint4 f = reinterpret_cast<const uint4*>(bm + sl * 128)[row];
-        {
-            const int nf = __popc(f.x) + __popc(f.y) + __popc(f.z) + __popc(f.w);
-            int incl = nf;
+    const int row = threadIdx.x & 31;
+    uint4 f = reinterpret_cast<const uint4*>(bm)[row];
+    {
+        const int nf = __popc(f.x) + __popc(f.y) + __popc(f.z) + __popc(f.w);
+        int incl = nf;
 #pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const int v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
-                if (row >= d) incl += v;
-            }
-            int rank = incl - nf;
-            const int lo = sinfo[8 * sl + 4], hi = sinfo[8 * sl + 5];
-            if (rank < lo || incl > hi) {  // the segment boundary crosses this row
-                uint32_t wb[4] = {f.x, f.y, f.z, f.w};
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    uint32_t bits = wb[j], keepw = 0;
-                    while (bits) {
-                        const uint32_t low = bits & (0u - bits);
-                        if (rank >= lo && rank < hi) keepw |= low;
-                        bits ^= low;
-                        ++rank;
-                    }
-                    wb[j] = keepw;
-                }
-                f = make_uint4(wb[0], wb[1], wb[2], wb[3]);
-            }
+        for (int d = 1; d < 32; d <<= 1) {
+            const int v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+            if (row >= d) incl += v;
         }
-        const uint2* P = planes + (size_t)sl * pstride + (row + geo.R - 2) * 5;
-        uint32_t e0[5][5], e1[5][5];
+        int rank = incl - nf;
+        if (rank < lo || incl > hi) {  // the segment boundary crosses this row
+            uint32_t wb[4] = {f.x, f.y, f.z, f.w};
 #pragma unroll
-        for (int i = 0; i < 5; ++i)
-#pragma unroll
-            for (int j = 0; j < 5; ++j) {
-                const uint2 w = P[i * 5 + j];
-                e0[i][j] = w.x;
-                e1[i][j] = w.y;
+            for (int j = 0; j < 4; ++j) {
+                uint32_t bits = wb[j], keepw = 0;
+                while (bits) {
+                    const uint32_t low = bits & (0u - bits);
+                    if (rank >= lo && rank < hi) keepw |= low;
+                    bits ^= low;
+                    ++rank;
+                }
+                wb[j] = keepw;
             }
-        uint32_t le0[5], any0[5], le1[5], any1[5], dm[5], ds[5];
-        box5_counts(e0, le0, any0);
-        box5_counts(e1, le1, any1);
+            f = make_uint4(wb[0], wb[1], wb[2], wb[3]);
+        }
+    }
+    const uint2* P = P0 + (row + geo.R - 2) * 5;
+    uint32_t e0[5][5], e1[5][5];
+#pragma unroll
+    for (int i = 0; i < 5; ++i)
 #pragma unroll
         for (int j = 0; j < 5; ++j) {
-            const uint32_t pass = le0[j] & le1[j], elig = any0[j] & any1[j], ext = e0[2][j] | e1[2][j];
-            dm[j] = FIN ? (~elig | pass) : (~elig | (pass & ext));
-            ds[j] = elig & ~pass;
+            const uint2 w = P[i * 5 + j];
+            e0[i][j] = w.x;
+            e1[i][j] = w.y;
         }
-        uint4* fm = reinterpret_cast<uint4*>(f3m + sl * 128 + 4 * row);
-        // plane bit 16 + c = tile column c
-        *fm = make_uint4(f.x & __funnelshift_r(dm[0], dm[1], 16), f.y & __funnelshift_r(dm[1], dm[2], 16),
-                         f.z & __funnelshift_r(dm[2], dm[3], 16), f.w & __funnelshift_r(dm[3], dm[4], 16));
-        *reinterpret_cast<uint4*>(bs7 + sl * 128 + 4 * row) =
-            make_uint4(f.x & __funnelshift_r(ds[0], ds[1], 16), f.y & __funnelshift_r(ds[1], ds[2], 16),
-                       f.z & __funnelshift_r(ds[2], ds[3], 16), f.w & __funnelshift_r(ds[3], ds[4], 16));
+    uint32_t le0[5], any0[5], le1[5], any1[5], dm[5], ds[5];
+    box5_counts(e0, le0, any0);
+    box5_counts(e1, le1, any1);
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+        const uint32_t pass = le0[j] & le1[j], elig = any0[j] & any1[j], ext = e0[2][j] | e1[2][j];
+        dm[j] = FIN ? (~elig | pass) : (~elig | (pass & ext));
+        ds[j] = elig & ~pass;
     }
+    // plane bit 16 + c = tile column c
+    m = make_uint4(f.x & __funnelshift_r(dm[0], dm[1], 16), f.y & __funnelshift_r(dm[1], dm[2], 16),
+                   f.z & __funnelshift_r(dm[2], dm[3], 16), f.w & __funnelshift_r(dm[3], dm[4], 16));
+    s = make_uint4(f.x & __funnelshift_r(ds[0], ds[1], 16), f.y & __funnelshift_r(ds[1], ds[2], 16),
+                   f.z & __funnelshift_r(ds[2], ds[3], 16), f.w & __funnelshift_r(ds[3], ds[4], 16));
+}
+
+// One whole level K (9 or 11) of one pixel, out of line (the rare flagged pixels of the chained intervals):
+// 0: level A fails; else *out = the result.
+template <int K>
+__device__ __noinline__ int level_radix_full(const uint8_t* __restrict__ B, const GGeo& geo, int ty, int tx, uint8_t* out) {
+    const int st = level_radix_test<K>(B, geo, ty, tx, out);
+    if (st == 2) *out = level_radix_median<K>(B, geo, ty, tx);
+    return st;
 }
 
 // Queues of the fast levels.  Level index l <-> k = 5 + 2 l; |S_k| = qcount[2 l], |M_k| = qcount[2 l + 1].
@@ -1053,7 +1064,9 @@ __device__ __forceinline__ void dense_level5(const uint2* planes, int pstride, c
 constexpr int FAST_FLAG = 0x8000;
 
 // Pass A of level K: plane test of S_K = X[0, nS) -> S_K+2 (front of Y), M_K (tail of Y), or the pixel keeps g.
-template <bool FIN, int NTHR, int CAP, int K, class Slot, class PlaneOf, class Out>
+// CHAIN (K + 2 is the last level): a pixel that fails level K takes the K + 2 test at once, and the front list
+// becomes M_K+2 -- the next interval then runs the median passes of both levels side by side.
+template <bool FIN, int NTHR, int CAP, int K, bool CHAIN, class Slot, class PlaneOf, class Out>
 __device__ __forceinline__ void fast_pass_a(Slot slot, PlaneOf plane, const GGeo& geo, const uint16_t* X, uint16_t* Y,
                                             int nS, int* cSn, int* cM, bool last, int wrot, Out out) {
     constexpr int NWARP = NTHR / 32;
@@ -1070,7 +1083,20 @@ __device__ __forceinline__ void fast_pass_a(Slot slot, PlaneOf plane, const GGeo
                 int c0, c255;
                 plane_counts<(K <= 11 ? K : 11)>(plane(sl), geo, ty, tx, c0, c255);
                 if (c0 > M || c255 > M) {
-                    cls = last ? 0 : 1;
+                    if constexpr (CHAIN && K <= 9) {
+                        constexpr int M2 = ((K + 2) * (K + 2) - 1) / 2;
+                        plane_counts<(K <= 9 ? K + 2 : 11)>(plane(sl), geo, ty, tx, c0, c255);
+                        if (c0 <= M2 && c255 <= M2) {
+                            const uint32_t g = slot(sl)[(size_t)(ty + geo.R) * geo.BS + tx + geo.CP];
+                            if (g != 0u && g != 255u) {
+                                if (FIN) out(sl, pix, (uint8_t)g, K + 2);
+                            } else {
+                                cls = 1;  // front list: M_K+2
+                            }
+                        }
+                    } else {
+                        cls = last ? 0 : 1;
+                    }
                 } else {
                     const uint32_t g = slot(sl)[(size_t)(ty + geo.R) * geo.BS + tx + geo.CP];
                     if (g != 0u && g != 255u) {
@@ -1102,12 +1128,17 @@ __device__ __forceinline__ void fast_pass_a(Slot slot, PlaneOf plane, const GGeo
 
 // Pass B of level K: the median pass over M_K = tail of X, nM entries; flagged pixels that fail the
 // generic level A move to M_K+2 (tail of Y, flagged).
-template <bool FIN, int NTHR, int CAP, int K, int NETMAX, class Slot, class Out>
+// FRONT: the list sits at the front of X instead (entry j at X[j]; see fast_pass_a CHAIN), the warps rotated by wrot.
+// INL (K + 2 is the last level and its median pass runs beside this one): a flagged pixel that fails here takes
+// level K + 2 at once, in its own thread (rare), instead of moving to M_K+2.
+template <bool FIN, int NTHR, int CAP, int K, int NETMAX, bool FRONT, bool INL, class Slot, class Out>
 __device__ __forceinline__ void fast_pass_b(Slot slot, const GGeo& geo, const uint16_t* X, uint16_t* Y, int nM, int* cMn,
-                                            bool last, Out out) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+                                            bool last, int wrot, Out out) {
+    constexpr int NWARP = NTHR / 32;
+    const int lane = threadIdx.x & 31, warp = ((threadIdx.x >> 5) + NWARP - wrot) % NWARP;
     const uint32_t below = (1u << lane) - 1u;
-    const uint16_t* Mq = X + CAP - 1;  // entry j at Mq[-j]
+    const uint16_t* Mq = FRONT ? X : X + CAP - 1;  // entry j at Mq[-j] (FRONT: Mq[j])
+    constexpr int DIR = FRONT ? -1 : 1;
     if constexpr (K <= NETMAX && K <= 9) {
         const int npairs = (nM + 1) >> 1;
         for (int base = warp * 32; base < npairs; base += NTHR) {
@@ -1115,9 +1146,9 @@ __device__ __forceinline__ void fast_pass_b(Slot slot, const GGeo& geo, const ui
             uint32_t keep = 0;
             int ea = 0, eb = 0;
             if (i < npairs) {
-                ea = Mq[-2 * i];
+                ea = Mq[-DIR * 2 * i];
                 const bool hasb = 2 * i + 1 < nM;
-                eb = hasb ? Mq[-(2 * i + 1)] : ea;
+                eb = hasb ? Mq[-DIR * (2 * i + 1)] : ea;
                 const int sa = (ea >> 12) & 7, pa = ea & 4095, sb = (eb >> 12) & 7, pb = eb & 4095;
                 uint32_t done, outw;
                 level_pair2<K>(slot(sa), slot(sb), geo, pa, pb, done, outw);
@@ -1128,7 +1159,16 @@ __device__ __forceinline__ void fast_pass_b(Slot slot, const GGeo& geo, const ui
                     else keep |= 2u;
                 }
             }
-            if (!last) {  // only pixels whose windows lack a 0 or a 255 can fail here
+            if constexpr (INL && (K == 7 || K == 9)) {
+#pragma unroll
+                for (int l = 0; l < 2; ++l) {
+                    if (keep >> l & 1u) {
+                        const int e = l ? eb : ea, sl = (e >> 12) & 7, pix = e & 4095;
+                        uint8_t o = 0;
+                        if (level_radix_full<K + 2>(slot(sl), geo, pix >> 7, pix & 127, &o)) out(sl, pix, o, K + 2);
+                    }
+                }
+            } else if (!last) {  // only pixels whose windows lack a 0 or a 255 can fail here
                 const uint32_t balA = __ballot_sync(0xFFFFFFFFu, keep & 1u);
                 const uint32_t balB = __ballot_sync(0xFFFFFFFFu, keep & 2u);
                 const int c = __popc(balA) + __popc(balB);
@@ -1147,7 +1187,7 @@ __device__ __forceinline__ void fast_pass_b(Slot slot, const GGeo& geo, const ui
             bool keep = false;
             int e = 0;
             if (i < nM) {
-                e = Mq[-i];
+                e = Mq[-DIR * i];
                 const int sl = (e >> 12) & 7, pix = e & 4095, ty = pix >> 7, tx = pix & 127;
                 const uint8_t* B = slot(sl);
                 uint8_t o = 0;
@@ -1157,11 +1197,17 @@ __device__ __forceinline__ void fast_pass_b(Slot slot, const GGeo& geo, const ui
                     if (st == 2) o = level_radix_median<K>(B, geo, ty, tx);
                     if (st) out(sl, pix, o, K);
                     keep = st == 0;
+                    if constexpr (INL && K == 9) {
+                        if (keep) {
+                            if (level_radix_full<11>(B, geo, ty, tx, &o)) out(sl, pix, o, 11);
+                            keep = false;
+                        }
+                    }
                 } else {
                     keep = true;  // generic levels: fast_pass_generic
                 }
             }
-            if (!last) {
+            if (!last && !(INL && K == 9)) {
                 const uint32_t bal = __ballot_sync(0xFFFFFFFFu, keep);
                 if (bal) {
                     int qb = 0;
@@ -1213,6 +1259,7 @@ template <bool FIN, int NTHR, int CAP, class Slot, class PlaneOf, class Out, int
 __device__ __forceinline__ void grow_levels_fast(Slot slot, PlaneOf plane, const GGeo& geo, uint16_t* Q0, uint16_t* Q1,
                                                  int* qcount, int smax, Out out) {
     constexpr int NWARP = NTHR / 32;
+    bool chained = false;  // the previous interval's pass A covered the last two levels: X's front list is M_kA
     for (int i = 0;; ++i) {
         const int kB = 5 + 2 * i, kA = kB + 2;
         if (kB > smax) break;
@@ -1230,23 +1277,38 @@ __device__ __forceinline__ void grow_levels_fast(Slot slot, PlaneOf plane, const
             // S_kB is empty unless this is the first generic level (pass A below routes everything to M)
             fast_pass_generic<NTHR, CAP>(slot, geo, X, Y, 0, nM, cMn, kB, lastB, out);
         } else if (kB == 5) {
-            fast_pass_b<FIN, NTHR, CAP, 5, NETMAX>(slot, geo, X, Y, nM, cMn, lastB, out);
+            fast_pass_b<FIN, NTHR, CAP, 5, NETMAX, false, false>(slot, geo, X, Y, nM, cMn, lastB, 0, out);
         } else if (kB == 7) {
-            fast_pass_b<FIN, NTHR, CAP, 7, NETMAX>(slot, geo, X, Y, nM, cMn, lastB, out);
+            if (chained) fast_pass_b<FIN, NTHR, CAP, 7, NETMAX, false, true>(slot, geo, X, Y, nM, cMn, lastB, 0, out);
+            else fast_pass_b<FIN, NTHR, CAP, 7, NETMAX, false, false>(slot, geo, X, Y, nM, cMn, lastB, 0, out);
         } else if (kB == 9) {
-            fast_pass_b<FIN, NTHR, CAP, 9, NETMAX>(slot, geo, X, Y, nM, cMn, lastB, out);
+            if (chained) fast_pass_b<FIN, NTHR, CAP, 9, NETMAX, false, true>(slot, geo, X, Y, nM, cMn, lastB, 0, out);
+            else fast_pass_b<FIN, NTHR, CAP, 9, NETMAX, false, false>(slot, geo, X, Y, nM, cMn, lastB, 0, out);
         } else {
-            fast_pass_b<FIN, NTHR, CAP, 11, NETMAX>(slot, geo, X, Y, nM, cMn, lastB, out);
+            fast_pass_b<FIN, NTHR, CAP, 11, NETMAX, false, false>(slot, geo, X, Y, nM, cMn, lastB, 0, out);
         }
-        // the warps with one median round fewer start the tests
+        // the warps with one median round fewer start the second pass
         const int per = (kB <= NETMAX && kB <= 9) ? 64 : 32;
         const int wrot = ((nM + per - 1) / per) % NWARP;
-        if (nS > 0) {
-            if (kA == 7) fast_pass_a<FIN, NTHR, CAP, 7>(slot, plane, geo, X, Y, nS, cSn, cMn, lastA, wrot, out);
-            else if (kA == 9) fast_pass_a<FIN, NTHR, CAP, 9>(slot, plane, geo, X, Y, nS, cSn, cMn, lastA, wrot, out);
-            else if (kA == 11) fast_pass_a<FIN, NTHR, CAP, 11>(slot, plane, geo, X, Y, nS, cSn, cMn, lastA, wrot, out);
-            else fast_pass_a<FIN, NTHR, CAP, 13>(slot, plane, geo, X, Y, nS, cSn, cMn, lastA, wrot, out);
+        const bool chain = !chained && kA + 2 == smax && smax <= 11;
+        if (chained) {
+            // kA = smax: the medians of the front list, beside pass B of kB
+            if (kA == 9) fast_pass_b<FIN, NTHR, CAP, 9, NETMAX, true, false>(slot, geo, X, Y, nS, cMn, true, wrot, out);
+            else fast_pass_b<FIN, NTHR, CAP, 11, NETMAX, true, false>(slot, geo, X, Y, nS, cMn, true, wrot, out);
+        } else if (nS > 0) {
+            if (kA == 7) {
+                if (chain) fast_pass_a<FIN, NTHR, CAP, 7, true>(slot, plane, geo, X, Y, nS, cSn, cMn, lastA, wrot, out);
+                else fast_pass_a<FIN, NTHR, CAP, 7, false>(slot, plane, geo, X, Y, nS, cSn, cMn, lastA, wrot, out);
+            } else if (kA == 9) {
+                if (chain) fast_pass_a<FIN, NTHR, CAP, 9, true>(slot, plane, geo, X, Y, nS, cSn, cMn, lastA, wrot, out);
+                else fast_pass_a<FIN, NTHR, CAP, 9, false>(slot, plane, geo, X, Y, nS, cSn, cMn, lastA, wrot, out);
+            } else if (kA == 11) {
+                fast_pass_a<FIN, NTHR, CAP, 11, false>(slot, plane, geo, X, Y, nS, cSn, cMn, lastA, wrot, out);
+            } else {
+                fast_pass_a<FIN, NTHR, CAP, 13, false>(slot, plane, geo, X, Y, nS, cSn, cMn, lastA, wrot, out);
+            }
         }
+        chained = chain;
         __syncthreads();
 #ifdef HYB_TRACE
         // fast-level profile (kernel id 1): slots 5 + i += interval time (pass B of k = 5 + 2 i, pass A of k + 2)
@@ -1256,7 +1318,7 @@ __device__ __forceinline__ void grow_levels_fast(Slot slot, PlaneOf plane, const
             g_trace[(1024 + blockIdx.x) * 16 + 5 + i] += t1 - t_iv;
         }
 #endif
-        if (*cMn == 0 && (lastA || *cSn == 0)) break;
+        if (*cMn == 0 && (lastA || *cSn == 0)) break;  // (after a chained pass A, *cSn = |M_smax|)
     }
 }
 
@@ -1569,20 +1631,16 @@ __device__ __forceinline__ void grow_range(const CUtensorMap* tm, const GGeo& ge
         int n = ctl[1];
         auto slot_out = [&](int sl, int pix, uint8_t v, int k) { out(sinfo + 8 * sl, pix, v, k); };
         if (sm.planes) {
-            uint32_t* f3m = reinterpret_cast<uint32_t*>(Q1);  // [SLOTS][128] failures -> k = 5 medians needed
-            uint32_t* bs7 = f3m + SLOTS * 128;                // [SLOTS][128] still open after k = 5
             build_planes<NTHR>(bufs, geo, sm.planes, sm.pstride, ns);
             __syncthreads();
             GTRACE(9);
-            if (warp < ns) mbar_wait_warp(sm.bmbar + cb, (bmphase >> cb) & 1u);
-            bmphase ^= 1u << cb;
-            dense_level5<NTHR, FIN>(sm.planes, sm.pstride, geo, ns, sm.bms + cb * SLOTS * 128, sinfo, f3m, bs7);
-            __syncthreads();
-            GTRACE(10);
-            // queues from the two bitmaps: S_7 at the front of Q0, M_5 at its tail (slot order as the warps arrive)
+            // warp w: the dense k = 5 pass of slot w, then its queue entries -- S_7 at the front of Q0, M_5 at its
+            // tail (slot order as the warps arrive); the row masks stay in registers
             if (warp < ns) {
-                const uint4 m4 = reinterpret_cast<const uint4*>(f3m + 128 * warp)[lane];
-                const uint4 s4 = reinterpret_cast<const uint4*>(bs7 + 128 * warp)[lane];
+                mbar_wait_warp(sm.bmbar + cb, (bmphase >> cb) & 1u);
+                uint4 m4, s4;
+                dense_level5<FIN>(sm.planes + (size_t)warp * sm.pstride, geo, sm.bms + (cb * SLOTS + warp) * 128,
+                                  sinfo[8 * warp + 4], sinfo[8 * warp + 5], m4, s4);
                 const uint32_t mb[4] = {m4.x, m4.y, m4.z, m4.w}, sb[4] = {s4.x, s4.y, s4.z, s4.w};
                 const int mine = (__popc(s4.x) + __popc(s4.y) + __popc(s4.z) + __popc(s4.w)) |
                                  ((__popc(m4.x) + __popc(m4.y) + __popc(m4.z) + __popc(m4.w)) << 16);
@@ -1618,6 +1676,7 @@ __device__ __forceinline__ void grow_range(const CUtensorMap* tm, const GGeo& ge
                     }
                 }
             }
+            bmphase ^= 1u << cb;
             __syncthreads();
             GTRACE(11);
             auto slot = [&](int sl) { return bufs + (size_t)sl * geo.b_bytes; };

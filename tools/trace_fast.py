@@ -32,10 +32,10 @@ tt = np.frombuffer(buf, dtype=np.uint64).reshape(2, 1024, 16).astype(np.int64)
 t = tt[1]
 t = t[(t[:, 4] > 0)]
 print(f"config {cfg}: AMF call {e0.elapsed_time(e1) * 1e3:.1f} us, {len(t)} growth CTAs, batches/CTA {t[:, 4].mean():.1f}")
-names = {13: "entry", 1: "promote + loads issued", 2: "segment mask", 3: "tile wait + edges", 9: "planes", 10: "dense k=5",
-         11: "queue build", 5: "B(5) | A(7)", 6: "B(7) | A(9)", 7: "B(9) | A(11)", 8: "B(11)"}
+names = {13: "entry", 1: "promote + loads issued", 3: "tile wait + edges", 9: "planes",
+         11: "dense k=5 + queue build", 5: "B(5) | A(7)", 6: "B(7) | A(9 -> 11)", 7: "B(9) | B(11)", 8: "flagged leftovers"}
 tot = 0.0
-for s in (13, 1, 2, 3, 9, 10, 11, 5, 6, 7, 8):
+for s in (13, 1, 3, 9, 11, 5, 6, 7, 8):
     v = t[:, s] / 1e3
     tot += v.mean()
     print(f"{names[s]:24s} per-CTA mean {v.mean():8.1f} us   max {v.max():8.1f}   per batch {1e3 * v.mean() / t[:, 4].mean():7.0f} ns")
