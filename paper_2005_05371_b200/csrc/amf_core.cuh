@@ -582,13 +582,13 @@ __device__ __forceinline__ int level_radix_test(const uint8_t* __restrict__ B, c
 }
 
 // Second pass: the window median by bitwise radix select (values within [zmin, zmax]).
-template <int K>
+template <int K, bool FULL = false>
 __device__ __forceinline__ uint8_t level_radix_median(const uint8_t* __restrict__ B, const GGeo& geo, int ty, int tx) {
     using W = Win<K>;
     uint32_t w[K][W::AW];
     load_window<K>(B, geo, ty, tx, w);
-    uint32_t zmin, zmax;
-    window_minmax<K>(w, zmin, zmax);
+    uint32_t zmin = 0u, zmax = 255u;  // FULL: the window is known to hold a 0 and a 255 (plane tests)
+    if (!FULL) window_minmax<K>(w, zmin, zmax);
     return (uint8_t)select_rank<K>(w, W::M, zmin, zmax);
 }
 
@@ -1192,9 +1192,12 @@ __device__ __forceinline__ void fast_pass_b(Slot slot, const GGeo& geo, const ui
                 const uint8_t* B = slot(sl);
                 uint8_t o = 0;
                 if constexpr (K == 9 || K == 11) {
-                    int st = 2;  // unflagged: level A passed and g is an impulse -> the median
-                    if (e & FAST_FLAG) st = level_radix_test<K>(B, geo, ty, tx, &o);
-                    if (st == 2) o = level_radix_median<K>(B, geo, ty, tx);
+                    int st = 2;  // unflagged: level A passed and g is an impulse -> the median (values span 0..255)
+                    if (e & FAST_FLAG) {
+                        st = level_radix_full<K>(B, geo, ty, tx, &o);
+                    } else {
+                        o = level_radix_median<K, true>(B, geo, ty, tx);
+                    }
                     if (st) out(sl, pix, o, K);
                     keep = st == 0;
                     if constexpr (INL && K == 9) {
