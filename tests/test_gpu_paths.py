@@ -1,5 +1,5 @@
 """Both AMF kernel paths against the oracle, whichever the dispatch picks by default: the two-kernel path
-(amf_k3_kernel + amf_grow_kernel, with and without the impulse-plane test) and the fused per-batch
+(amf_k3_kernel + amf_grow_kernel) and the fused per-batch
 kernel (amf_fused_kernel), forced by HYB_AMF_SPLIT / HYB_AMF_FUSED in a subprocess (the library reads
 them once).  Row ranges, finalized_at, stacks, borders and every smax variant of both."""
 import os

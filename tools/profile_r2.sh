@@ -15,6 +15,9 @@ done
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file $o/launches_config4.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $o/ncu_launch.log 2>&1; echo "launch list rc=$?"
 for c in 1 2 3 4; do
+  if [ $c = 3 ]; then cmd="python tools/batch_dev.py 512 1"; else cmd="python tools/hybrid_dev.py $c 1"; fi  # config 3 = the 512-slice stack
   timeout 900 ncu --set full --import-source on --clock-control none -o $o/full_config$c \
-      python tools/hybrid_dev.py $c 1 > $o/ncu_full_$c.log 2>&1; echo "ncu full config $c rc=$?"
+      $cmd > $o/ncu_full_$c.log 2>&1; echo "ncu full config $c rc=$?"
 done
+timeout 600 python tools/strip_projection.py 2 4 > $o/strip_projection.txt 2>&1; cat $o/strip_projection.txt
+timeout 300 python tools/strip_stages.py 4 > $o/strip_stages.txt 2>&1; tail -12 $o/strip_stages.txt
