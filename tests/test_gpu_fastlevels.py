@@ -56,6 +56,15 @@ for smax in (11, 13, 15):
             f2 = denoise.adaptive_median_rows(gd, smax, a, b)
             assert np.array_equal(f2.cpu().numpy(), oracle.amf(g, smax, a, b)), (smax, name, "range")
             n += 4
+# windows beyond the plane tests and the unrolled selects (generic levels), taller halos
+for smax in (19, 33):
+    for name, g in inputs(150, 200, smax):
+        gd = torch.from_numpy(np.ascontiguousarray(g)).cuda()
+        f, fin = denoise.adaptive_median_rows(gd, smax, 0, 150, finalized_at=True)
+        rf, rfin = oracle.amf(g, smax, finalized_at=True)
+        assert np.array_equal(f.cpu().numpy(), rf), (smax, name)
+        assert np.array_equal(fin.cpu().numpy(), rfin), (smax, name, "fin")
+        n += 1
 # many tiles per CTA: segments of one tile split across batches / CTAs
 g = capi.make_phantom(2100, 4200, 30, 20.0, 0.5, 77)
 gd = torch.from_numpy(g).cuda()
