@@ -282,7 +282,8 @@ struct GrowCfg {
 // With the bit-plane levels (amf_core.cuh grow_levels_fast) the k = 9 medians are few (config 4: ~270 per batch), so
 // the wide variant keeps networks to k = 7 (80 registers) and spends the registers on 12 warps per CTA instead:
 // measured config 4 AMF 1.864 ms (k = 9 network, 256 threads) / 1.860 (radix, 256) / 1.813 (radix, 384); 3 CTAs / SM of
-// 5- or 6-tile batches 2.04 / 2.11 ms -- the pool size matters more than the warps.
+// 5- or 6-tile batches 2.04 / 2.11 ms -- the pool size matters more than the warps.  On the final levels: 384 threads
+// 1.739 ms, 448 (72 registers) 1.747, 512 (64 registers, small spills) 1.793; half the work static 1.751.
 #ifndef HYB_WIDE_NETMAX
 #define HYB_WIDE_NETMAX 7  // largest window the wide variant grows with a selection network
 #endif
