@@ -1058,10 +1058,61 @@ __device__ __noinline__ int level_radix_full(const uint8_t* __restrict__ B, cons
     return st;
 }
 
+// Median of a K x K window known to hold a 0 and a 255, by a pair of lanes (half = lane & 1): each loads half of
+// the window rows and counts its share per radix step, one shuffle adds the two.  The deep levels hold a few
+// hundred pixels per batch; at one pixel per lane they fill a warp or two whose ~1 000-instruction selects the
+// other warps wait for, at one pixel per lane pair the work spreads over twice the warps at half the length.
+// Every lane of the warp must call it (full-mask shuffle); both lanes return the median.
+template <int K>
+__device__ __forceinline__ uint32_t radix_median_pair(const uint8_t* __restrict__ B, const GGeo& geo, int ty, int tx,
+                                                      int half) {
+    using W = Win<K>;
+    constexpr int NR = (K + 1) / 2;  // row slots per lane; the last slot of half 1 lies beyond the window
+    const int start = tx + geo.CP - W::RK;
+    const int sh = 8 * (start & 3);
+    const uint32_t* rowp =
+        reinterpret_cast<const uint32_t*>(B + (size_t)(ty + geo.R - W::RK) * geo.BS) + (start >> 2);
+    uint32_t w[NR][W::AW];
+#pragma unroll
+    for (int s = 0; s < NR; ++s) {
+        const int r = min(half * NR + s, K - 1);
+        uint32_t raw[W::NRAW];
+#pragma unroll
+        for (int j = 0; j < W::NRAW; ++j) raw[j] = rowp[r * (geo.BS >> 2) + j];
+#pragma unroll
+        for (int j = 0; j < W::AW; ++j) w[s][j] = __funnelshift_r(raw[j], (j + 1 < W::NRAW) ? raw[j + 1] : 0u, sh);
+    }
+    const uint32_t lastm = (half * NR + NR - 1 < K) ? 0xFFFFFFFFu : 0u;
+    uint32_t prefix = 0;
+    int below = 0;
+#pragma unroll 1
+    for (int b = 7; b >= 0; --b) {
+        const uint32_t M = ((0xFFu << b) & 0xFFu) * 0x01010101u;
+        const uint32_t P = prefix * 0x01010101u;
+        uint32_t c128 = 0;
+#pragma unroll
+        for (int s = 0; s < NR; ++s)
+#pragma unroll
+            for (int j = 0; j < W::AW; ++j)
+                c128 = zero_bytes_acc((w[s][j] ^ P) & M, s == NR - 1 ? (W::v80(j) & lastm) : W::v80(j), c128);
+        c128 += __shfl_xor_sync(0xFFFFFFFFu, c128, 1);
+        const int c = (int)(c128 >> 7);
+        if (below + c <= W::M) {
+            below += c;
+            prefix |= 1u << b;
+        }
+    }
+    return prefix;
+}
+
 // Queues of the fast levels.  Level index l <-> k = 5 + 2 l; |S_k| = qcount[2 l], |M_k| = qcount[2 l + 1].
 // S_k (open pixels, unflagged, plane-testable) sits at the front of a buffer, M_k (pixels whose level-k
 // median is needed: impulse centres that passed A, and every flagged pixel) at its tail, growing down.
 constexpr int FAST_FLAG = 0x8000;
+#ifndef HYB_FAST_PAIRS
+#define HYB_FAST_PAIRS 0  // 1: the side-by-side deep median passes take one pixel per lane pair (radix_median_pair);
+                          // measured slower, config 4 AMF 1.753 vs 1.739 ms per lane
+#endif
 
 // Pass A of level K: plane test of S_K = X[0, nS) -> S_K+2 (front of Y), M_K (tail of Y), or the pixel keeps g.
 // CHAIN (K + 2 is the last level): a pixel that fails level K takes the K + 2 test at once, and the front list
@@ -1223,6 +1274,37 @@ __device__ __forceinline__ void fast_pass_b(Slot slot, const GGeo& geo, const ui
     }
 }
 
+// Pass B of level K (9 or 11) in the interval where the k = smax - 2 and k = smax median passes run side by side:
+// one pixel per lane pair (radix_median_pair), 16 per warp round.  Nothing is queued here: FRONT (K = smax) is the
+// last level, and a flagged pixel that fails the generic level K = smax - 2 takes level smax at once (out of line).
+template <bool FIN, int NTHR, int CAP, int K, bool FRONT, class Slot, class Out>
+__device__ __forceinline__ void fast_pass_b_pair(Slot slot, const GGeo& geo, const uint16_t* X, int nM, int wrot, Out out) {
+    constexpr int NWARP = NTHR / 32;
+    const int lane = threadIdx.x & 31, warp = ((threadIdx.x >> 5) + NWARP - wrot) % NWARP;
+    const int half = lane & 1;
+    for (int base = warp * 16; base < nM; base += NWARP * 16) {
+        const int idx = base + (lane >> 1);
+        const bool act = idx < nM;
+        const int j = act ? idx : nM - 1;
+        const int e = FRONT ? X[j] : X[CAP - 1 - j];
+        const int sl = (e >> 12) & 7, pix = e & 4095, ty = pix >> 7, tx = pix & 127;
+        const uint8_t* B = slot(sl);
+        const uint32_t med = radix_median_pair<K>(B, geo, ty, tx, half);
+        if (act && half == 0) {
+            if (!(e & FAST_FLAG)) {
+                out(sl, pix, (uint8_t)med, K);
+            } else {
+                uint8_t o = 0;
+                if (level_radix_full<K>(B, geo, ty, tx, &o)) {
+                    out(sl, pix, o, K);
+                } else if constexpr (!FRONT && K == 9) {
+                    if (level_radix_full<11>(B, geo, ty, tx, &o)) out(sl, pix, o, 11);
+                }
+            }
+        }
+    }
+}
+
 // Levels k >= 13 (beyond the plane tests and the unrolled selects): every entry of S_k (front of X) and
 // M_k (tail of X) takes the generic level; failures move to M_k+2 (tail of Y).
 template <int NTHR, int CAP, class Slot, class Out>
@@ -1262,6 +1344,7 @@ template <bool FIN, int NTHR, int CAP, class Slot, class PlaneOf, class Out, int
 __device__ __forceinline__ void grow_levels_fast(Slot slot, PlaneOf plane, const GGeo& geo, uint16_t* Q0, uint16_t* Q1,
                                                  int* qcount, int smax, Out out) {
     constexpr int NWARP = NTHR / 32;
+    constexpr bool PAIRS = HYB_FAST_PAIRS != 0;
     bool chained = false;  // the previous interval's pass A covered the last two levels: X's front list is M_kA
     for (int i = 0;; ++i) {
         const int kB = 5 + 2 * i, kA = kB + 2;
@@ -1285,19 +1368,26 @@ __device__ __forceinline__ void grow_levels_fast(Slot slot, PlaneOf plane, const
             if (chained) fast_pass_b<FIN, NTHR, CAP, 7, NETMAX, false, true>(slot, geo, X, Y, nM, cMn, lastB, 0, out);
             else fast_pass_b<FIN, NTHR, CAP, 7, NETMAX, false, false>(slot, geo, X, Y, nM, cMn, lastB, 0, out);
         } else if (kB == 9) {
-            if (chained) fast_pass_b<FIN, NTHR, CAP, 9, NETMAX, false, true>(slot, geo, X, Y, nM, cMn, lastB, 0, out);
+            if (chained && PAIRS && NETMAX < 9) fast_pass_b_pair<FIN, NTHR, CAP, 9, false>(slot, geo, X, nM, 0, out);
+            else if (chained) fast_pass_b<FIN, NTHR, CAP, 9, NETMAX, false, true>(slot, geo, X, Y, nM, cMn, lastB, 0, out);
             else fast_pass_b<FIN, NTHR, CAP, 9, NETMAX, false, false>(slot, geo, X, Y, nM, cMn, lastB, 0, out);
         } else {
             fast_pass_b<FIN, NTHR, CAP, 11, NETMAX, false, false>(slot, geo, X, Y, nM, cMn, lastB, 0, out);
         }
         // the warps with one median round fewer start the second pass
-        const int per = (kB <= NETMAX && kB <= 9) ? 64 : 32;
+        const int per = (kB <= NETMAX && kB <= 9) ? 64 : (chained && PAIRS && kB == 9) ? 16 : 32;
         const int wrot = ((nM + per - 1) / per) % NWARP;
         const bool chain = !chained && kA + 2 == smax && smax <= 11;
         if (chained) {
             // kA = smax: the medians of the front list, beside pass B of kB
-            if (kA == 9) fast_pass_b<FIN, NTHR, CAP, 9, NETMAX, true, false>(slot, geo, X, Y, nS, cMn, true, wrot, out);
-            else fast_pass_b<FIN, NTHR, CAP, 11, NETMAX, true, false>(slot, geo, X, Y, nS, cMn, true, wrot, out);
+            if (PAIRS && NETMAX < 9) {
+                if (kA == 9) fast_pass_b_pair<FIN, NTHR, CAP, 9, true>(slot, geo, X, nS, wrot, out);
+                else fast_pass_b_pair<FIN, NTHR, CAP, 11, true>(slot, geo, X, nS, wrot, out);
+            } else if (kA == 9) {
+                fast_pass_b<FIN, NTHR, CAP, 9, NETMAX, true, false>(slot, geo, X, Y, nS, cMn, true, wrot, out);
+            } else {
+                fast_pass_b<FIN, NTHR, CAP, 11, NETMAX, true, false>(slot, geo, X, Y, nS, cMn, true, wrot, out);
+            }
         } else if (nS > 0) {
             if (kA == 7) {
                 if (chain) fast_pass_a<FIN, NTHR, CAP, 7, true>(slot, plane, geo, X, Y, nS, cSn, cMn, lastA, wrot, out);

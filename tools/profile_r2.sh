@@ -18,6 +18,11 @@ for c in 1 2 3 4; do
   if [ $c = 3 ]; then cmd="python tools/batch_dev.py 512 1"; else cmd="python tools/hybrid_dev.py $c 1"; fi  # config 3 = the 512-slice stack
   timeout 900 ncu --set full --import-source on --clock-control none -o $o/full_config$c \
       $cmd > $o/ncu_full_$c.log 2>&1; echo "ncu full config $c rc=$?"
+  # summaries are made here (gpurun merges at most 64 MiB back): only config 4's report travels
+  (echo "# ncu --set full --clock-control none, $cmd, tag $tag"; python tools/ncu_report.py $o/full_config$c.ncu-rep) > $o/ncu_full_config$c.txt 2>&1
+  python tools/ncu_counters.py $c $o/full_config$c.ncu-rep > /dev/null 2>&1
+  if [ $c != 4 ]; then rm -f $o/full_config$c.ncu-rep; fi
 done
+cp profiles/ncu_counters.json $o/ncu_counters.json
 timeout 600 python tools/strip_projection.py 2 4 > $o/strip_projection.txt 2>&1; cat $o/strip_projection.txt
 timeout 300 python tools/strip_stages.py 4 > $o/strip_stages.txt 2>&1; tail -12 $o/strip_stages.txt
