@@ -796,8 +796,10 @@ cudaError_t launch_amf(const Plane& p, int smax, uint8_t* fin, size_t fpitch, si
     const bool wide = smax >= HYB_WIDE_MIN_SMAX;
     // zero / 255 bit-plane levels (amf_core.cuh grow_levels_fast) for the wide variant; HYB_GROW_FAST=0: plain levels (A/B)
     static const bool fast_env = !(getenv("HYB_GROW_FAST") && atoi(getenv("HYB_GROW_FAST")) == 0);
-    const bool fast = wide && fast_env && (smax - 1) / 2 <= 16;
-    const size_t gsm = wide ? grow_smem<GrowWide>(geo, fast) : grow_smem<GrowLean>(geo);
+    // HYB_GROW_FAST_LEAN=1: the lean variant too (experiment)
+    static const bool fast_lean = getenv("HYB_GROW_FAST_LEAN") && atoi(getenv("HYB_GROW_FAST_LEAN")) != 0;
+    const bool fast = (wide || fast_lean) && fast_env && (smax - 1) / 2 <= 16;
+    const size_t gsm = wide ? grow_smem<GrowWide>(geo, fast) : grow_smem<GrowLean>(geo, fast);
     auto kern = wide ? (fin ? amf_grow_kernel<true, GrowWide> : amf_grow_kernel<false, GrowWide>)
                      : (fin ? amf_grow_kernel<true, GrowLean> : amf_grow_kernel<false, GrowLean>);
     const int vi = (fin ? 1 : 0) + (wide ? 2 : 0);
