@@ -82,3 +82,11 @@ def test_wide_growth_routes_vs_oracle(fast):
     r = subprocess.run([sys.executable, "-c", SCRIPT], cwd=ROOT, env=e, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert r.stdout.strip().startswith("ok"), r.stdout
+
+
+def test_wide_growth_randomized():
+    """tools/fuzz_wide.py: 250 random shapes / densities / salt-pepper mixes / row ranges at smax 11..17."""
+    r = subprocess.run([sys.executable, "tools/fuzz_wide.py", "250", "99"], cwd=ROOT, capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert r.stdout.strip().startswith("ok"), r.stdout
