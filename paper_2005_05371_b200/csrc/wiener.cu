@@ -227,7 +227,8 @@ cudaError_t launch(const Plane& p, int win, unsigned long long* wsum, const long
 constexpr int FNW = 8;           // warps per CTA
 // Tile rows for images >= 16 MPix (8 below): a tile pays N - 1 prologue rows of box sums, so taller tiles
 // amortise them, at the cost of shared memory per warp.  Measured (W1 ms, config 2 = 5x5 / config 4 = 7x7):
-// 16 rows 0.168 / 0.667, 24 rows 0.160 / 0.682, 32 rows 0.178 / 0.663.
+// 16 rows 0.168 / 0.667, 24 rows 0.160 / 0.682, 32 rows 0.178 / 0.663.  With the four-pixel sums (w1_core.cuh hsums4):
+// 24 rows everywhere 0.146 / 0.617, 32 rows 0.163 / 0.598, the default 0.146 / 0.595; 4 gain CTAs per SM 0.149 / 0.606.
 #ifndef HYB_W1_FH
 #define HYB_W1_FH(RW) ((RW) <= 2 ? 24 : 16)
 #endif
